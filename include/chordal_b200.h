@@ -1,0 +1,150 @@
+/*
+ * chordal_b200.h -- C ABI of libchordal_b200.so, the sm_100a chordality test.
+ *
+ * This is the drop-in boundary for the reference's hot path (arXiv 1508.06329,
+ * package "chordalkit", /root/reference/pkg/src/chordalkit).  The reference is
+ * pure Python; its "FFI" for this path is the set of Python entry points listed
+ * next to each function.  The Python mirror in paper_1508_06329_b200/ binds
+ * these symbols with ctypes (see INTEGRATION.md for the binding a chordalkit
+ * maintainer would add).
+ *
+ * Conventions
+ *  - Vertices are 0-based int32 (the reference is 1-based only at its API
+ *    edge, graph.py:1-7; the Python layer converts).
+ *  - Dense graphs: packed little-endian bit rows exactly like Graph._packed
+ *    (graph.py:78-88: bit j&7 of byte j>>3 of row i <=> edge i-j), with a row
+ *    pitch `stride` in bytes: stride % 16 == 0, stride >= ceil(n/8), padding
+ *    bits zero, base pointer 16-byte aligned.
+ *  - CSR graphs: int64 indptr[n+1], int32 indices (sorted ascending per row,
+ *    symmetric, no self loops) -- the adjacency_lists0() shape (graph.py:152).
+ *  - "_dev" arguments are device pointers; every call is asynchronous on
+ *    `stream` (a cudaStream_t; NULL = legacy default stream) unless the name
+ *    ends in _host.  The library keeps no global mutable state, holds no
+ *    caller pointer after return and is reentrant per stream.
+ *  - Witness triples are int32[3] = (v, p, z) -- WitnessTriple (peo.py:26-45),
+ *    0-based -- or (-1, -1, -1) when the ordering is a PEO.
+ *  - Every function returns a chordal status code (CHORDAL_OK == 0).
+ */
+#ifndef CHORDAL_B200_H
+#define CHORDAL_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CHORDAL_OK 0
+#define CHORDAL_EINVAL 1     /* bad argument (maps to ValueError / InvalidOrdering) */
+#define CHORDAL_ETOOLARGE 2  /* n beyond this kernel's capacity (maps to GraphTooLarge) */
+#define CHORDAL_ECUDA 3      /* CUDA launch/runtime failure */
+#define CHORDAL_ENOMEM 4     /* device allocation failed (host-buffer entry points) */
+
+/* LexBFS tie rules.
+ *  ASCENDING  : max label, ties -> smallest vertex id.  = lexbfs_partition /
+ *               lexbfs_labels with LOWEST_INDEX (search.py:262-310, 500-532,
+ *               _arraylex.py:22-65) = parallel_lexbfs(Arbitration.fixed_priority())
+ *               (parallel/lexbfs.py:234-262).
+ *  DESCENDING : parallel_lexbfs(Arbitration.fixed_priority("descending")):
+ *               starts at vertex 0, ties -> largest id.
+ *  SEEDED_ARB : parallel_lexbfs(Arbitration.seeded(seed)): starts at vertex 0;
+ *               at iteration i the winner among the max-label set is
+ *               argmax_w (splitmix64(prefix_i ^ w), w), w 1-based,
+ *               prefix_i = mix64(seed, 4(i-1)+3, mix64(crc32("current"), 0))
+ *               (parallel/engine.py:47-53, parallel/lexbfs.py:211-225).      */
+#define CHORDAL_TIE_ASCENDING 0
+#define CHORDAL_TIE_DESCENDING 1
+#define CHORDAL_TIE_SEEDED_ARB 2
+
+/* Largest n the single-CTA dense LexBFS kernel accepts (state lives in SMEM). */
+#define CHORDAL_DENSE_LEXBFS_MAX_N 32768
+
+int chordal_abi_version(void);
+const char *chordal_strerror(int status);
+
+/* ---- dense single graph ------------------------------------------------ */
+
+/* LexBFS ordering.  Replaces lexbfs_partition (search.py:500-506),
+ * lexbfs_labels (search.py:262-268) and parallel_lexbfs (parallel/lexbfs.py:
+ * 234-243).  Writes order_dev[n] (vertex at each position) and pos_dev[n]
+ * (position of each vertex).  n <= CHORDAL_DENSE_LEXBFS_MAX_N. */
+int chordal_lexbfs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int32_t tie_rule,
+                         uint64_t seed, int32_t *order_dev, int32_t *pos_dev, void *stream);
+
+/* pos_dev[order_dev[i]] = i  (VertexOrdering.pos0, graph.py:224-230). */
+int chordal_positions(const int32_t *order_dev, int64_t n, int32_t *pos_dev, void *stream);
+
+/* Sets *key_dev = UINT64_MAX (the "no violation" key). */
+int chordal_key_init(uint64_t *key_dev, void *stream);
+
+/* Vertex-parallel PEO check over v in [v_begin, v_end): for each v finds the
+ * parent p (left neighbour with the greatest position, peo.py:106-121) and
+ * tests LN(v)\{p} subset of LN(p) (peo.py:124-142, parallel/peo.py:57-65);
+ * atomically lowers *key_dev to min((p << 32) | v) over violating v.  The
+ * minimum key is the reference's deterministic witness pair (ascending p, then
+ * ascending v, peo.py:81-85).  Row shards of one graph can run on different
+ * GPUs and be combined with an integer MIN all-reduce of the key. */
+int chordal_peo_dense_key(const uint8_t *adj_dev, int64_t n, int64_t stride,
+                          const int32_t *order_dev, const int32_t *pos_dev, int64_t v_begin,
+                          int64_t v_end, uint64_t *key_dev, void *stream);
+
+/* Resolves the key to the witness triple: z = smallest vertex id in
+ * LN(v) \ {p} \ N(p)  (peo.py:126-141 / _first_witness_big peo.py:167-173). */
+int chordal_peo_dense_witness(const uint8_t *adj_dev, int64_t n, int64_t stride,
+                              const int32_t *pos_dev, const uint64_t *key_dev,
+                              int32_t *witness_dev, void *stream);
+
+/* is_peo (peo.py:72-97): key_init + peo_dense_key over all v + witness. */
+int chordal_peo_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, const int32_t *order_dev,
+                      const int32_t *pos_dev, uint64_t *key_dev, int32_t *witness_dev,
+                      void *stream);
+
+/* is_chordal (peo.py:177-202) / parallel_is_chordal (parallel/peo.py:98-114):
+ * LexBFS then the PEO check, all on `stream`. */
+int chordal_is_chordal_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int32_t tie_rule,
+                             uint64_t seed, int32_t *order_dev, int32_t *pos_dev,
+                             uint64_t *key_dev, int32_t *witness_dev, void *stream);
+
+/* Host-buffer form of is_chordal: copies the unpadded packed rows
+ * (row_bytes = ceil(n/8), exactly Graph._packed) to the device, runs the
+ * pipeline, copies order (n int32) and witness back and synchronises.
+ * *chordal_out = 1 chordal / 0 not.  Allocates and frees its own device
+ * memory (stream-ordered). */
+int chordal_is_chordal_dense_host(const uint8_t *adj_host, int64_t n, int64_t row_bytes,
+                                  int32_t tie_rule, uint64_t seed, int32_t *order_host,
+                                  int32_t *witness_host, int32_t *chordal_out);
+
+/* Relabel: out row r, bit s = adj[perm[r]][perm[s]] (perm a 0-based
+ * permutation, out distinct from adj, same stride).  Lets the ascending
+ * kernel replay lexbfs_array with a seeded initial arrangement
+ * (search.py:535-541, _arraylex.py:22-27): order = perm[order_relabelled]. */
+int chordal_permute_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, const int32_t *perm_dev,
+                          uint8_t *out_dev, void *stream);
+
+/* ---- batches of small dense graphs (one warp-resident search per graph) - */
+
+/* Largest n per graph the batched kernel accepts. */
+#define CHORDAL_BATCH_MAX_N 1024
+
+/* is_chordal over `batch` independent graphs of n vertices, graph b at
+ * adj_dev + b * n * stride.  Writes orders_dev[b*n + i] and
+ * witness_dev[3*b + k]; verdict = witness[3*b] < 0.  LOWEST_INDEX ties. */
+int chordal_is_chordal_batch(const uint8_t *adj_dev, int64_t batch, int64_t n, int64_t stride,
+                             int32_t *orders_dev, int32_t *witness_dev, void *stream);
+
+/* ---- synthetic inputs --------------------------------------------------- */
+
+/* gen_dense_random (generate.py:32-56) bit for bit: Philox4x64-10 keyed by
+ * key = mix64(seed, crc32("dense-random")) (rng.py:18-21), uniform doubles
+ * (x >> 11) * 2^-53 drawn row-major over the upper triangle (draw u*n+v
+ * decides edge u<v), mirrored.  Graph b (seed = seed0 + b * seed_step) is
+ * written at adj_dev + b * n * stride; rows are fully overwritten. */
+int chordal_gen_dense_random(uint8_t *adj_dev, int64_t batch, int64_t n, int64_t stride, double p,
+                             int64_t seed0, int64_t seed_step, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* CHORDAL_B200_H */

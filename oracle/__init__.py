@@ -1,0 +1,160 @@
+"""CPU parity oracle for the chordality-test hot path -- TEST INFRASTRUCTURE.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU-baseline
+legs (``cpu_baseline`` and ``--impl reference``) may import this module.  The
+product package ``paper_1508_06329_b200`` never imports it and has no CPU
+fallback.
+
+The C restatement lives in ``chordal_oracle.c`` (each function cites the
+reference file:line it restates); this module loads the compiled
+``_build/liboracle.so`` with ctypes and exposes numpy-level helpers, all
+0-based.  Parity pinning: ``tests/test_oracle_golden.py`` checks every helper
+against fixtures produced by running the reference itself
+(``tests/golden/make_golden.py``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "_build", "liboracle.so")
+_lib = None
+
+
+def build() -> str:
+    """Compile the oracle with the committed Makefile (idempotent)."""
+    cc = "/usr/bin/gcc" if os.path.exists("/usr/bin/gcc") else os.environ.get("CC", "gcc")
+    subprocess.run(["make", "-s", "-C", _HERE, f"CC={cc}"], check=True)
+    return _LIB_PATH
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not os.path.exists(_LIB_PATH) or os.path.getmtime(_LIB_PATH) < os.path.getmtime(
+            os.path.join(_HERE, "chordal_oracle.c")
+        ):
+            build()
+        L = ctypes.CDLL(_LIB_PATH)
+        P = ctypes.c_void_p
+        i64 = ctypes.c_int64
+        L.oracle_lexbfs_partition.argtypes = [P, i64, i64, P, P]
+        L.oracle_lexbfs_partition_csr.argtypes = [P, P, i64, P]
+        L.oracle_lexbfs_array.argtypes = [P, i64, i64, P, P]
+        L.oracle_lexbfs_arbitrated.argtypes = [P, i64, i64, ctypes.c_int, ctypes.c_uint64, P]
+        L.oracle_is_peo.argtypes = [P, i64, i64, P, P]
+        L.oracle_is_peo_csr.argtypes = [P, P, i64, P, P]
+        L.oracle_is_chordal_batch.argtypes = [P, i64, i64, i64, i64, P, P, P, ctypes.c_int]
+        L.oracle_splitmix64.argtypes = [ctypes.c_uint64]
+        L.oracle_splitmix64.restype = ctypes.c_uint64
+        L.oracle_max_threads.restype = ctypes.c_int
+        _lib = L
+    return _lib
+
+
+def _ptr(a: np.ndarray | None):
+    return None if a is None else a.ctypes.data_as(ctypes.c_void_p)
+
+
+def _rows(packed: np.ndarray) -> np.ndarray:
+    return np.ascontiguousarray(packed, dtype=np.uint8)
+
+
+def lexbfs_partition(packed: np.ndarray, n: int, members: np.ndarray | None = None) -> np.ndarray:
+    """lexbfs_partition(method="linked") (search.py:515-532); 0-based order."""
+    rows = _rows(packed)
+    order = np.empty(n, dtype=np.int32)
+    m = None if members is None else np.ascontiguousarray(members, dtype=np.int32)
+    rc = lib().oracle_lexbfs_partition(_ptr(rows), n, rows.shape[1] if n else 0, _ptr(m), _ptr(order))
+    if rc:
+        raise MemoryError("oracle_lexbfs_partition")
+    return order
+
+
+def lexbfs_array(packed: np.ndarray, n: int, initial: np.ndarray | None = None) -> np.ndarray:
+    """lexbfs_array (_arraylex.py:22-65); 0-based order."""
+    rows = _rows(packed)
+    order = np.empty(n, dtype=np.int32)
+    ini = None if initial is None else np.ascontiguousarray(initial, dtype=np.int32)
+    rc = lib().oracle_lexbfs_array(_ptr(rows), n, rows.shape[1] if n else 0, _ptr(ini), _ptr(order))
+    if rc:
+        raise MemoryError("oracle_lexbfs_array")
+    return order
+
+
+ARB_ASCENDING, ARB_DESCENDING, ARB_SEEDED = 0, 1, 2
+
+
+def lexbfs_arbitrated(packed: np.ndarray, n: int, mode: int, seed: int = 0) -> np.ndarray:
+    """parallel_lexbfs election rule (parallel/lexbfs.py:234-262); 0-based."""
+    rows = _rows(packed)
+    order = np.empty(n, dtype=np.int32)
+    rc = lib().oracle_lexbfs_arbitrated(
+        _ptr(rows), n, rows.shape[1] if n else 0, mode, seed & ((1 << 64) - 1), _ptr(order)
+    )
+    if rc:
+        raise MemoryError("oracle_lexbfs_arbitrated")
+    return order
+
+
+def is_peo(packed: np.ndarray, n: int, order0: np.ndarray) -> tuple[bool, tuple[int, int, int] | None]:
+    """is_peo (peo.py:72-149); witness 0-based (v, p, z) or None."""
+    rows = _rows(packed)
+    o = np.ascontiguousarray(order0, dtype=np.int32)
+    w = np.full(3, -1, dtype=np.int32)
+    rc = lib().oracle_is_peo(_ptr(rows), n, rows.shape[1] if n else 0, _ptr(o), _ptr(w))
+    if rc < 0:
+        raise MemoryError("oracle_is_peo")
+    return (True, None) if rc == 1 else (False, (int(w[0]), int(w[1]), int(w[2])))
+
+
+def lexbfs_partition_csr(indptr: np.ndarray, indices: np.ndarray, n: int) -> np.ndarray:
+    ip = np.ascontiguousarray(indptr, dtype=np.int64)
+    ix = np.ascontiguousarray(indices, dtype=np.int32)
+    order = np.empty(n, dtype=np.int32)
+    if lib().oracle_lexbfs_partition_csr(_ptr(ip), _ptr(ix), n, _ptr(order)):
+        raise MemoryError("oracle_lexbfs_partition_csr")
+    return order
+
+
+def is_peo_csr(indptr, indices, n: int, order0) -> tuple[bool, tuple[int, int, int] | None]:
+    ip = np.ascontiguousarray(indptr, dtype=np.int64)
+    ix = np.ascontiguousarray(indices, dtype=np.int32)
+    o = np.ascontiguousarray(order0, dtype=np.int32)
+    w = np.full(3, -1, dtype=np.int32)
+    rc = lib().oracle_is_peo_csr(_ptr(ip), _ptr(ix), n, _ptr(o), _ptr(w))
+    if rc < 0:
+        raise MemoryError("oracle_is_peo_csr")
+    return (True, None) if rc == 1 else (False, (int(w[0]), int(w[1]), int(w[2])))
+
+
+def is_chordal(packed: np.ndarray, n: int):
+    """is_chordal (peo.py:177-202): (chordal, order0, witness0|None)."""
+    order = lexbfs_partition(packed, n)
+    ok, w = is_peo(packed, n, order)
+    return ok, order, w
+
+
+def is_chordal_batch(adj: np.ndarray, n: int, nthreads: int | None = None):
+    """Batch of dense graphs ``adj[b, n, stride]``; returns (verdict, orders, witness)."""
+    a = np.ascontiguousarray(adj, dtype=np.uint8)
+    B = a.shape[0]
+    orders = np.empty((B, n), dtype=np.int32)
+    wit = np.full((B, 3), -1, dtype=np.int32)
+    verdict = np.zeros(B, dtype=np.int32)
+    nt = nthreads or lib().oracle_max_threads()
+    rc = lib().oracle_is_chordal_batch(
+        _ptr(a), B, n, a.shape[2], a.shape[1] * a.shape[2], _ptr(orders), _ptr(wit), _ptr(verdict), nt
+    )
+    if rc:
+        raise MemoryError("oracle_is_chordal_batch")
+    return verdict.astype(bool), orders, wit
+
+
+def max_threads() -> int:
+    return int(lib().oracle_max_threads())

@@ -1,0 +1,92 @@
+"""ctypes binding of libchordal_b200.so (declared in include/chordal_b200.h).
+
+This is the only way the package computes anything: there is no CPU fallback.
+If the shared library is missing the import fails loudly; if CUDA is not
+available a call raises ``DeviceError``.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import DeviceError, GraphTooLarge, InvalidOrdering
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libchordal_b200.so")
+
+OK, EINVAL, ETOOLARGE, ECUDA, ENOMEM = 0, 1, 2, 3, 4
+TIE_ASCENDING, TIE_DESCENDING, TIE_SEEDED_ARB = 0, 1, 2
+DENSE_LEXBFS_MAX_N = 32768
+BATCH_MAX_N = 1024
+
+# name -> argtypes (restype is int unless listed in _RESTYPES)
+_P, _I64, _I32, _U64, _D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double
+SIGNATURES = {
+    "chordal_abi_version": [],
+    "chordal_strerror": [ctypes.c_int],
+    "chordal_lexbfs_dense": [_P, _I64, _I64, _I32, _U64, _P, _P, _P],
+    "chordal_positions": [_P, _I64, _P, _P],
+    "chordal_key_init": [_P, _P],
+    "chordal_peo_dense_key": [_P, _I64, _I64, _P, _P, _I64, _I64, _P, _P],
+    "chordal_peo_dense_witness": [_P, _I64, _I64, _P, _P, _P, _P],
+    "chordal_peo_dense": [_P, _I64, _I64, _P, _P, _P, _P, _P],
+    "chordal_is_chordal_dense": [_P, _I64, _I64, _I32, _U64, _P, _P, _P, _P, _P],
+    "chordal_is_chordal_dense_host": [_P, _I64, _I64, _I32, _U64, _P, _P, _P],
+    "chordal_permute_dense": [_P, _I64, _I64, _P, _P, _P],
+    "chordal_is_chordal_batch": [_P, _I64, _I64, _I64, _P, _P, _P],
+    "chordal_gen_dense_random": [_P, _I64, _I64, _I64, _D, _I64, _I64, _P],
+}
+_RESTYPES = {"chordal_strerror": ctypes.c_char_p}
+
+if not os.path.exists(LIB_PATH):
+    raise ImportError(
+        f"{LIB_PATH} is missing: build it with `python -c 'import __graft_entry__ as g; g.build()'` "
+        "(the package has no CPU fallback)"
+    )
+
+lib = ctypes.CDLL(LIB_PATH)
+for _name, _args in SIGNATURES.items():
+    _fn = getattr(lib, _name)
+    _fn.argtypes = _args
+    _fn.restype = _RESTYPES.get(_name, ctypes.c_int)
+
+
+def exported_symbols() -> list[str]:
+    return list(SIGNATURES)
+
+
+def check(status: int, what: str) -> None:
+    """Map a library status code onto the reference's exception types."""
+    if status == OK:
+        return
+    msg = f"{what}: {lib.chordal_strerror(status).decode()}"
+    if status == EINVAL:
+        raise ValueError(msg)
+    if status == ETOOLARGE:
+        raise GraphTooLarge(msg)
+    if status == ENOMEM:
+        raise MemoryError(msg)
+    raise DeviceError(msg)
+
+
+def require_cuda():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise DeviceError("CUDA device not available: the chordality kernels run only on a GPU")
+    return torch
+
+
+def stream_ptr(stream=None) -> int:
+    import torch
+
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def ptr(t) -> int:
+    return int(t.data_ptr())
+
+
+__all__ = ["lib", "check", "require_cuda", "stream_ptr", "ptr", "InvalidOrdering"]

@@ -1,0 +1,219 @@
+// capi.cu -- extern "C" entry points of libchordal_b200.so (include/chordal_b200.h).
+//
+// Thin validation + launch layer: no global mutable state, no retained caller
+// pointers; every device entry point is asynchronous on the caller's stream.
+#include <cstring>
+
+#include "common.cuh"
+
+namespace chordal {
+int launch_lexbfs_dense(const uint8_t *, int64_t, int64_t, int32_t, uint64_t, uint64_t, int32_t *,
+                        int32_t *, cudaStream_t);
+int launch_positions(const int32_t *, int64_t, int32_t *, cudaStream_t);
+int launch_key_init(uint64_t *, cudaStream_t);
+int launch_peo_dense_key(const uint8_t *, int64_t, int64_t, const int32_t *, const int32_t *, int64_t,
+                         int64_t, uint64_t *, cudaStream_t);
+int launch_peo_dense_witness(const uint8_t *, int64_t, int64_t, const int32_t *, const uint64_t *,
+                             int32_t *, cudaStream_t);
+int launch_permute_dense(const uint8_t *, int64_t, int64_t, const int32_t *, uint8_t *, cudaStream_t);
+int launch_batch(const uint8_t *, int64_t, int64_t, int64_t, int32_t *, int32_t *, cudaStream_t);
+int launch_gen_dense_random(uint8_t *, int64_t, int64_t, int64_t, double, int64_t, int64_t, uint32_t,
+                            cudaStream_t);
+}  // namespace chordal
+
+using namespace chordal;
+
+namespace {
+
+// zlib crc32 (label_hash, _bitops.py:77-79)
+uint32_t crc32_str(const char *s) {
+    uint32_t c = 0xFFFFFFFFu;
+    for (; *s; ++s) {
+        c ^= (uint8_t)*s;
+        for (int k = 0; k < 8; ++k) c = (c >> 1) ^ (0xEDB88320u & (0u - (c & 1u)));
+    }
+    return c ^ 0xFFFFFFFFu;
+}
+
+inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int check_dense(const void *adj, int64_t n, int64_t stride) {
+    if (n < 0) return CHORDAL_EINVAL;
+    if (n == 0) return CHORDAL_OK;
+    if (!adj) return CHORDAL_EINVAL;
+    if (n > 0x7FFFFFFF) return CHORDAL_ETOOLARGE;
+    if (stride % 16 != 0 || stride < (n + 7) / 8) return CHORDAL_EINVAL;
+    if (reinterpret_cast<uintptr_t>(adj) % 16 != 0) return CHORDAL_EINVAL;
+    return CHORDAL_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int chordal_abi_version(void) { return 1; }
+
+const char *chordal_strerror(int status) {
+    switch (status) {
+        case CHORDAL_OK: return "ok";
+        case CHORDAL_EINVAL: return "invalid argument";
+        case CHORDAL_ETOOLARGE: return "graph too large for this kernel";
+        case CHORDAL_ECUDA: return "CUDA error";
+        case CHORDAL_ENOMEM: return "device allocation failed";
+        default: return "unknown status";
+    }
+}
+
+int chordal_lexbfs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int32_t tie_rule,
+                         uint64_t seed, int32_t *order_dev, int32_t *pos_dev, void *stream) {
+    int rc = check_dense(adj_dev, n, stride);
+    if (rc) return rc;
+    if (n == 0) return CHORDAL_OK;
+    if (!order_dev || !pos_dev) return CHORDAL_EINVAL;
+    if (tie_rule < 0 || tie_rule > 2) return CHORDAL_EINVAL;
+    return launch_lexbfs_dense(adj_dev, n, stride, tie_rule, seed, current_cell(crc32_str("current")),
+                               order_dev, pos_dev, as_stream(stream));
+}
+
+int chordal_positions(const int32_t *order_dev, int64_t n, int32_t *pos_dev, void *stream) {
+    if (n < 0 || (n > 0 && (!order_dev || !pos_dev))) return CHORDAL_EINVAL;
+    return launch_positions(order_dev, n, pos_dev, as_stream(stream));
+}
+
+int chordal_key_init(uint64_t *key_dev, void *stream) {
+    if (!key_dev) return CHORDAL_EINVAL;
+    return launch_key_init(key_dev, as_stream(stream));
+}
+
+int chordal_peo_dense_key(const uint8_t *adj_dev, int64_t n, int64_t stride,
+                          const int32_t *order_dev, const int32_t *pos_dev, int64_t v_begin,
+                          int64_t v_end, uint64_t *key_dev, void *stream) {
+    int rc = check_dense(adj_dev, n, stride);
+    if (rc) return rc;
+    if (n == 0) return CHORDAL_OK;
+    if (!order_dev || !pos_dev || !key_dev) return CHORDAL_EINVAL;
+    return launch_peo_dense_key(adj_dev, n, stride, order_dev, pos_dev, v_begin, v_end, key_dev,
+                                as_stream(stream));
+}
+
+int chordal_peo_dense_witness(const uint8_t *adj_dev, int64_t n, int64_t stride,
+                              const int32_t *pos_dev, const uint64_t *key_dev,
+                              int32_t *witness_dev, void *stream) {
+    int rc = check_dense(adj_dev, n, stride);
+    if (rc) return rc;
+    if (!key_dev || !witness_dev) return CHORDAL_EINVAL;
+    if (n == 0) {
+        // empty graph: always a PEO
+        static const int32_t none[3] = {-1, -1, -1};
+        if (cudaMemcpyAsync(witness_dev, none, sizeof(none), cudaMemcpyHostToDevice,
+                            as_stream(stream)) != cudaSuccess)
+            return CHORDAL_ECUDA;
+        return CHORDAL_OK;
+    }
+    if (!pos_dev) return CHORDAL_EINVAL;
+    return launch_peo_dense_witness(adj_dev, n, stride, pos_dev, key_dev, witness_dev,
+                                    as_stream(stream));
+}
+
+int chordal_peo_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, const int32_t *order_dev,
+                      const int32_t *pos_dev, uint64_t *key_dev, int32_t *witness_dev,
+                      void *stream) {
+    int rc = chordal_key_init(key_dev, stream);
+    if (rc) return rc;
+    rc = chordal_peo_dense_key(adj_dev, n, stride, order_dev, pos_dev, 0, n, key_dev, stream);
+    if (rc) return rc;
+    return chordal_peo_dense_witness(adj_dev, n, stride, pos_dev, key_dev, witness_dev, stream);
+}
+
+int chordal_is_chordal_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int32_t tie_rule,
+                             uint64_t seed, int32_t *order_dev, int32_t *pos_dev,
+                             uint64_t *key_dev, int32_t *witness_dev, void *stream) {
+    int rc = chordal_lexbfs_dense(adj_dev, n, stride, tie_rule, seed, order_dev, pos_dev, stream);
+    if (rc) return rc;
+    return chordal_peo_dense(adj_dev, n, stride, order_dev, pos_dev, key_dev, witness_dev, stream);
+}
+
+int chordal_is_chordal_dense_host(const uint8_t *adj_host, int64_t n, int64_t row_bytes,
+                                  int32_t tie_rule, uint64_t seed, int32_t *order_host,
+                                  int32_t *witness_host, int32_t *chordal_out) {
+    if (n < 0 || !witness_host || !chordal_out || (n > 0 && (!adj_host || !order_host)))
+        return CHORDAL_EINVAL;
+    if (n > 0 && row_bytes < (n + 7) / 8) return CHORDAL_EINVAL;
+    if (n == 0) {
+        witness_host[0] = witness_host[1] = witness_host[2] = -1;
+        *chordal_out = 1;
+        return CHORDAL_OK;
+    }
+    const int64_t stride = (((n + 7) / 8) + 15) / 16 * 16;
+    cudaStream_t s;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return CHORDAL_ECUDA;
+    const size_t adj_bytes = (size_t)n * stride;
+    const size_t small = 16 + 12 + 2 * sizeof(int32_t) * (size_t)n;
+    uint8_t *dev = nullptr;
+    int rc = CHORDAL_OK;
+    if (cudaMallocAsync((void **)&dev, adj_bytes + small + 256, s) != cudaSuccess) {
+        cudaStreamDestroy(s);
+        return CHORDAL_ENOMEM;
+    }
+    uint8_t *adj = dev;
+    uint64_t *key = reinterpret_cast<uint64_t *>(dev + ((adj_bytes + 15) & ~size_t(15)));
+    int32_t *wit = reinterpret_cast<int32_t *>(key + 2);
+    int32_t *order = wit + 4;
+    int32_t *pos = order + n;
+    do {
+        if (stride != row_bytes) {
+            if (cudaMemsetAsync(adj, 0, adj_bytes, s) != cudaSuccess) { rc = CHORDAL_ECUDA; break; }
+        }
+        if (cudaMemcpy2DAsync(adj, stride, adj_host, row_bytes, (n + 7) / 8, n,
+                              cudaMemcpyHostToDevice, s) != cudaSuccess) { rc = CHORDAL_ECUDA; break; }
+        rc = chordal_is_chordal_dense(adj, n, stride, tie_rule, seed, order, pos, key, wit, s);
+        if (rc) break;
+        if (cudaMemcpyAsync(order_host, order, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaMemcpyAsync(witness_host, wit, sizeof(int32_t) * 3, cudaMemcpyDeviceToHost, s) != cudaSuccess) {
+            rc = CHORDAL_ECUDA;
+            break;
+        }
+    } while (0);
+    cudaFreeAsync(dev, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess && rc == CHORDAL_OK) rc = CHORDAL_ECUDA;
+    cudaStreamDestroy(s);
+    if (rc == CHORDAL_OK) *chordal_out = witness_host[0] < 0 ? 1 : 0;
+    return rc;
+}
+
+int chordal_permute_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, const int32_t *perm_dev,
+                          uint8_t *out_dev, void *stream) {
+    int rc = check_dense(adj_dev, n, stride);
+    if (rc) return rc;
+    if (n == 0) return CHORDAL_OK;
+    rc = check_dense(out_dev, n, stride);
+    if (rc) return rc;
+    if (!perm_dev || out_dev == adj_dev) return CHORDAL_EINVAL;
+    return launch_permute_dense(adj_dev, n, stride, perm_dev, out_dev, as_stream(stream));
+}
+
+int chordal_is_chordal_batch(const uint8_t *adj_dev, int64_t batch, int64_t n, int64_t stride,
+                             int32_t *orders_dev, int32_t *witness_dev, void *stream) {
+    if (batch < 0 || n < 0) return CHORDAL_EINVAL;
+    if (batch == 0 || n == 0) return CHORDAL_OK;
+    if (n > CHORDAL_BATCH_MAX_N) return CHORDAL_ETOOLARGE;
+    int rc = check_dense(adj_dev, n, stride);
+    if (rc) return rc;
+    if (!orders_dev || !witness_dev) return CHORDAL_EINVAL;
+    return launch_batch(adj_dev, batch, n, stride, orders_dev, witness_dev, as_stream(stream));
+}
+
+int chordal_gen_dense_random(uint8_t *adj_dev, int64_t batch, int64_t n, int64_t stride, double p,
+                             int64_t seed0, int64_t seed_step, void *stream) {
+    if (batch < 0 || n < 0) return CHORDAL_EINVAL;
+    if (batch == 0 || n == 0) return CHORDAL_OK;
+    int rc = check_dense(adj_dev, n, stride);
+    if (rc) return rc;
+    if (!(p > 0.0 && p <= 1.0)) return CHORDAL_EINVAL;
+    if (n == 1) return cudaMemsetAsync(adj_dev, 0, (size_t)batch * stride, as_stream(stream)) == cudaSuccess
+                          ? CHORDAL_OK : CHORDAL_ECUDA;
+    return launch_gen_dense_random(adj_dev, batch, n, stride, p, seed0, seed_step,
+                                   crc32_str("dense-random"), as_stream(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,160 @@
+"""Synthetic inputs of the benchmark configurations, bit-identical to the reference.
+
+These build the *inputs* of the hot path (they are not on it).  Each function
+replays the reference generator's draws from the same named Philox4x64-10
+stream (rng.py:18-21: key = mix64(seed, crc32(label))), so the same seed gives
+the same graph as ``chordalkit.generate`` with the same numpy; the equality is
+pinned by sha256 fixtures in tests/golden/ produced from the reference itself.
+
+``gen_dense_random_device`` draws the identical dense graphs directly in HBM
+(csrc/gen.cu) -- the batched configuration's 65,536 inputs are born on the GPU.
+"""
+
+from __future__ import annotations
+
+import hashlib
+import zlib
+
+import numpy as np
+
+from .errors import InvalidProbability, InvalidSize
+from .graph import Graph, _check_size, row_width
+
+_MASK64 = (1 << 64) - 1
+
+
+def _splitmix64(x: int) -> int:
+    x = (x + 0x9E3779B97F4A7C15) & _MASK64
+    x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & _MASK64
+    x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & _MASK64
+    return x ^ (x >> 31)
+
+
+def stream_key(seed: int, label: str) -> int:
+    """mix64(seed, crc32(label)) -- the Philox key of rng.stream (rng.py:18-21)."""
+    h = _splitmix64(int(seed) & _MASK64)
+    return _splitmix64(h ^ zlib.crc32(label.encode("ascii")))
+
+
+def stream(seed: int, label: str = "") -> np.random.Generator:
+    return np.random.Generator(np.random.Philox(key=stream_key(seed, label)))
+
+
+def gen_clique(n: int, *, cap: int | None = None) -> Graph:
+    """Complete graph K_n (generate.py:18-29)."""
+    if n < 1:
+        raise InvalidSize("clique needs at least one vertex")
+    _check_size(n, cap)
+    bits = np.ones((n, n), dtype=bool)
+    np.fill_diagonal(bits, False)
+    return Graph._from_packed(n, np.packbits(bits, axis=1, bitorder="little"))
+
+
+def gen_dense_random(n: int, p: float, seed: int, *, cap: int | None = None) -> Graph:
+    """G(n, p) with the reference's draw layout (generate.py:32-56), on the host."""
+    if not 0.0 < p <= 1.0:
+        raise InvalidProbability(f"edge probability must be in (0, 1], got {p}")
+    _check_size(n, cap)
+    w = row_width(n)
+    packed = np.zeros((n, w), dtype=np.uint8)
+    if n <= 1:
+        return Graph._from_packed(n, packed)
+    gen = stream(seed, "dense-random")
+    col = np.arange(n, dtype=np.int64)
+    for r0 in range(0, n, 1024):  # 1024-row blocks, one draw per cell, row-major
+        r1 = min(r0 + 1024, n)
+        upper = (gen.random((r1 - r0, n)) < p) & (col[None, :] > np.arange(r0, r1)[:, None])
+        packed[r0:r1] |= np.packbits(upper, axis=1, bitorder="little")[:, :w]
+        lower = np.packbits(upper.T, axis=1, bitorder="little")
+        packed[:, r0 >> 3 : (r0 >> 3) + lower.shape[1]] |= lower
+    return Graph._from_packed(n, packed)
+
+
+def gen_dense_random_device(n: int, p: float, seeds, *, stride: int | None = None, out=None):
+    """The same graphs drawn on the GPU: uint8[B, n, stride] for seeds seed0 + b*step.
+
+    ``seeds`` is ``range``-like (start, step) or an int (one graph).
+    """
+    from . import _native, ops
+    from .graph import device_stride
+
+    torch = _native.require_cuda()
+    if isinstance(seeds, int):
+        seeds = range(seeds, seeds + 1)
+    B = len(seeds)
+    s = stride or device_stride(n)
+    if out is None:
+        out = torch.empty((B, n, s), dtype=torch.uint8, device="cuda")
+    step = seeds.step if B > 1 else 1
+    return ops.gen_dense_random(out, n, s, p, seeds.start, step)
+
+
+def chordal_random_edges(n: int, k: int, seed: int) -> tuple[np.ndarray, np.ndarray]:
+    """0-based edge endpoints of gen_chordal_random (generate.py:118-155).
+
+    Vertex i attaches to a random subset of a random earlier vertex j plus the
+    clique j attached to; the draw sequence (integers(-1,2), integers(0,i),
+    choice(size, want, replace=False)) is replayed call for call.
+    """
+    if n < 1:
+        raise InvalidSize("need at least one vertex")
+    if not 0 <= k < n:
+        raise InvalidSize(f"attachment size must satisfy 0 <= k < n, got {k}")
+    if k == 0 or n == 1:
+        return np.empty(0, dtype=np.int64), np.empty(0, dtype=np.int64)
+    gen = stream(seed, "chordal-random")
+    attached: list[np.ndarray] = [np.empty(0, dtype=np.int64)]
+    heads, tails = [], []
+    for i in range(1, n):
+        if k >= i:
+            chosen = np.arange(i, dtype=np.int64)
+        else:
+            want = int(np.clip(k + gen.integers(-1, 2), 1, i))
+            j = int(gen.integers(0, i))
+            pool = np.append(attached[j], j)
+            chosen = pool if want >= pool.size else pool[gen.choice(pool.size, size=want, replace=False)]
+        attached.append(chosen)
+        heads.append(np.full(chosen.size, i, dtype=np.int64))
+        tails.append(chosen)
+    return np.concatenate(heads), np.concatenate(tails)
+
+
+def gen_chordal_random(n: int, k: int, seed: int, *, cap: int | None = None) -> Graph:
+    """Random chordal graph by clique attachment (generate.py:118-155)."""
+    if n < 1:
+        raise InvalidSize("need at least one vertex")
+    if not 0 <= k < n:
+        raise InvalidSize(f"attachment size must satisfy 0 <= k < n, got {k}")
+    _check_size(n, cap)
+    u, v = chordal_random_edges(n, k, seed)
+    if u.size == 0:
+        return Graph(n, np.zeros((n, row_width(n)), dtype=np.uint8), 0)
+    return Graph._from_numpy_edges(n, u + 1, v + 1)
+
+
+def remove_first_chord(g: Graph) -> tuple[Graph, tuple[int, int] | None]:
+    """Drop the first edge u<v (edges() order) whose endpoints share two
+    non-adjacent common neighbours; the copy then has a chordless 4-cycle.
+
+    The rule that turns the chordal configuration graphs into their
+    non-chordal twins.  Returns (graph, removed 1-based edge).
+    """
+    n = g.n
+    rows = np.unpackbits(np.asarray(g._packed), axis=1, bitorder="little", count=n).astype(bool)
+    for u in range(n):
+        for v in np.flatnonzero(rows[u, u + 1 :]) + u + 1:
+            common = np.flatnonzero(rows[u] & rows[v])
+            if common.size < 2:
+                continue
+            sub = rows[np.ix_(common, common)]
+            if (~sub).sum() > common.size:  # some off-diagonal non-edge
+                packed = np.array(g._packed, copy=True)
+                packed[u, v >> 3] &= np.uint8(0xFF ^ (1 << (v & 7)))
+                packed[v, u >> 3] &= np.uint8(0xFF ^ (1 << (u & 7)))
+                return Graph(n, packed, g.m - 1), (u + 1, int(v) + 1)
+    return g, None
+
+
+def packed_sha256(packed: np.ndarray) -> str:
+    """Fingerprint of the reference layout (n, ceil(n/8)) of a graph."""
+    return hashlib.sha256(np.ascontiguousarray(packed, dtype=np.uint8).tobytes()).hexdigest()

@@ -1,0 +1,141 @@
+"""Device-level operations: thin wrappers over the C ABI on torch tensors.
+
+Every function here launches CUDA work on the current torch stream and
+returns device tensors; the reference-shaped entry points in ``search``,
+``peo`` and ``parallel`` convert to numpy / 1-based types at the edge.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native
+from ._native import check, lib, ptr, stream_ptr
+from .device import DeviceRows
+
+U64_MAX = (1 << 64) - 1
+
+
+def _i32(torch, n, dev):
+    return torch.empty(max(n, 1), dtype=torch.int32, device=dev)
+
+
+def lexbfs(rows: DeviceRows, tie_rule: int = _native.TIE_ASCENDING, seed: int = 0, stream=None):
+    """LexBFS on device rows -> (order int32[n], pos int32[n]) device tensors."""
+    torch = _native.require_cuda()
+    n = rows.n
+    order = _i32(torch, n, rows.data.device)
+    pos = _i32(torch, n, rows.data.device)
+    if n:
+        check(
+            lib.chordal_lexbfs_dense(
+                rows.ptr, n, rows.stride, tie_rule, seed & U64_MAX, ptr(order), ptr(pos), stream_ptr(stream)
+            ),
+            "chordal_lexbfs_dense",
+        )
+    return order[:n], pos[:n]
+
+
+def permute(rows: DeviceRows, perm0: np.ndarray, stream=None) -> DeviceRows:
+    """Relabelled copy: row r, bit s = rows[perm0[r]][perm0[s]]."""
+    torch = _native.require_cuda()
+    p = torch.as_tensor(np.ascontiguousarray(perm0, dtype=np.int32)).to(rows.data.device)
+    out = torch.empty_like(rows.data)
+    check(lib.chordal_permute_dense(rows.ptr, rows.n, rows.stride, ptr(p), ptr(out), stream_ptr(stream)),
+          "chordal_permute_dense")
+    return DeviceRows(rows.n, rows.stride, out)
+
+
+def positions(order, stream=None):
+    torch = _native.require_cuda()
+    n = int(order.numel())
+    pos = _i32(torch, n, order.device)
+    if n:
+        check(lib.chordal_positions(ptr(order), n, ptr(pos), stream_ptr(stream)), "chordal_positions")
+    return pos[:n]
+
+
+def peo(rows: DeviceRows, order, pos, stream=None):
+    """PEO check -> witness int32[3] device tensor ((-1,-1,-1) when a PEO)."""
+    torch = _native.require_cuda()
+    key = torch.empty(1, dtype=torch.int64, device=rows.data.device)
+    wit = torch.empty(4, dtype=torch.int32, device=rows.data.device)
+    check(
+        lib.chordal_peo_dense(rows.ptr, rows.n, rows.stride, ptr(order) if rows.n else None,
+                              ptr(pos) if rows.n else None, ptr(key), ptr(wit), stream_ptr(stream)),
+        "chordal_peo_dense",
+    )
+    return wit[:3]
+
+
+def peo_key(rows: DeviceRows, order, pos, v_begin: int, v_end: int, key, stream=None):
+    """Accumulate the minimum violation key of v in [v_begin, v_end) into ``key`` (int64[1])."""
+    check(
+        lib.chordal_peo_dense_key(rows.ptr, rows.n, rows.stride, ptr(order), ptr(pos), v_begin, v_end,
+                                  ptr(key), stream_ptr(stream)),
+        "chordal_peo_dense_key",
+    )
+
+
+def key_init(key, stream=None):
+    check(lib.chordal_key_init(ptr(key), stream_ptr(stream)), "chordal_key_init")
+
+
+def peo_witness(rows: DeviceRows, pos, key, stream=None):
+    torch = _native.require_cuda()
+    wit = torch.empty(4, dtype=torch.int32, device=rows.data.device)
+    check(
+        lib.chordal_peo_dense_witness(rows.ptr, rows.n, rows.stride, ptr(pos) if rows.n else None, ptr(key),
+                                      ptr(wit), stream_ptr(stream)),
+        "chordal_peo_dense_witness",
+    )
+    return wit[:3]
+
+
+def is_chordal(rows: DeviceRows, tie_rule: int = _native.TIE_ASCENDING, seed: int = 0, stream=None):
+    """Fused pipeline -> (order, pos, witness) device tensors."""
+    torch = _native.require_cuda()
+    n = rows.n
+    dev = rows.data.device
+    order = _i32(torch, n, dev)
+    pos = _i32(torch, n, dev)
+    key = torch.empty(1, dtype=torch.int64, device=dev)
+    wit = torch.empty(4, dtype=torch.int32, device=dev)
+    check(
+        lib.chordal_is_chordal_dense(rows.ptr, n, rows.stride, tie_rule, seed & U64_MAX, ptr(order), ptr(pos),
+                                     ptr(key), ptr(wit), stream_ptr(stream)),
+        "chordal_is_chordal_dense",
+    )
+    return order[:n], pos[:n], wit[:3]
+
+
+def is_chordal_batch(adj, n: int, stride: int, stream=None):
+    """Batched pipeline on adj uint8[B, n, stride] -> (orders int32[B,n], witness int32[B,3])."""
+    torch = _native.require_cuda()
+    B = int(adj.shape[0])
+    orders = torch.empty((max(B, 1), max(n, 1)), dtype=torch.int32, device=adj.device)
+    wit = torch.empty((max(B, 1), 3), dtype=torch.int32, device=adj.device)
+    if B and n:
+        check(
+            lib.chordal_is_chordal_batch(ptr(adj), B, n, stride, ptr(orders), ptr(wit), stream_ptr(stream)),
+            "chordal_is_chordal_batch",
+        )
+    return orders[:B, :n], wit[:B]
+
+
+def gen_dense_random(adj, n: int, stride: int, p: float, seed0: int, seed_step: int = 1, stream=None):
+    """Fill adj uint8[B, n, stride] with gen_dense_random(n, p, seed0 + b*seed_step)."""
+    B = int(adj.shape[0])
+    if B and n:
+        check(
+            lib.chordal_gen_dense_random(ptr(adj), B, n, stride, float(p), int(seed0), int(seed_step),
+                                         stream_ptr(stream)),
+            "chordal_gen_dense_random",
+        )
+    return adj
+
+
+def witness_tuple(w) -> tuple[int, int, int] | None:
+    """Device witness tensor -> 0-based (v, p, z) or None."""
+    a = w.cpu().numpy() if hasattr(w, "cpu") else np.asarray(w)
+    return None if int(a[0]) < 0 else (int(a[0]), int(a[1]), int(a[2]))

@@ -1,0 +1,117 @@
+"""LexBFS orderings -- the reference's ``chordalkit.search`` entry points on the GPU.
+
+``lexbfs_labels`` (search.py:262-310) and ``lexbfs_partition``
+(search.py:500-532) keep their signatures and return types; both run the
+persistent single-CTA kernel of ``csrc/lexbfs_dense.cu``.  Under the default
+``LOWEST_INDEX`` tie-break every reference method ("linked", "array",
+"auto") yields the same order (the reference's own equality tests,
+test_search.py:98-112), and so does this one.
+
+Seeded tie-breaks are method-dependent in the reference:
+``method="array"`` (and "auto" for n >= 1024) breaks ties by a Philox
+permutation of the vertices (search.py:535-541); that is replayed here by
+relabelling the graph on the device with the same permutation and running the
+ascending kernel.  The linked seeded variants (n < 1024 under "auto") draw
+per-step or per-split random choices and are not offered yet.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _native, ops
+from .device import device_rows
+from .errors import GraphTooLarge
+from .graph import VertexOrdering
+
+_ARRAY_MIN_N = 1024  # the reference's auto-dispatch threshold (search.py:29)
+
+
+@dataclass(frozen=True)
+class TieBreak:
+    """How to pick among equally eligible vertices (search.py:32-41)."""
+
+    seed: int | None = None
+
+    def generator(self, label: str):
+        if self.seed is None:
+            return None
+        from .generate import stream
+
+        return stream(self.seed, label)
+
+
+LOWEST_INDEX = TieBreak()
+
+
+def seeded(seed: int) -> TieBreak:
+    return TieBreak(int(seed))
+
+
+@dataclass(frozen=True)
+class LexLabel:
+    """A lexicographic label: digits appended over time, strictly falling (search.py:51-69)."""
+
+    digits: tuple[int, ...] = ()
+
+    def __post_init__(self):
+        d = self.digits
+        if any(b >= a for a, b in zip(d, d[1:])):
+            raise ValueError(f"label digits must strictly descend: {d}")
+
+    def extended(self, digit: int) -> "LexLabel":
+        return LexLabel(self.digits + (digit,))
+
+    def __lt__(self, other: "LexLabel") -> bool:
+        return self.digits < other.digits
+
+    def __le__(self, other: "LexLabel") -> bool:
+        return self.digits <= other.digits
+
+
+def _run_lexbfs(g, tie_break: TieBreak, label: str, method: str) -> VertexOrdering:
+    n = int(g.n)
+    if n == 0:
+        return VertexOrdering(())
+    if n > _native.DENSE_LEXBFS_MAX_N:
+        raise GraphTooLarge(
+            f"n={n} exceeds the dense LexBFS kernel capacity {_native.DENSE_LEXBFS_MAX_N}; use the CSR path"
+        )
+    rows = device_rows(g)
+    if tie_break.seed is None:
+        order, pos = ops.lexbfs(rows, _native.TIE_ASCENDING)
+        return VertexOrdering._trusted(order.cpu().numpy(), pos.cpu().numpy())
+    if method != "array":
+        raise NotImplementedError(
+            "seeded tie-breaks of the linked reference methods (n < 1024 under method='auto') "
+            "are not replayed on the GPU yet; pass method='array'"
+        )
+    initial = np.asarray(tie_break.generator(label).permutation(n), dtype=np.int64)
+    perm = ops.permute(rows, initial)
+    order_r, _ = ops.lexbfs(perm, _native.TIE_ASCENDING)
+    order0 = initial[order_r.cpu().numpy()]
+    return VertexOrdering._trusted(order0)
+
+
+def lexbfs_labels(g, tie_break: TieBreak = LOWEST_INDEX, *, debug: bool = False,
+                  method: str = "auto") -> VertexOrdering:
+    """Lexicographic BFS (label-class formulation, search.py:262-310) on the GPU."""
+    if method not in ("auto", "array", "linked"):
+        raise ValueError(f"unknown method {method!r}")
+    if method == "auto":
+        method = "array" if g.n >= _ARRAY_MIN_N and not debug else "linked"
+    return _run_lexbfs(g, tie_break, "lexbfs-labels", method)
+
+
+def lexbfs_partition(g, tie_break: TieBreak = LOWEST_INDEX, *, method: str = "auto",
+                     _watch=None) -> VertexOrdering:
+    """Lexicographic BFS (partition refinement, search.py:500-532) on the GPU."""
+    if method not in ("auto", "array", "linked"):
+        raise ValueError(f"unknown method {method!r}")
+    if _watch is not None:
+        raise NotImplementedError("_watch observes the CPU PartitionList; the GPU search has none")
+    if method == "auto":
+        method = "array" if g.n >= _ARRAY_MIN_N else "linked"
+    return _run_lexbfs(g, tie_break, "lexbfs-partition", method)

@@ -1,0 +1,52 @@
+"""The C-ABI library loads and exports every symbol include/chordal_b200.h declares.
+
+No compute calls here (this runs without a GPU).
+"""
+
+import ctypes
+import os
+import re
+
+from conftest import ROOT
+
+HEADER = os.path.join(ROOT, "include", "chordal_b200.h")
+
+
+def declared_functions():
+    text = open(HEADER).read()
+    return sorted(set(re.findall(r"^(?:int|const char \*)\s*(chordal_\w+)\s*\(", text, flags=re.M)))
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for must in ("chordal_lexbfs_dense", "chordal_peo_dense", "chordal_is_chordal_dense",
+                 "chordal_is_chordal_dense_host", "chordal_is_chordal_batch", "chordal_peo_dense_key",
+                 "chordal_peo_dense_witness"):
+        assert must in names
+
+
+def test_library_exports_every_declared_symbol():
+    from paper_1508_06329_b200 import _native
+
+    lib = ctypes.CDLL(_native.LIB_PATH)
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+    # and the ctypes binding covers every declared entry point
+    assert set(declared_functions()) <= set(_native.exported_symbols())
+
+
+def test_library_is_sm100a():
+    import subprocess
+
+    from paper_1508_06329_b200 import _native
+
+    out = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "--list-elf", _native.LIB_PATH],
+                         capture_output=True, text=True).stdout
+    assert "sm_100a" in out
+
+
+def test_status_strings():
+    from paper_1508_06329_b200 import _native
+
+    assert _native.lib.chordal_strerror(0) == b"ok"
+    assert _native.lib.chordal_abi_version() == 1

@@ -1,0 +1,312 @@
+"""Parity of the CUDA path (through libchordal_b200.so) with the reference.
+
+Checked against (a) fixtures frozen from the reference itself
+(tests/golden/) and (b) the CPU oracle (oracle/, itself pinned to those
+fixtures by test_oracle_golden.py) on seeded inputs.  Integer / index work:
+everything must be bit-exact -- identical orders, verdicts and witnesses.
+"""
+
+import ctypes
+import hashlib
+import os
+
+import numpy as np
+import pytest
+
+import oracle
+import paper_1508_06329_b200 as P
+from conftest import GOLDEN, exhaustive_graph_packed, load_json, load_npz, named_packed
+from paper_1508_06329_b200 import _native
+from paper_1508_06329_b200.generate import (
+    gen_chordal_random,
+    gen_dense_random,
+    gen_dense_random_device,
+    packed_sha256,
+    remove_first_chord,
+)
+from paper_1508_06329_b200.parallel import Arbitration
+
+pytestmark = pytest.mark.gpu
+
+ASC = Arbitration.fixed_priority()
+DESC = Arbitration.fixed_priority("descending")
+NAMED = load_json("named.json")
+CONFIGS = load_json("configs.json") if os.path.exists(os.path.join(GOLDEN, "configs.json")) else {}
+
+
+def G(packed, n):
+    return P.Graph._from_packed(n, np.array(packed, dtype=np.uint8, copy=True))
+
+
+def o0(ordering):
+    return ordering.order0.tolist()
+
+
+def w0(w):
+    return None if w is None else [w.v - 1, w.p - 1, w.z - 1]
+
+
+def sha(a):
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+# ---------------------------------------------------------------- goldens ----
+
+
+@pytest.mark.parametrize("rec", NAMED["graphs"], ids=[r["name"] for r in NAMED["graphs"]])
+def test_named_goldens(rec):
+    g = G(named_packed(rec), rec["n"])
+    assert o0(P.lexbfs_partition(g)) == rec["lexbfs_partition"]
+    assert o0(P.lexbfs_labels(g)) == rec["lexbfs_labels"]
+    assert o0(P.parallel_lexbfs(g, ASC)) == rec["par_asc"]
+    assert o0(P.parallel_lexbfs(g, DESC)) == rec["par_desc"]
+    for s, o in rec["par_seeded"].items():
+        assert o0(P.parallel_lexbfs(g, Arbitration.seeded(int(s)))) == o
+    v = P.is_chordal(g)
+    assert v.chordal == rec["chordal"] and w0(v.witness) == rec["witness"]
+    if v.chordal:
+        assert o0(v.peo) == rec["lexbfs_partition"]
+    pv = P.parallel_is_chordal(g, Arbitration.seeded(6))
+    assert pv.chordal == rec["par_seeded6_chordal"] and w0(pv.witness) == rec["par_seeded6_witness"]
+
+
+def test_frozen_values_of_the_reference_suite():
+    graphs = {r["name"]: G(named_packed(r), r["n"]) for r in NAMED["graphs"]}
+    c4 = graphs["c4"]
+    assert list(P.lexbfs_partition(c4)) == [1, 2, 4, 3]            # test_search.py:34-39
+    assert list(P.parallel_lexbfs(c4, DESC)) == [1, 4, 2, 3]        # test_parallel_lexbfs.py:54-57
+    ok, w = P.is_peo(c4, P.VertexOrdering([1, 2, 4, 3]))           # test_peo.py:39-43
+    assert not ok and (w.v, w.p, w.z) == (3, 4, 2) and w.verify(c4, P.VertexOrdering([1, 2, 4, 3]))
+    assert list(P.lexbfs_partition(graphs["p3_relabeled"])) == [1, 3, 2]
+    assert list(P.lexbfs_partition(graphs["disconnected6"])) == [1, 3, 2, 5, 6, 4]
+    assert list(P.is_chordal(graphs["clique4"]).peo) == [1, 2, 3, 4]
+    assert P.parallel_peo_test(graphs["star5"], P.VertexOrdering([2, 3, 4, 5, 1])) is False
+    assert P.parallel_peo_test(graphs["star5"], P.VertexOrdering([1, 2, 3, 4, 5])) is True
+
+
+def test_frozen_peo_cases():
+    graphs = {r["name"]: r for r in NAMED["graphs"]}
+    for case in NAMED["peo_cases"]:
+        rec = graphs[case["graph"]]
+        g = G(named_packed(rec), rec["n"])
+        ok, w = P.is_peo(g, P.VertexOrdering.from_zero_based(case["order"]))
+        assert ok == case["ok"] and w0(w) == case["witness"]
+
+
+def test_random_small_goldens(small_corpus):
+    c = small_corpus
+    for i in range(len(c)):
+        n = int(c.ns[i])
+        g = G(c.packed(i), n)
+        assert o0(P.lexbfs_partition(g)) == c.vec("lex", i).tolist(), i
+        assert o0(P.parallel_lexbfs(g, DESC)) == c.vec("par_desc", i).tolist(), i
+        assert o0(P.parallel_lexbfs(g, Arbitration.seeded(i))) == c.vec("par_seeded", i).tolist(), i
+        assert o0(P.lexbfs_partition(g, P.seeded(i), method="array")) == c.vec("seeded_array", i).tolist(), i
+        ok, w = P.is_peo(g, P.VertexOrdering.from_zero_based(c.vec("perm", i)))
+        assert ok == bool(c.z["perm_ok"][i])
+        assert (w0(w) or [-1, -1, -1]) == c.z["perm_witness"][i].tolist(), i
+        v = P.is_chordal(g)
+        assert (w0(v.witness) or [-1, -1, -1]) == c.z["chordal_witness"][i].tolist(), i
+
+
+def test_exhaustive5_single_and_batch():
+    z = load_npz("exhaustive5.npz")
+    for n in range(1, 6):
+        idx = np.flatnonzero(z["n"] == n)
+        graphs = [G(exhaustive_graph_packed(n, int(z["mask"][k])), n) for k in idx]
+        bv = P.is_chordal_batch(graphs)
+        for j, k in enumerate(idx):
+            assert bv.orders0[j].tolist() == z["order"][k][:n].tolist()
+            assert bool(bv.chordal[j]) == bool(z["chordal"][k])
+            assert bv.witness0[j].tolist() == z["witness"][k].tolist()
+        for j in range(0, len(idx), 7):
+            v = P.is_chordal(graphs[j])
+            assert (w0(v.witness) or [-1, -1, -1]) == z["witness"][idx[j]].tolist()
+
+
+# ------------------------------------------------------- oracle, larger n ----
+
+
+def _random_cases():
+    out = []
+    for n, kind, seed in [(100, "dense", 1), (257, "chordal", 2), (500, "dense", 3), (1000, "chordal", 4),
+                          (1000, "sparse", 5), (2048, "chordal", 6), (3000, "dense", 7), (5000, "chordal", 8),
+                          (8191, "sparse", 9)]:
+        if kind == "dense":
+            g = gen_dense_random(n, 0.5, seed)
+        elif kind == "sparse":
+            g = gen_dense_random(n, 4.0 / n, seed)
+        else:
+            g = gen_chordal_random(n, 6, seed)
+        out.append((f"{kind}{n}", g))
+        if kind == "chordal":
+            h, _ = remove_first_chord(g)
+            out.append((f"{kind}{n}-chord", h))
+    return out
+
+
+@pytest.mark.parametrize("name,g", _random_cases(), ids=[c[0] for c in _random_cases()])
+def test_against_oracle(name, g):
+    n = g.n
+    ok, order, w = oracle.is_chordal(g._packed, n)
+    v = P.is_chordal(g)
+    assert v.chordal == ok
+    assert o0(P.lexbfs_partition(g)) == order.tolist()
+    assert w0(v.witness) == (None if w is None else list(w))
+    # arbitrary orderings exercise the parent search's full-row fallback
+    rng = np.random.default_rng(n)
+    perm = rng.permutation(n)
+    ok2, w2 = oracle.is_peo(g._packed, n, perm)
+    okg, wg = P.is_peo(g, P.VertexOrdering.from_zero_based(perm))
+    assert okg == ok2 and w0(wg) == (None if w2 is None else list(w2))
+    assert P.parallel_peo_test(g, P.VertexOrdering.from_zero_based(perm)) is ok2
+    for arb, mode, seed in ((DESC, oracle.ARB_DESCENDING, 0), (Arbitration.seeded(n), oracle.ARB_SEEDED, n)):
+        assert o0(P.parallel_lexbfs(g, arb)) == oracle.lexbfs_arbitrated(g._packed, n, mode, seed).tolist()
+
+
+# ---------------------------------------------------------------- configs ----
+
+
+@pytest.mark.skipif("1" not in CONFIGS, reason="configs.json not generated")
+def test_config1():
+    orders = load_npz("configs_orders.npz")
+    g = gen_chordal_random(1000, 8, 0)
+    h, _ = remove_first_chord(g)
+    for graph, key, okey in ((g, "chordal", "c1_chordal"), (h, "nonchordal", "c1_nonchordal")):
+        exp = CONFIGS["1"][key]
+        v = P.is_chordal(graph)
+        assert v.chordal == exp["chordal"] and w0(v.witness) == exp["witness"]
+        assert o0(P.lexbfs_partition(graph)) == orders[okey].astype(int).tolist()
+    assert w0(P.is_chordal(h).witness) == [1, 873, 2]  # (v=2, p=874, z=3), SURVEY §8d
+
+
+@pytest.mark.skipif("2" not in CONFIGS, reason="configs.json not generated")
+def test_config2():
+    orders = load_npz("configs_orders.npz")
+    d = P.Graph._from_packed(8192, gen_dense_random_device(8192, 0.5, 0)[0, :, :1024].cpu().numpy())
+    assert packed_sha256(d._packed) == CONFIGS["2"]["dense"]["packed_sha256"]
+    c = gen_chordal_random(8192, 8, 0)
+    assert packed_sha256(c._packed) == CONFIGS["2"]["chordal"]["packed_sha256"]
+    for graph, key, okey in ((d, "dense", "c2_dense"), (c, "chordal", "c2_chordal")):
+        exp = CONFIGS["2"][key]
+        v = P.is_chordal(graph)
+        assert v.chordal == exp["chordal"] and w0(v.witness) == exp["witness"]
+        assert o0(P.lexbfs_partition(graph)) == orders[okey].astype(int).tolist()
+
+
+@pytest.mark.skipif("3" not in CONFIGS, reason="configs.json not generated")
+def test_config3_dense_stressor():
+    exp = CONFIGS["3"]["dense"]
+    adj = gen_dense_random_device(32768, 0.5, 0)
+    d = P.Graph._from_packed(32768, adj[0].cpu().numpy())
+    assert packed_sha256(d._packed) == exp["packed_sha256"]
+    v = P.is_chordal(d)
+    assert v.chordal == exp["chordal"] and w0(v.witness) == exp["witness"]
+    assert sha(P.lexbfs_partition(d).order0.astype(np.int32)) == exp["order_sha256"]
+
+
+@pytest.mark.slow
+@pytest.mark.skipif("3" not in CONFIGS, reason="configs.json not generated")
+def test_config3_chordal_pair():
+    g = gen_chordal_random(32768, 1024, 0, cap=32768)
+    exp = CONFIGS["3"]["chordal"]
+    assert packed_sha256(g._packed) == exp["packed_sha256"]
+    v = P.is_chordal(g)
+    assert v.chordal and sha(v.peo.order0.astype(np.int32)) == exp["order_sha256"]
+    h, e = remove_first_chord(g)
+    expn = CONFIGS["3"]["nonchordal"]
+    assert list(e) == expn["removed_edge"]
+    vn = P.is_chordal(h)
+    assert not vn.chordal and w0(vn.witness) == expn["witness"]  # (v=2, p=3600, z=3)
+    assert sha(P.lexbfs_partition(h).order0.astype(np.int32)) == expn["order_sha256"]
+
+
+@pytest.mark.skipif("4" not in CONFIGS, reason="configs.json not generated")
+def test_config4_sample_batch():
+    sample = CONFIGS["4"]["sample"]
+    graphs = [gen_dense_random(512, 0.5, r["seed"]) if r["seed"] % 2 == 0 else gen_chordal_random(512, 8, r["seed"])
+              for r in sample]
+    bv = P.is_chordal_batch(graphs)
+    for b, r in enumerate(sample):
+        assert sha(bv.orders0[b].astype(np.int32)) == r["order_sha256"]
+        assert bool(bv.chordal[b]) == r["chordal"]
+        assert (None if bv.chordal[b] else bv.witness0[b].tolist()) == r["witness"]
+
+
+def test_batch_against_oracle_mixed_sizes():
+    for n in (17, 64, 100, 512, 700, 1024):
+        gs = [gen_dense_random(n, [0.05, 0.5, 0.9][s % 3], s) if s % 2 == 0 else gen_chordal_random(n, 5, s)
+              for s in range(24)]
+        gs += [remove_first_chord(gen_chordal_random(n, 5, 100 + s))[0] for s in range(8)]
+        bv = P.is_chordal_batch(gs)
+        verdict, orders, wit = oracle.is_chordal_batch(np.stack([g._packed for g in gs]), n)
+        assert (bv.chordal == verdict).all()
+        assert (bv.orders0 == orders).all()
+        assert (bv.witness0 == wit).all()
+
+
+# ------------------------------------------------------- inputs and e2e ----
+
+
+def test_device_dense_generator_bit_exact():
+    for n, p, seeds in ((512, 0.5, range(0, 8, 2)), (1000, 0.3, range(3, 5)), (33, 0.7, range(1)), (2, 1.0, range(1))):
+        adj = gen_dense_random_device(n, p, seeds).cpu().numpy()
+        w = (n + 7) // 8
+        for b, s in enumerate(seeds):
+            ref = gen_dense_random(n, p, s)._packed
+            assert (adj[b, :, :w] == ref).all(), (n, s)
+            assert not adj[b, :, w:].any()
+
+
+def test_host_buffer_entry_point():
+    for g in (gen_chordal_random(1000, 8, 0), remove_first_chord(gen_chordal_random(1000, 8, 0))[0],
+              gen_dense_random(777, 0.5, 1)):
+        n = g.n
+        order = np.empty(n, dtype=np.int32)
+        wit = np.empty(3, dtype=np.int32)
+        chordal = ctypes.c_int32(-1)
+        packed = np.ascontiguousarray(g._packed)
+        rc = _native.lib.chordal_is_chordal_dense_host(
+            packed.ctypes.data, n, packed.shape[1], 0, 0, order.ctypes.data, wit.ctypes.data, ctypes.byref(chordal))
+        assert rc == 0
+        ok, o, w = oracle.is_chordal(packed, n)
+        assert bool(chordal.value) == ok and order.tolist() == o.tolist()
+        assert (wit.tolist() if not ok else None) == (None if w is None else list(w))
+
+
+def test_reference_graph_objects_are_accepted():
+    """Any object with n and _packed (e.g. a chordalkit.Graph) is a valid input."""
+
+    class Foreign:
+        __slots__ = ("n", "_packed", "m")
+
+        def __init__(self, g):
+            self.n, self._packed, self.m = g.n, g._packed, g.m
+
+        def has_edge(self, u, v):
+            return bool((self._packed[u - 1, (v - 1) >> 3] >> ((v - 1) & 7)) & 1)
+
+    g = remove_first_chord(gen_chordal_random(300, 5, 1))[0]
+    f = Foreign(g)
+    v = P.is_chordal(f)
+    assert not v.chordal and v.witness.verify(f, P.lexbfs_partition(f))
+    assert w0(v.witness) == w0(P.is_chordal(g).witness)
+
+
+def test_edge_cases():
+    e0 = P.Graph.from_edge_list(0, [])
+    v = P.is_chordal(e0)
+    assert v.chordal and list(v.peo) == []
+    assert P.is_peo(e0, P.VertexOrdering([])) == (True, None)
+    assert list(P.is_chordal(P.Graph.from_edge_list(1, [])).peo) == [1]
+    assert list(P.parallel_lexbfs(P.Graph.from_edge_list(2, [(1, 2)]), ASC)) == [1, 2]
+    big = P.Graph.from_edge_list(32768, [], cap=32768)
+    assert o0(P.lexbfs_partition(big)) == list(range(32768))
+    assert o0(P.parallel_lexbfs(big, DESC)) == [0] + list(range(32767, 0, -1))
+    star = P.Graph.from_edge_list(32768, [(1, k) for k in range(2, 32769)], cap=32768)
+    v = P.is_chordal(star)
+    assert v.chordal and o0(v.peo) == list(range(32768))
+    with pytest.raises(P.GraphTooLarge):
+        P.lexbfs_partition(P.Graph.from_edge_list(32769, [], cap=40000))
+    with pytest.raises(P.GraphTooLarge):
+        P.is_chordal_batch([P.Graph.from_edge_list(1025, [])])
