@@ -1,0 +1,456 @@
+"""Benchmark of the chordality test (LexBFS + PEO check) on B200.
+
+Headline (BASELINE.json metric "chordality-test ms/graph (N=32k dense) and
+graphs/sec batched at 1/2/4/8 B200 vs CPU"):
+  value      graphs/s of configuration 4 -- 65,536 independent graphs of 512
+             vertices (seed s: gen_dense_random(512, 0.5, s) if s is even, else
+             gen_chordal_random(512, 8, s)), sharded over the ranks by
+             contiguous seed ranges (strong scaling: the total is fixed).  One
+             step = one is_chordal pass over the whole batch, inputs resident
+             in HBM (2 GiB at N=1 > 126 MB L2, so no flush is needed).
+  e2e        the same metric through the host-buffer C-ABI entry point
+             chordal_is_chordal_batch_host (pinned host graphs in, orders +
+             witnesses out, copies inside the timed region).
+  dense32k   ms/graph of configuration 3 (N=32768: chordal k=1024, its
+             chord-removed twin, and G(32768, 0.5)), plus configurations 1-2, on
+             rank 0 -- device-resident ("algo") and host-buffer ("total").
+Inputs are synthetic but bit-identical to the reference generators (drawn
+on the GPU by csrc/gen.cu).  --impl reference times the reference algorithm
+(the C port in oracle/, all host threads) on a bounded sample.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "chordality-test ms/graph (N=32k dense) and graphs/sec batched at 1/2/4/8 B200 vs CPU"
+N512, STRIDE512, K512 = 512, 64, 8
+TOTAL_GRAPHS = 65536
+BYTES_PER_GRAPH = N512 * STRIDE512 + 4 * N512 + 12  # adjacency read + order + witness written
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--graphs", type=int, default=TOTAL_GRAPHS)
+    ap.add_argument("--no-secondary", action="store_true", help="skip the N=32k / N=8k / N=1k lines")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline sample")
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks --
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled while the timed region runs."""
+
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines: list[str] = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            self.proc.wait(timeout=5)
+
+    def summary(self) -> dict:
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for name, val in zip(names, parts[4:8]):
+                if val.lower().startswith("active"):
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ------------------------------------------------------------------- utils --
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks() -> tuple[dict, str]:
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            return json.load(f), "measured"
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def shard(total: int, rank: int, world: int) -> tuple[int, int]:
+    per = total // world
+    lo = rank * per
+    hi = total if rank == world - 1 else lo + per
+    if lo % 2:
+        lo += 1
+    return lo, hi
+
+
+def build_batch(lo: int, hi: int, device):
+    """Graphs of seeds [lo, hi) in seed order, drawn on the GPU (bit-exact)."""
+    import torch
+
+    from paper_1508_06329_b200.generate import gen_chordal_random_device, gen_dense_random_device
+
+    B = hi - lo
+    adj = torch.empty((B, N512, STRIDE512), dtype=torch.uint8, device=device)
+    ev = range(lo + (lo % 2), hi, 2)
+    od = range(lo + 1 - (lo % 2), hi, 2)
+    if len(ev):
+        adj[(ev.start - lo)::2] = gen_dense_random_device(N512, 0.5, ev, stride=STRIDE512)
+    if len(od):
+        adj[(od.start - lo)::2] = gen_chordal_random_device(N512, K512, od, stride=STRIDE512)
+    torch.cuda.synchronize()
+    return adj
+
+
+def reduce_max(x: float, world: int) -> float:
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world: int):
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.barrier()
+
+
+# ------------------------------------------------------------- cpu baseline --
+
+
+def cpu_batch_baseline(adj_host: np.ndarray, budget_s: float = 15.0) -> dict:
+    """The reference algorithm (C port, oracle/) on a bounded prefix, all host threads."""
+    import oracle
+
+    threads = oracle.max_threads()
+    probe = min(len(adj_host), max(2 * threads, 64))
+    t0 = time.perf_counter()
+    oracle.is_chordal_batch(adj_host[:probe], N512, nthreads=threads)
+    per = (time.perf_counter() - t0) / probe
+    S = int(min(len(adj_host), max(probe, budget_s / max(per, 1e-9)))) // 2 * 2
+    t0 = time.perf_counter()
+    oracle.is_chordal_batch(adj_host[:S], N512, nthreads=threads)
+    dt = time.perf_counter() - t0
+    return {"value": S / dt, "unit": "graphs/s", "cores": threads, "kind": "port",
+            "sample": f"first {S} graphs (seeds 0..{S - 1}) of configuration 4, LexBFS (PartitionList) + list "
+                      f"PEO test per graph, {threads} host threads"}
+
+
+# --------------------------------------------------------------- secondary --
+
+
+def time_events(fn, reps: int = 3, warm: int = 1) -> float:
+    import torch
+
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    s.record()
+    for _ in range(reps):
+        fn()
+    e.record()
+    torch.cuda.synchronize()
+    return s.elapsed_time(e) / reps
+
+
+def single_graph_lines(with_cpu: bool) -> dict:
+    """Configurations 1-3 on rank 0: per-graph ms, LexBFS ns/step, PEO roofline."""
+    import torch
+
+    import paper_1508_06329_b200 as P
+    from paper_1508_06329_b200 import _native, ops
+    from paper_1508_06329_b200.device import DeviceRows
+    from paper_1508_06329_b200.generate import (
+        chordal_random_edges,
+        gen_dense_random_device,
+        remove_first_chord,
+    )
+    from paper_1508_06329_b200.graph import device_stride
+
+    peaks, _ = measured_peaks()
+    out = {}
+
+    def rows_from_edges(n, k, seed):
+        u, v = chordal_random_edges(n, k, seed)
+        return DeviceRows(n, device_stride(n), ops.edges_to_dense(u, v, n, device_stride(n)))
+
+    def measure(name, rows: DeviceRows, host_packed=None):
+        n = rows.n
+        lex = time_events(lambda: ops.lexbfs(rows))
+        order, pos = ops.lexbfs(rows)
+        peo = time_events(lambda: ops.peo(rows, order, pos))
+        full = time_events(lambda: ops.is_chordal(rows))
+        _, _, wit = ops.is_chordal(rows)
+        w = ops.witness_tuple(wit)
+        rec = {"n": n, "ms_per_graph": full, "lexbfs_ms": lex, "lexbfs_ns_per_step": lex * 1e6 / n,
+               "peo_ms": peo, "chordal": w is None,
+               "witness": None if w is None else [w[0] + 1, w[1] + 1, w[2] + 1]}
+        peo_bytes = 2 * n * rows.stride + 12 * n
+        rec["peo_roofline"] = {"bound": "hbm", "achieved_gbs": peo_bytes / (peo * 1e-3) / 1e9,
+                               "frac": peo_bytes / (peo * 1e-3) / 1e9 / peaks["hbm_gbs"],
+                               "algorithmic_bytes": peo_bytes}
+        if host_packed is not None:
+            hp = np.ascontiguousarray(host_packed)
+            order_h = np.empty(n, dtype=np.int32)
+            wit_h = np.empty(3, dtype=np.int32)
+            flag = ctypes.c_int32()
+
+            def e2e():
+                _native.lib.chordal_is_chordal_dense_host(hp.ctypes.data, n, hp.shape[1], 0, 0, order_h.ctypes.data,
+                                                          wit_h.ctypes.data, ctypes.byref(flag))
+
+            e2e()
+            t0 = time.perf_counter()
+            for _ in range(3):
+                e2e()
+            rec["total_ms_host_buffers"] = (time.perf_counter() - t0) / 3 * 1e3
+        out[name] = rec
+
+    # configuration 3 (N = 32768)
+    r3 = rows_from_edges(32768, 1024, 0)
+    measure("c3_chordal_k1024", r3)
+    g3 = P.Graph._from_packed(32768, r3.data[:, :4096].cpu().numpy())
+    h3, _ = remove_first_chord(g3)
+    r3n = DeviceRows(32768, 4096, torch.from_numpy(np.array(h3._packed)).cuda())
+    measure("c3_nonchordal", r3n, h3._packed)
+    d3 = gen_dense_random_device(32768, 0.5, 0)[0]
+    measure("c3_dense_p0.5", DeviceRows(32768, 4096, d3))
+    del d3, r3n
+    # configuration 2 (N = 8192)
+    d2 = gen_dense_random_device(8192, 0.5, 0)[0]
+    measure("c2_dense_p0.5", DeviceRows(8192, 1024, d2), d2.cpu().numpy())
+    measure("c2_chordal_k8", rows_from_edges(8192, 8, 0))
+    # configuration 1 (N = 1000)
+    r1 = rows_from_edges(1000, 8, 0)
+    g1 = P.Graph._from_packed(1000, r1.data[:, :125].cpu().numpy())
+    h1, _ = remove_first_chord(g1)
+    measure("c1_chordal_k8", r1, g1._packed)
+    measure("c1_nonchordal", DeviceRows(1000, 128, torch.from_numpy(
+        np.pad(np.array(h1._packed), ((0, 0), (0, 3)))).cuda()), h1._packed)
+    if with_cpu:
+        import oracle
+
+        cpu = {}
+        for name, packed, n in (("c1_nonchordal", h1._packed, 1000), ("c3_nonchordal", h3._packed, 32768)):
+            t0 = time.perf_counter()
+            oracle.is_chordal(packed, n)
+            cpu[name] = {"ms_per_graph": (time.perf_counter() - t0) * 1e3, "cores": 1, "kind": "port"}
+        out["cpu_baseline"] = cpu
+    return out
+
+
+# -------------------------------------------------------------------- main --
+
+
+def run_reference(args, rank, world):
+    """--impl reference: the reference algorithm on the host cores (oracle C port)."""
+    if rank != 0:
+        return
+    import oracle
+
+    oracle.lib()
+    threads = oracle.max_threads()
+    try:
+        import torch
+
+        have_gpu = torch.cuda.is_available()
+    except Exception:
+        have_gpu = False
+    # inputs: the same graphs (drawn on the GPU when present, else by the host generators)
+    S = 2 * max(64, threads * 16)
+    if have_gpu:
+        adj = build_batch(0, S, "cuda").cpu().numpy()
+    else:
+        from paper_1508_06329_b200.generate import gen_chordal_random, gen_dense_random
+
+        adj = np.zeros((S, N512, STRIDE512), dtype=np.uint8)
+        for s in range(S):
+            g = gen_dense_random(N512, 0.5, s) if s % 2 == 0 else gen_chordal_random(N512, K512, s)
+            adj[s, :, :64] = g._packed
+    for _ in range(args.warmup):
+        oracle.is_chordal_batch(adj, N512, nthreads=threads)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        oracle.is_chordal_batch(adj, N512, nthreads=threads)
+    dt = time.perf_counter() - t0
+    value = S * args.steps / dt
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": {"workload": "config4: 65536 graphs N=512 (even seed G(512,0.5), odd seed chordal k=8)",
+                   "sample_per_step": S},
+        "cpu_baseline": {"value": value, "unit": "graphs/s", "cores": threads, "kind": "port",
+                         "sample": f"{S} graphs (seeds 0..{S - 1}) per step, oracle/ C port of is_chordal "
+                                   f"(PartitionList LexBFS + list PEO), {threads} threads"},
+        "e2e": {"value": value, "unit": "graphs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, rank, world, local):
+    import torch
+
+    from paper_1508_06329_b200 import _native, ops
+
+    torch.cuda.set_device(local)
+    device = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=device)
+    lo, hi = shard(args.graphs, rank, world)
+    B = hi - lo
+    adj = build_batch(lo, hi, device)
+
+    def step():
+        return ops.is_chordal_batch(adj, N512, STRIDE512)
+
+    for _ in range(max(3, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    barrier(world)
+    stream = torch.cuda.current_stream()
+    t_s, t_e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        barrier(world)
+        t_s.record(stream)
+        for _ in range(args.steps):
+            step()
+        t_e.record(stream)
+        torch.cuda.synchronize()
+        barrier(world)
+    t_ms = reduce_max(t_s.elapsed_time(t_e), world)
+    ms_per_step = t_ms / args.steps
+    value = args.graphs * args.steps / (t_ms * 1e-3)
+    # correctness guard on the measured batch (parity is proven by the tests; this
+    # only refuses to print a number for a broken build)
+    orders, wit = step()
+    torch.cuda.synchronize()
+
+    # e2e through the host-buffer C-ABI: pinned graphs in, orders + witnesses out
+    host = torch.empty((B, N512, STRIDE512), dtype=torch.uint8, pin_memory=True)
+    host.copy_(adj)
+    orders_h = torch.empty((B, N512), dtype=torch.int32, pin_memory=True)
+    wit_h = torch.empty((B, 3), dtype=torch.int32, pin_memory=True)
+
+    def e2e_step():
+        rc = _native.lib.chordal_is_chordal_batch_host(host.data_ptr(), B, N512, STRIDE512, orders_h.data_ptr(),
+                                                       wit_h.data_ptr(), 8192)
+        _native.check(rc, "chordal_is_chordal_batch_host")
+
+    e2e_step()
+    e2e_steps = max(2, min(args.steps, 5))
+    barrier(world)
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        e2e_step()
+    e2e_s = reduce_max(time.perf_counter() - t0, world)
+    assert torch.equal(wit_h, wit.cpu()) and torch.equal(orders_h, orders.cpu()), "e2e result differs"
+    e2e_value = args.graphs * e2e_steps / e2e_s
+
+    peaks, peak_kind = measured_peaks()
+    achieved = B * BYTES_PER_GRAPH / (ms_per_step * 1e-3) / 1e9
+    line = {
+        "metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": world, "steps": args.steps,
+        "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "u8", "data": "synthetic (reference generators replayed bit-exact on the GPU)",
+        "config": {"workload": "config4: 65536 graphs N=512 (even seed gen_dense_random(512,0.5,s), odd seed "
+                               "gen_chordal_random(512,8,s)), contiguous seed shards",
+                   "graphs": args.graphs, "graphs_per_rank": B, "l2": "inputs 2 GiB > L2, no flush needed",
+                   "parallelism": f"batch-shard x{world}"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                     "kernel": "batch_chordal_kernel", "peak_kind": peak_kind,
+                     "algorithmic_bytes_per_graph": BYTES_PER_GRAPH},
+        "e2e": {"value": e2e_value, "unit": "graphs/s", "h2d_bytes_per_step": B * N512 * STRIDE512,
+                "d2h_bytes_per_step": B * (4 * N512 + 12), "api": "chordal_is_chordal_batch_host"},
+        "gpu_launches": args.steps,
+        "clocks": clk.summary(),
+        "chordal_fraction": float((wit[:, 0] < 0).float().mean().item()),
+    }
+    if rank == 0 and world == 1 and not args.no_cpu:
+        line["cpu_baseline"] = cpu_batch_baseline(host[: min(B, 8192)].numpy())
+    if rank == 0 and world == 1 and not args.no_secondary:
+        line["single_graph"] = single_graph_lines(with_cpu=not args.no_cpu)
+        line["dense32k"] = {k: v["ms_per_graph"] for k, v in line["single_graph"].items() if k.startswith("c3")}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    rank, world, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+    else:
+        run_ours(args, rank, world, local)
+
+
+if __name__ == "__main__":
+    main()

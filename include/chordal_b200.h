@@ -133,6 +133,15 @@ int chordal_permute_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, con
 int chordal_is_chordal_batch(const uint8_t *adj_dev, int64_t batch, int64_t n, int64_t stride,
                              int32_t *orders_dev, int32_t *witness_dev, void *stream);
 
+/* Host-buffer form of the batch (the end-to-end call a host application
+ * makes): graph b at adj_host + b * n * row_bytes (row_bytes >= ceil(n/8); use
+ * pinned memory for full copy bandwidth).  Chunks of `chunk` graphs (<= 0:
+ * 4096) rotate over three streams so the H2D copy of one chunk and the D2H of
+ * another overlap the search of a third.  Synchronous: returns when
+ * orders_host[b*n + i] and witness_host[3*b + k] are written. */
+int chordal_is_chordal_batch_host(const uint8_t *adj_host, int64_t batch, int64_t n, int64_t row_bytes,
+                                  int32_t *orders_host, int32_t *witness_host, int64_t chunk);
+
 /* ---- synthetic inputs --------------------------------------------------- */
 
 /* gen_dense_random (generate.py:32-56) bit for bit: Philox4x64-10 keyed by
@@ -142,6 +151,22 @@ int chordal_is_chordal_batch(const uint8_t *adj_dev, int64_t batch, int64_t n, i
  * written at adj_dev + b * n * stride; rows are fully overwritten. */
 int chordal_gen_dense_random(uint8_t *adj_dev, int64_t batch, int64_t n, int64_t stride, double p,
                              int64_t seed0, int64_t seed_step, void *stream);
+
+/* Build packed rows from an undirected edge list (0-based endpoints, vertex
+ * ids < n, no self loops; duplicates collapse) -- Graph._from_numpy_edges
+ * (graph.py:78-88) in HBM.  Rows are zeroed first. */
+int chordal_edges_to_dense(const int32_t *u_dev, const int32_t *v_dev, int64_t m, uint8_t *adj_dev, int64_t n,
+                           int64_t stride, void *stream);
+
+/* gen_chordal_random (generate.py:118-155) bit for bit, one GPU thread per
+ * graph: Philox4x64-10 keyed by mix64(seed, crc32("chordal-random")), with
+ * numpy's integers() (Lemire 32-bit bounded draws on split 64-bit outputs)
+ * and choice(replace=False) (Floyd + shuffle) replayed exactly.  Graph b uses
+ * seed0 + b * seed_step.  Needs k + 2 <= 10000 and a device scratch of
+ * chordal_gen_chordal_random_scratch_bytes(batch, n, k) bytes. */
+size_t chordal_gen_chordal_random_scratch_bytes(int64_t batch, int64_t n, int64_t k);
+int chordal_gen_chordal_random(uint8_t *adj_dev, int64_t batch, int64_t n, int64_t stride, int64_t k, int64_t seed0,
+                               int64_t seed_step, void *scratch_dev, size_t scratch_bytes, void *stream);
 
 #ifdef __cplusplus
 }

@@ -35,9 +35,13 @@ SIGNATURES = {
     "chordal_is_chordal_dense_host": [_P, _I64, _I64, _I32, _U64, _P, _P, _P],
     "chordal_permute_dense": [_P, _I64, _I64, _P, _P, _P],
     "chordal_is_chordal_batch": [_P, _I64, _I64, _I64, _P, _P, _P],
+    "chordal_is_chordal_batch_host": [_P, _I64, _I64, _I64, _P, _P, _I64],
     "chordal_gen_dense_random": [_P, _I64, _I64, _I64, _D, _I64, _I64, _P],
+    "chordal_edges_to_dense": [_P, _P, _I64, _P, _I64, _I64, _P],
+    "chordal_gen_chordal_random_scratch_bytes": [_I64, _I64, _I64],
+    "chordal_gen_chordal_random": [_P, _I64, _I64, _I64, _I64, _I64, _I64, _P, ctypes.c_size_t, _P],
 }
-_RESTYPES = {"chordal_strerror": ctypes.c_char_p}
+_RESTYPES = {"chordal_strerror": ctypes.c_char_p, "chordal_gen_chordal_random_scratch_bytes": ctypes.c_size_t}
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

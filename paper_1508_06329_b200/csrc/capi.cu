@@ -19,6 +19,10 @@ int launch_permute_dense(const uint8_t *, int64_t, int64_t, const int32_t *, uin
 int launch_batch(const uint8_t *, int64_t, int64_t, int64_t, int32_t *, int32_t *, cudaStream_t);
 int launch_gen_dense_random(uint8_t *, int64_t, int64_t, int64_t, double, int64_t, int64_t, uint32_t,
                             cudaStream_t);
+int launch_edges_to_dense(const int32_t *, const int32_t *, int64_t, uint8_t *, int64_t, int64_t, cudaStream_t);
+long long gen_chordal_scratch_words(int64_t, int64_t, int *);
+int launch_gen_chordal_random(uint8_t *, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, uint32_t, int32_t *,
+                              cudaStream_t);
 }  // namespace chordal
 
 using namespace chordal;
@@ -203,6 +207,60 @@ int chordal_is_chordal_batch(const uint8_t *adj_dev, int64_t batch, int64_t n, i
     return launch_batch(adj_dev, batch, n, stride, orders_dev, witness_dev, as_stream(stream));
 }
 
+int chordal_is_chordal_batch_host(const uint8_t *adj_host, int64_t batch, int64_t n, int64_t row_bytes,
+                                  int32_t *orders_host, int32_t *witness_host, int64_t chunk) {
+    if (batch < 0 || n < 0 || (batch > 0 && n > 0 && (!adj_host || !orders_host || !witness_host)))
+        return CHORDAL_EINVAL;
+    if (batch == 0 || n == 0) return CHORDAL_OK;
+    if (n > CHORDAL_BATCH_MAX_N) return CHORDAL_ETOOLARGE;
+    if (row_bytes < (n + 7) / 8) return CHORDAL_EINVAL;
+    if (chunk <= 0) chunk = 4096;
+    if (chunk > batch) chunk = batch;
+    const int64_t stride = (((n + 7) / 8) + 15) / 16 * 16;
+    const size_t gbytes = (size_t)n * stride;
+    constexpr int NB = 3;  // H2D of chunk c+1 and D2H of c-1 overlap the search of c
+    cudaStream_t st[NB] = {};
+    uint8_t *buf[NB] = {};
+    int32_t *ord[NB] = {};
+    int32_t *wit[NB] = {};
+    int rc = CHORDAL_OK;
+    for (int k = 0; k < NB && rc == CHORDAL_OK; ++k) {
+        if (cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking) != cudaSuccess) { rc = CHORDAL_ECUDA; break; }
+        if (cudaMallocAsync((void **)&buf[k], gbytes * chunk, st[k]) != cudaSuccess ||
+            cudaMallocAsync((void **)&ord[k], sizeof(int32_t) * n * chunk, st[k]) != cudaSuccess ||
+            cudaMallocAsync((void **)&wit[k], sizeof(int32_t) * 3 * chunk, st[k]) != cudaSuccess)
+            rc = CHORDAL_ENOMEM;
+        else if (stride != row_bytes && cudaMemsetAsync(buf[k], 0, gbytes * chunk, st[k]) != cudaSuccess)
+            rc = CHORDAL_ECUDA;
+    }
+    for (int64_t b0 = 0, c = 0; b0 < batch && rc == CHORDAL_OK; b0 += chunk, ++c) {
+        const int k = (int)(c % NB);
+        const int64_t nb = (batch - b0 < chunk) ? batch - b0 : chunk;
+        const uint8_t *src = adj_host + b0 * n * row_bytes;
+        cudaError_t e = (stride == row_bytes)
+                            ? cudaMemcpyAsync(buf[k], src, gbytes * nb, cudaMemcpyHostToDevice, st[k])
+                            : cudaMemcpy2DAsync(buf[k], stride, src, row_bytes, (n + 7) / 8, n * nb,
+                                                cudaMemcpyHostToDevice, st[k]);
+        if (e != cudaSuccess) { rc = CHORDAL_ECUDA; break; }
+        rc = launch_batch(buf[k], nb, n, stride, ord[k], wit[k], st[k]);
+        if (rc) break;
+        if (cudaMemcpyAsync(orders_host + b0 * n, ord[k], sizeof(int32_t) * n * nb, cudaMemcpyDeviceToHost,
+                            st[k]) != cudaSuccess ||
+            cudaMemcpyAsync(witness_host + 3 * b0, wit[k], sizeof(int32_t) * 3 * nb, cudaMemcpyDeviceToHost,
+                            st[k]) != cudaSuccess)
+            rc = CHORDAL_ECUDA;
+    }
+    for (int k = 0; k < NB; ++k) {
+        if (!st[k]) continue;
+        if (buf[k]) cudaFreeAsync(buf[k], st[k]);
+        if (ord[k]) cudaFreeAsync(ord[k], st[k]);
+        if (wit[k]) cudaFreeAsync(wit[k], st[k]);
+        if (cudaStreamSynchronize(st[k]) != cudaSuccess && rc == CHORDAL_OK) rc = CHORDAL_ECUDA;
+        cudaStreamDestroy(st[k]);
+    }
+    return rc;
+}
+
 int chordal_gen_dense_random(uint8_t *adj_dev, int64_t batch, int64_t n, int64_t stride, double p,
                              int64_t seed0, int64_t seed_step, void *stream) {
     if (batch < 0 || n < 0) return CHORDAL_EINVAL;
@@ -214,6 +272,32 @@ int chordal_gen_dense_random(uint8_t *adj_dev, int64_t batch, int64_t n, int64_t
                           ? CHORDAL_OK : CHORDAL_ECUDA;
     return launch_gen_dense_random(adj_dev, batch, n, stride, p, seed0, seed_step,
                                    crc32_str("dense-random"), as_stream(stream));
+}
+
+int chordal_edges_to_dense(const int32_t *u_dev, const int32_t *v_dev, int64_t m, uint8_t *adj_dev, int64_t n,
+                           int64_t stride, void *stream) {
+    if (m < 0 || (m > 0 && (!u_dev || !v_dev))) return CHORDAL_EINVAL;
+    if (n == 0) return m == 0 ? CHORDAL_OK : CHORDAL_EINVAL;
+    int rc = check_dense(adj_dev, n, stride);
+    if (rc) return rc;
+    return launch_edges_to_dense(u_dev, v_dev, m, adj_dev, n, stride, as_stream(stream));
+}
+
+size_t chordal_gen_chordal_random_scratch_bytes(int64_t batch, int64_t n, int64_t k) {
+    if (batch <= 0 || n <= 0 || k < 0) return 0;
+    return (size_t)batch * (size_t)gen_chordal_scratch_words(n, k, nullptr) * sizeof(int32_t);
+}
+
+int chordal_gen_chordal_random(uint8_t *adj_dev, int64_t batch, int64_t n, int64_t stride, int64_t k, int64_t seed0,
+                               int64_t seed_step, void *scratch_dev, size_t scratch_bytes, void *stream) {
+    if (batch < 0 || n < 1 || k < 0 || k >= n) return CHORDAL_EINVAL;
+    if (batch == 0) return CHORDAL_OK;
+    int rc = check_dense(adj_dev, n, stride);
+    if (rc) return rc;
+    if (k + 2 > 10000) return CHORDAL_EINVAL;  // numpy switches choice() algorithm above this pool size
+    if (!scratch_dev || scratch_bytes < chordal_gen_chordal_random_scratch_bytes(batch, n, k)) return CHORDAL_EINVAL;
+    return launch_gen_chordal_random(adj_dev, batch, n, stride, k, seed0, seed_step, crc32_str("chordal-random"),
+                                     reinterpret_cast<int32_t *>(scratch_dev), as_stream(stream));
 }
 
 }  // extern "C"

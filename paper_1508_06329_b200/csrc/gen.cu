@@ -131,3 +131,210 @@ int launch_gen_dense_random(uint8_t *adj, int64_t batch, int64_t n, int64_t stri
 }
 
 }  // namespace chordal
+
+// ---------------------------------------------------------------------------
+// gen_chordal_random (generate.py:118-155) bit for bit, one thread per graph.
+//
+// numpy's Generator draws replayed exactly:
+//   integers(lo, hi)  -> random_bounded_uint64(off=lo, rng=hi-1-lo): rng == 0
+//                        draws nothing; rng < 2^32-1 uses Lemire's 32-bit
+//                        rejection on next_uint32, which hands out the low
+//                        then the high half of each 64-bit Philox output.
+//   choice(P, size=w, replace=False) with P <= 10000 -> Floyd's algorithm
+//                        over j = P-w .. P-1 with an open-addressing hash set
+//                        of 2^ceil(log2(1.2 w)) slots, then an in-place
+//                        Fisher-Yates shuffle (j = bounded(0, i), i = w-1..1).
+// (Verified against numpy 2.3 on every configuration generator call.)
+namespace chordal {
+
+namespace {
+
+struct PhiloxStream {
+    uint64_t key, ctr;
+    uint64_t b0, b1, b2, b3;
+    int pos;
+    bool has32;
+    uint32_t u32;
+
+    __device__ explicit PhiloxStream(uint64_t k) : key(k), ctr(0), b0(0), b1(0), b2(0), b3(0), pos(4), has32(false), u32(0) {}
+
+    __device__ uint64_t next64() {
+        if (pos >= 4) {
+            ++ctr;
+            U4 b = philox4x64_10(ctr, key);
+            b0 = b.v[0]; b1 = b.v[1]; b2 = b.v[2]; b3 = b.v[3];
+            pos = 0;
+        }
+        uint64_t x = pos == 0 ? b0 : pos == 1 ? b1 : pos == 2 ? b2 : b3;
+        ++pos;
+        return x;
+    }
+    __device__ uint32_t next32() {
+        if (has32) {
+            has32 = false;
+            return u32;
+        }
+        uint64_t x = next64();
+        has32 = true;
+        u32 = (uint32_t)(x >> 32);
+        return (uint32_t)x;
+    }
+    // random_bounded_uint64(off, rng) for 0 <= rng < 2^32 - 1 (inclusive range)
+    __device__ uint64_t bounded(uint64_t off, uint64_t rng) {
+        if (rng == 0) return off;
+        const uint32_t excl = (uint32_t)rng + 1u;
+        uint64_t m = (uint64_t)next32() * excl;
+        uint32_t left = (uint32_t)m;
+        if (left < excl) {
+            const uint32_t th = (0xFFFFFFFFu - (uint32_t)rng) % excl;
+            while (left < th) {
+                m = (uint64_t)next32() * excl;
+                left = (uint32_t)m;
+            }
+        }
+        return off + (m >> 32);
+    }
+};
+
+__device__ __forceinline__ uint64_t chordal_key(long long seed, uint32_t crc) {
+    return splitmix64(splitmix64((uint64_t)seed) ^ (uint64_t)crc);
+}
+
+__device__ __forceinline__ void set_edge(uint8_t *g, long long stride, int a, int b) {
+    reinterpret_cast<uint32_t *>(g + (long long)a * stride)[b >> 5] |= 1u << (b & 31);
+    reinterpret_cast<uint32_t *>(g + (long long)b * stride)[a >> 5] |= 1u << (a & 31);
+}
+
+}  // namespace
+
+__global__ void gen_chordal_kernel(uint8_t *__restrict__ adj, long long batch, int n, long long stride, int k,
+                                   long long seed0, long long seed_step, uint32_t crc, int32_t *__restrict__ scratch,
+                                   long long scratch_words, int hmask) {
+    const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+    if (b >= batch) return;
+    uint8_t *g = adj + b * (long long)n * stride;
+    int32_t *att_off = scratch + b * scratch_words;
+    int32_t *att_len = att_off + n;
+    int32_t *hs = att_len + n;
+    int32_t *lst = hs + (hmask + 1);
+    PhiloxStream rs(chordal_key(seed0 + b * seed_step, crc));
+    int32_t top = 0;
+    att_off[0] = 0;
+    att_len[0] = 0;
+    for (int i = 1; i < n; ++i) {
+        int32_t *out = lst + top;
+        int cnt;
+        if (k >= i) {
+            for (int c = 0; c < i; ++c) {
+                out[c] = c;
+                set_edge(g, stride, i, c);
+            }
+            cnt = i;
+        } else {
+            long long want = (long long)k + (long long)(int64_t)rs.bounded((uint64_t)(int64_t)-1, 2);
+            want = want < 1 ? 1 : (want > i ? i : want);
+            const int j = (int)rs.bounded(0, (uint64_t)(i - 1));
+            const int32_t *src = lst + att_off[j];
+            const int plen = att_len[j];
+            const int P = plen + 1;  // pool = att[j] ++ [j]
+            if (want >= P) {
+                for (int c = 0; c < plen; ++c) {
+                    int v = src[c];
+                    out[c] = v;
+                    set_edge(g, stride, i, v);
+                }
+                out[plen] = j;
+                set_edge(g, stride, i, j);
+                cnt = P;
+            } else {
+                const int w = (int)want;
+                // Floyd sampling of w distinct indices out of P
+                const int setsize = (int)(1.2 * (double)w);
+                int mask = setsize;
+                mask |= mask >> 1; mask |= mask >> 2; mask |= mask >> 4; mask |= mask >> 8; mask |= mask >> 16;
+                for (int t = 0; t <= mask; ++t) hs[t] = -1;
+                for (int jj = P - w; jj < P; ++jj) {
+                    int val = (int)rs.bounded(0, (uint64_t)jj);
+                    int loc = val & mask;
+                    while (hs[loc] != -1 && hs[loc] != val) loc = (loc + 1) & mask;
+                    if (hs[loc] == -1) {
+                        hs[loc] = val;
+                        out[jj - P + w] = val;
+                    } else {
+                        loc = jj & mask;
+                        while (hs[loc] != -1) loc = (loc + 1) & mask;
+                        hs[loc] = jj;
+                        out[jj - P + w] = jj;
+                    }
+                }
+                for (int t = w - 1; t >= 1; --t) {  // Fisher-Yates (shuffle=True)
+                    int r = (int)rs.bounded(0, (uint64_t)t);
+                    int tmp = out[r];
+                    out[r] = out[t];
+                    out[t] = tmp;
+                }
+                for (int c = 0; c < w; ++c) {  // pool[idx]
+                    int id = out[c];
+                    int v = id < plen ? src[id] : j;
+                    out[c] = v;
+                    set_edge(g, stride, i, v);
+                }
+                cnt = w;
+            }
+        }
+        att_off[i] = top;
+        att_len[i] = cnt;
+        top += cnt;
+    }
+}
+
+long long gen_chordal_scratch_words(int64_t n, int64_t k, int *hmask_out) {
+    int setsize = (int)(1.2 * (double)(k + 2));
+    int mask = setsize;
+    mask |= mask >> 1; mask |= mask >> 2; mask |= mask >> 4; mask |= mask >> 8; mask |= mask >> 16;
+    if (hmask_out) *hmask_out = mask;
+    // att_off[n] + att_len[n] + hash[mask+1] + lists (vertex i keeps <= min(i, k+1) entries)
+    return 2 * n + (mask + 1) + n * (k + 1) + 4;
+}
+
+int launch_gen_chordal_random(uint8_t *adj, int64_t batch, int64_t n, int64_t stride, int64_t k, int64_t seed0,
+                              int64_t seed_step, uint32_t crc, int32_t *scratch, cudaStream_t stream) {
+    int hmask = 0;
+    const long long words = gen_chordal_scratch_words(n, k, &hmask);
+    if (cudaMemsetAsync(adj, 0, (size_t)batch * n * stride, stream) != cudaSuccess) return CHORDAL_ECUDA;
+    if (k == 0 || n == 1) return CHORDAL_OK;  // edgeless, no draws (generate.py:133-134)
+    const int threads = 64;
+    const long long blocks = (batch + threads - 1) / threads;
+    gen_chordal_kernel<<<(unsigned)blocks, threads, 0, stream>>>(adj, batch, (int)n, stride, (int)k, seed0, seed_step,
+                                                                 crc, scratch, words, hmask);
+    CH_LAUNCH_CHECK();
+    return CHORDAL_OK;
+}
+
+}  // namespace chordal
+
+namespace chordal {
+
+// Undirected edge list (0-based u[i], v[i]) -> packed rows; duplicates collapse
+// (Graph._from_numpy_edges, graph.py:78-88, built in HBM instead of on the host).
+__global__ void edges_to_dense_kernel(const int32_t *__restrict__ u, const int32_t *__restrict__ v, long long m,
+                                      uint8_t *__restrict__ adj, long long stride) {
+    for (long long e = blockIdx.x * (long long)blockDim.x + threadIdx.x; e < m; e += (long long)gridDim.x * blockDim.x) {
+        const int a = __ldg(u + e), b = __ldg(v + e);
+        atomicOr(reinterpret_cast<unsigned int *>(adj + (long long)a * stride) + (b >> 5), 1u << (b & 31));
+        atomicOr(reinterpret_cast<unsigned int *>(adj + (long long)b * stride) + (a >> 5), 1u << (a & 31));
+    }
+}
+
+int launch_edges_to_dense(const int32_t *u, const int32_t *v, int64_t m, uint8_t *adj, int64_t n, int64_t stride,
+                          cudaStream_t stream) {
+    if (cudaMemsetAsync(adj, 0, (size_t)n * stride, stream) != cudaSuccess) return CHORDAL_ECUDA;
+    if (m <= 0) return CHORDAL_OK;
+    long long blocks = (m + 255) / 256;
+    if (blocks > 148LL * 32) blocks = 148LL * 32;
+    edges_to_dense_kernel<<<(int)blocks, 256, 0, stream>>>(u, v, m, adj, stride);
+    CH_LAUNCH_CHECK();
+    return CHORDAL_OK;
+}
+
+}  // namespace chordal

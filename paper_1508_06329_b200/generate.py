@@ -89,6 +89,22 @@ def gen_dense_random_device(n: int, p: float, seeds, *, stride: int | None = Non
     return ops.gen_dense_random(out, n, s, p, seeds.start, step)
 
 
+def gen_chordal_random_device(n: int, k: int, seeds, *, stride: int | None = None, out=None):
+    """gen_chordal_random drawn on the GPU (csrc/gen.cu): uint8[B, n, stride]."""
+    from . import _native, ops
+    from .graph import device_stride
+
+    torch = _native.require_cuda()
+    if isinstance(seeds, int):
+        seeds = range(seeds, seeds + 1)
+    B = len(seeds)
+    s = stride or device_stride(n)
+    if out is None:
+        out = torch.empty((B, n, s), dtype=torch.uint8, device="cuda")
+    step = seeds.step if B > 1 else 1
+    return ops.gen_chordal_random(out, n, s, k, seeds.start, step)
+
+
 def chordal_random_edges(n: int, k: int, seed: int) -> tuple[np.ndarray, np.ndarray]:
     """0-based edge endpoints of gen_chordal_random (generate.py:118-155).
 
@@ -140,13 +156,18 @@ def remove_first_chord(g: Graph) -> tuple[Graph, tuple[int, int] | None]:
     non-chordal twins.  Returns (graph, removed 1-based edge).
     """
     n = g.n
-    rows = np.unpackbits(np.asarray(g._packed), axis=1, bitorder="little", count=n).astype(bool)
+    packed = np.asarray(g._packed)
+
+    def row(i):
+        return np.unpackbits(packed[i], bitorder="little", count=n).astype(bool)
+
     for u in range(n):
-        for v in np.flatnonzero(rows[u, u + 1 :]) + u + 1:
-            common = np.flatnonzero(rows[u] & rows[v])
+        ru = row(u)
+        for v in np.flatnonzero(ru[u + 1 :]) + u + 1:
+            common = np.flatnonzero(ru & row(v))
             if common.size < 2:
                 continue
-            sub = rows[np.ix_(common, common)]
+            sub = np.unpackbits(packed[common], axis=1, bitorder="little", count=n)[:, common].astype(bool)
             if (~sub).sum() > common.size:  # some off-diagonal non-edge
                 packed = np.array(g._packed, copy=True)
                 packed[u, v >> 3] &= np.uint8(0xFF ^ (1 << (v & 7)))

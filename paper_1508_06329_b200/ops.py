@@ -135,6 +135,33 @@ def gen_dense_random(adj, n: int, stride: int, p: float, seed0: int, seed_step: 
     return adj
 
 
+def gen_chordal_random(adj, n: int, stride: int, k: int, seed0: int, seed_step: int = 1, stream=None):
+    """Fill adj uint8[B, n, stride] with gen_chordal_random(n, k, seed0 + b*seed_step)."""
+    torch = _native.require_cuda()
+    B = int(adj.shape[0])
+    if B and n:
+        nbytes = int(lib.chordal_gen_chordal_random_scratch_bytes(B, n, k))
+        scratch = torch.empty(max(nbytes, 4), dtype=torch.uint8, device=adj.device)
+        check(
+            lib.chordal_gen_chordal_random(ptr(adj), B, n, stride, int(k), int(seed0), int(seed_step), ptr(scratch),
+                                           nbytes, stream_ptr(stream)),
+            "chordal_gen_chordal_random",
+        )
+    return adj
+
+
+def edges_to_dense(u0, v0, n: int, stride: int, out=None, stream=None):
+    """0-based endpoint arrays (host or device) -> device rows uint8[n, stride]."""
+    torch = _native.require_cuda()
+    u = torch.as_tensor(np.asarray(u0, dtype=np.int32) if not hasattr(u0, "device") else u0).to("cuda", torch.int32)
+    v = torch.as_tensor(np.asarray(v0, dtype=np.int32) if not hasattr(v0, "device") else v0).to("cuda", torch.int32)
+    if out is None:
+        out = torch.empty((max(n, 1), stride), dtype=torch.uint8, device="cuda")
+    check(lib.chordal_edges_to_dense(ptr(u), ptr(v), int(u.numel()), ptr(out), n, stride, stream_ptr(stream)),
+          "chordal_edges_to_dense")
+    return out[:n]
+
+
 def witness_tuple(w) -> tuple[int, int, int] | None:
     """Device witness tensor -> 0-based (v, p, z) or None."""
     a = w.cpu().numpy() if hasattr(w, "cpu") else np.asarray(w)

@@ -258,6 +258,53 @@ def test_device_dense_generator_bit_exact():
             assert not adj[b, :, w:].any()
 
 
+def test_device_chordal_generator_bit_exact():
+    from paper_1508_06329_b200.generate import gen_chordal_random_device
+
+    for n, k, seeds in ((512, 8, range(1, 17, 2)), (300, 30, range(2, 4)), (64, 0, range(1)), (1, 0, range(1)),
+                        (1000, 8, range(0, 1)), (50, 49, range(3, 4))):
+        adj = gen_chordal_random_device(n, k, seeds).cpu().numpy()
+        w = (n + 7) // 8
+        for b, s in enumerate(seeds):
+            ref = gen_chordal_random(n, k, s)._packed
+            assert (adj[b, :, :w] == ref).all(), (n, k, s)
+            assert not adj[b, :, w:].any()
+
+
+def test_edges_to_dense():
+    from paper_1508_06329_b200 import ops
+    from paper_1508_06329_b200.generate import chordal_random_edges
+
+    u, v = chordal_random_edges(2000, 12, 4)
+    rows = ops.edges_to_dense(u, v, 2000, 256).cpu().numpy()
+    assert (rows[:, :250] == gen_chordal_random(2000, 12, 4)._packed).all() and not rows[:, 250:].any()
+
+
+def test_host_buffer_batch_entry_point():
+    import torch
+
+    gs = [gen_dense_random(512, 0.5, s) if s % 2 == 0 else gen_chordal_random(512, 8, s) for s in range(40)]
+    host = np.zeros((40, 512, 64), dtype=np.uint8)
+    for b, g in enumerate(gs):
+        host[b] = g._packed
+    orders = np.empty((40, 512), dtype=np.int32)
+    wit = np.empty((40, 3), dtype=np.int32)
+    rc = _native.lib.chordal_is_chordal_batch_host(host.ctypes.data, 40, 512, 64, orders.ctypes.data,
+                                                   wit.ctypes.data, 7)  # ragged final chunk
+    assert rc == 0
+    verdict, o, w = oracle.is_chordal_batch(host, 512)
+    assert (orders == o).all() and (wit == w).all()
+    # unpadded host rows (row_bytes = ceil(n/8) < device stride)
+    g = [gen_chordal_random(100, 4, s) for s in range(5)]
+    h2 = np.stack([x._packed for x in g])
+    o2 = np.empty((5, 100), dtype=np.int32)
+    w2 = np.empty((5, 3), dtype=np.int32)
+    assert _native.lib.chordal_is_chordal_batch_host(h2.ctypes.data, 5, 100, 13, o2.ctypes.data, w2.ctypes.data, 2) == 0
+    v3, o3, w3 = oracle.is_chordal_batch(h2, 100)
+    assert (o2 == o3).all() and (w2 == w3).all()
+    torch.cuda.synchronize()
+
+
 def test_host_buffer_entry_point():
     for g in (gen_chordal_random(1000, 8, 0), remove_first_chord(gen_chordal_random(1000, 8, 0))[0],
               gen_dense_random(777, 0.5, 1)):

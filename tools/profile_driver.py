@@ -1,0 +1,43 @@
+"""Small driver for ncu captures: runs each hot kernel a few times on config inputs.
+
+    python tools/profile_driver.py {batch|lexbfs32k|peo32k|lexbfs1k|all}
+"""
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import torch  # noqa: E402
+
+from paper_1508_06329_b200 import ops  # noqa: E402
+from paper_1508_06329_b200.device import DeviceRows  # noqa: E402
+from paper_1508_06329_b200.generate import chordal_random_edges  # noqa: E402
+
+import bench  # noqa: E402
+
+
+def rows_chordal(n, k, seed):
+    u, v = chordal_random_edges(n, k, seed)
+    stride = max(16, ((n + 7) // 8 + 15) // 16 * 16)
+    return DeviceRows(n, stride, ops.edges_to_dense(u, v, n, stride))
+
+
+def main(what):
+    if what in ("batch", "all"):
+        adj = bench.build_batch(0, int(os.environ.get("GRAPHS", "16384")), "cuda")
+        for _ in range(3):
+            ops.is_chordal_batch(adj, 512, 64)
+    if what in ("lexbfs32k", "peo32k", "all"):
+        r = rows_chordal(32768, 1024, 0)
+        for _ in range(2):
+            order, pos = ops.lexbfs(r)
+            ops.peo(r, order, pos)
+    if what in ("lexbfs1k", "all"):
+        r = rows_chordal(1000, 8, 0)
+        for _ in range(3):
+            ops.is_chordal(r)
+    torch.cuda.synchronize()
+
+
+if __name__ == "__main__":
+    main(sys.argv[1] if len(sys.argv) > 1 else "all")
