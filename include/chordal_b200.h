@@ -65,12 +65,22 @@ const char *chordal_strerror(int status);
 
 /* ---- dense single graph ------------------------------------------------ */
 
+/* Workspace (device bytes) of chordal_lexbfs_dense / chordal_is_chordal_dense
+ * for a graph of n vertices and m edges. */
+size_t chordal_dense_workspace_bytes(int64_t n, int64_t m);
+
 /* LexBFS ordering.  Replaces lexbfs_partition (search.py:500-506),
  * lexbfs_labels (search.py:262-268) and parallel_lexbfs (parallel/lexbfs.py:
- * 234-243).  Writes order_dev[n] (vertex at each position) and pos_dev[n]
- * (position of each vertex).  n <= CHORDAL_DENSE_LEXBFS_MAX_N. */
-int chordal_lexbfs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int32_t tie_rule,
-                         uint64_t seed, int32_t *order_dev, int32_t *pos_dev, void *stream);
+ * 234-243).  Writes order_dev[n] (vertex at each position), pos_dev[n]
+ * (position of each vertex) and, if parent_dev is not NULL, the PEO parent of
+ * every vertex (-1 for none; all -1 when the dense engine ran, see below).
+ * m is the edge count (Graph.m); pass m < 0 to let the call count the edges,
+ * which synchronises `stream` once.  Engines: graphs with m > n^2/16 run the
+ * persistent single-CTA arrangement kernel (n <= 32768); sparser graphs are
+ * converted to CSR on the device and run the O(deg)-per-step slot kernel. */
+int chordal_lexbfs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int64_t m, int32_t tie_rule,
+                         uint64_t seed, int32_t *order_dev, int32_t *pos_dev, int32_t *parent_dev, void *ws,
+                         size_t ws_bytes, void *stream);
 
 /* pos_dev[order_dev[i]] = i  (VertexOrdering.pos0, graph.py:224-230). */
 int chordal_positions(const int32_t *order_dev, int64_t n, int32_t *pos_dev, void *stream);
@@ -78,16 +88,17 @@ int chordal_positions(const int32_t *order_dev, int64_t n, int32_t *pos_dev, voi
 /* Sets *key_dev = UINT64_MAX (the "no violation" key). */
 int chordal_key_init(uint64_t *key_dev, void *stream);
 
-/* Vertex-parallel PEO check over v in [v_begin, v_end): for each v finds the
- * parent p (left neighbour with the greatest position, peo.py:106-121) and
- * tests LN(v)\{p} subset of LN(p) (peo.py:124-142, parallel/peo.py:57-65);
- * atomically lowers *key_dev to min((p << 32) | v) over violating v.  The
- * minimum key is the reference's deterministic witness pair (ascending p, then
- * ascending v, peo.py:81-85).  Row shards of one graph can run on different
- * GPUs and be combined with an integer MIN all-reduce of the key. */
-int chordal_peo_dense_key(const uint8_t *adj_dev, int64_t n, int64_t stride,
-                          const int32_t *order_dev, const int32_t *pos_dev, int64_t v_begin,
-                          int64_t v_end, uint64_t *key_dev, void *stream);
+/* Vertex-parallel PEO check over v in [v_begin, v_end): for each v takes the
+ * parent p (parent_dev[v] if given, else the left neighbour with the greatest
+ * position, peo.py:106-121) and tests LN(v)\{p} subset of LN(p) (peo.py:
+ * 124-142, parallel/peo.py:57-65); atomically lowers *key_dev to
+ * min((p << 32) | v) over violating v.  The minimum key is the reference's
+ * deterministic witness pair (ascending p, then ascending v, peo.py:81-85).
+ * Row shards of one graph can run on different GPUs and be combined with an
+ * integer MIN all-reduce of the key. */
+int chordal_peo_dense_key(const uint8_t *adj_dev, int64_t n, int64_t stride, const int32_t *order_dev,
+                          const int32_t *pos_dev, const int32_t *parent_dev, int64_t v_begin, int64_t v_end,
+                          uint64_t *key_dev, void *stream);
 
 /* Resolves the key to the witness triple: z = smallest vertex id in
  * LN(v) \ {p} \ N(p)  (peo.py:126-141 / _first_witness_big peo.py:167-173). */
@@ -97,14 +108,15 @@ int chordal_peo_dense_witness(const uint8_t *adj_dev, int64_t n, int64_t stride,
 
 /* is_peo (peo.py:72-97): key_init + peo_dense_key over all v + witness. */
 int chordal_peo_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, const int32_t *order_dev,
-                      const int32_t *pos_dev, uint64_t *key_dev, int32_t *witness_dev,
+                      const int32_t *pos_dev, const int32_t *parent_dev, uint64_t *key_dev, int32_t *witness_dev,
                       void *stream);
 
 /* is_chordal (peo.py:177-202) / parallel_is_chordal (parallel/peo.py:98-114):
- * LexBFS then the PEO check, all on `stream`. */
-int chordal_is_chordal_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int32_t tie_rule,
-                             uint64_t seed, int32_t *order_dev, int32_t *pos_dev,
-                             uint64_t *key_dev, int32_t *witness_dev, void *stream);
+ * LexBFS then the PEO check (parents handed over when the slot engine ran),
+ * all on `stream`.  ws: chordal_dense_workspace_bytes(n, m) bytes. */
+int chordal_is_chordal_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int64_t m, int32_t tie_rule,
+                             uint64_t seed, int32_t *order_dev, int32_t *pos_dev, void *ws, size_t ws_bytes,
+                             int32_t *witness_dev, void *stream);
 
 /* Host-buffer form of is_chordal: copies the unpadded packed rows
  * (row_bytes = ceil(n/8), exactly Graph._packed) to the device, runs the
@@ -114,6 +126,34 @@ int chordal_is_chordal_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, 
 int chordal_is_chordal_dense_host(const uint8_t *adj_host, int64_t n, int64_t row_bytes,
                                   int32_t tie_rule, uint64_t seed, int32_t *order_host,
                                   int32_t *witness_host, int32_t *chordal_out);
+
+/* ---- CSR single graph (the N = 10^6 configuration) ---------------------- */
+
+/* Workspace of chordal_lexbfs_csr (about 60 bytes per vertex). */
+size_t chordal_lexbfs_csr_workspace_bytes(int64_t n);
+
+/* LexBFS on CSR adjacency with the slot engine (state in global memory):
+ * lexbfs_partition(g, method="linked") (search.py:500-532) on a graph that
+ * exposes adjacency_lists0().  parent_dev optional. */
+int chordal_lexbfs_csr(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, int32_t tie_rule,
+                       uint64_t seed, int32_t *order_dev, int32_t *pos_dev, int32_t *parent_dev, void *ws,
+                       size_t ws_bytes, void *stream);
+
+/* PEO check on CSR over v in [v_begin, v_end) (row shards), as
+ * chordal_peo_dense_key; membership z in N(p) by binary search in p's row. */
+int chordal_peo_csr_key(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, const int32_t *pos_dev,
+                        const int32_t *parent_dev, int64_t v_begin, int64_t v_end, uint64_t *key_dev, void *stream);
+int chordal_peo_csr_witness(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n,
+                            const int32_t *pos_dev, const uint64_t *key_dev, int32_t *witness_dev, void *stream);
+/* _is_peo_lists (peo.py:100-149) on CSR: init + key over all v + witness. */
+int chordal_peo_csr(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, const int32_t *pos_dev,
+                    const int32_t *parent_dev, uint64_t *key_dev, int32_t *witness_dev, void *stream);
+
+/* Packed rows -> CSR (ascending rows).  indptr_dev[n+1] is always written;
+ * indices_dev (capacity indptr[n]) is filled when not NULL, so a caller can
+ * size it from indptr[n] first. */
+int chordal_dense_to_csr(const uint8_t *adj_dev, int64_t n, int64_t stride, int64_t *indptr_dev,
+                         int32_t *indices_dev, void *stream);
 
 /* Relabel: out row r, bit s = adj[perm[r]][perm[s]] (perm a 0-based
  * permutation, out distinct from adj, same stride).  Lets the ascending

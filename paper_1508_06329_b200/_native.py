@@ -20,28 +20,41 @@ TIE_ASCENDING, TIE_DESCENDING, TIE_SEEDED_ARB = 0, 1, 2
 DENSE_LEXBFS_MAX_N = 32768
 BATCH_MAX_N = 1024
 
-# name -> argtypes (restype is int unless listed in _RESTYPES)
-_P, _I64, _I32, _U64, _D = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64, ctypes.c_double
+# name -> argtypes; restype is int unless listed in _RESTYPES
+_P, _I64, _I32, _U64 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint64
+_D, _SZ = ctypes.c_double, ctypes.c_size_t
 SIGNATURES = {
     "chordal_abi_version": [],
     "chordal_strerror": [ctypes.c_int],
-    "chordal_lexbfs_dense": [_P, _I64, _I64, _I32, _U64, _P, _P, _P],
+    "chordal_dense_workspace_bytes": [_I64, _I64],
+    "chordal_lexbfs_dense": [_P, _I64, _I64, _I64, _I32, _U64, _P, _P, _P, _P, _SZ, _P],
     "chordal_positions": [_P, _I64, _P, _P],
     "chordal_key_init": [_P, _P],
-    "chordal_peo_dense_key": [_P, _I64, _I64, _P, _P, _I64, _I64, _P, _P],
+    "chordal_peo_dense_key": [_P, _I64, _I64, _P, _P, _P, _I64, _I64, _P, _P],
     "chordal_peo_dense_witness": [_P, _I64, _I64, _P, _P, _P, _P],
-    "chordal_peo_dense": [_P, _I64, _I64, _P, _P, _P, _P, _P],
-    "chordal_is_chordal_dense": [_P, _I64, _I64, _I32, _U64, _P, _P, _P, _P, _P],
+    "chordal_peo_dense": [_P, _I64, _I64, _P, _P, _P, _P, _P, _P],
+    "chordal_is_chordal_dense": [_P, _I64, _I64, _I64, _I32, _U64, _P, _P, _P, _SZ, _P, _P],
     "chordal_is_chordal_dense_host": [_P, _I64, _I64, _I32, _U64, _P, _P, _P],
+    "chordal_lexbfs_csr_workspace_bytes": [_I64],
+    "chordal_lexbfs_csr": [_P, _P, _I64, _I32, _U64, _P, _P, _P, _P, _SZ, _P],
+    "chordal_peo_csr_key": [_P, _P, _I64, _P, _P, _I64, _I64, _P, _P],
+    "chordal_peo_csr_witness": [_P, _P, _I64, _P, _P, _P, _P],
+    "chordal_peo_csr": [_P, _P, _I64, _P, _P, _P, _P, _P],
+    "chordal_dense_to_csr": [_P, _I64, _I64, _P, _P, _P],
     "chordal_permute_dense": [_P, _I64, _I64, _P, _P, _P],
     "chordal_is_chordal_batch": [_P, _I64, _I64, _I64, _P, _P, _P],
     "chordal_is_chordal_batch_host": [_P, _I64, _I64, _I64, _P, _P, _I64],
     "chordal_gen_dense_random": [_P, _I64, _I64, _I64, _D, _I64, _I64, _P],
     "chordal_edges_to_dense": [_P, _P, _I64, _P, _I64, _I64, _P],
     "chordal_gen_chordal_random_scratch_bytes": [_I64, _I64, _I64],
-    "chordal_gen_chordal_random": [_P, _I64, _I64, _I64, _I64, _I64, _I64, _P, ctypes.c_size_t, _P],
+    "chordal_gen_chordal_random": [_P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _SZ, _P],
 }
-_RESTYPES = {"chordal_strerror": ctypes.c_char_p, "chordal_gen_chordal_random_scratch_bytes": ctypes.c_size_t}
+_RESTYPES = {
+    "chordal_strerror": ctypes.c_char_p,
+    "chordal_gen_chordal_random_scratch_bytes": _SZ,
+    "chordal_dense_workspace_bytes": _SZ,
+    "chordal_lexbfs_csr_workspace_bytes": _SZ,
+}
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -1,77 +1,91 @@
 // batch.cu -- is_chordal over many small independent graphs (n <= 1024).
 //
 // One warp (= one CTA) per graph.  The graph's packed adjacency is staged in
-// shared memory once (a single pass over HBM), then the warp runs the same
-// LexBFS refinement as lexbfs_dense.cu (reached-region arrangement + unreached
-// bitset, class-start bitmask, stable segmented partition) with __syncwarp
-// instead of block barriers, followed by the PEO check of peo_dense.cu with
-// lanes striding over vertices.  Replaces is_chordal (peo.py:177-202) called
-// once per graph by the reference's bench loop (bench.py:86-95).
+// shared memory once (a single pass over HBM, edges counted on the way), then
+// the warp runs one of two LexBFS engines and the PEO check.  Replaces
+// is_chordal (peo.py:177-202) called once per graph by the reference's bench
+// loop (bench.py:86-95).
+//
+//   dense graphs (m > n^2/16): the arrangement engine of lexbfs_dense.cu
+//     (reached-region arrangement + unreached bitset, stable segmented
+//     partition per step) -- random dense graphs split into singleton classes
+//     after O(log n) steps and the search exits early;
+//   other graphs: the O(deg)-per-step slot engine (slot_engine.cuh), which
+//     also yields every vertex's PEO parent.
+// PEO check: lanes stride over vertices; parent from the engine (or a short
+// backward scan over the order); stray = A[v] & ~A[p] & ~{p} confirmed by
+// pos < pos(p); the minimum (p << 32 | v) key is the reference's witness.
 #include "common.cuh"
+#include "slot_engine.cuh"
 
 namespace chordal {
 
 namespace {
 
 struct BatchLayout {
-    size_t adj, arrA, arrB, segtot, ord, pos, U, bnd, Fw, Bw, cin, lbin, total;
+    size_t adj, ord, pos, par, uni, total;
+    // arrangement engine (inside uni)
+    size_t arrA, arrB, segtot, U, bnd, Fw, Bw, cin, lbin, arr_end;
+    // slot engine (inside uni)
+    size_t cls, slot, c_head, c_end, c_live, c_prev, c_next, c_tgt, c_cnt, c_split, freel, touched, scratch, nbuf,
+        slot_end;
+    int cap;
     __host__ __device__ static size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
     __host__ __device__ BatchLayout(int n, int stride) {
         const int W = (n + 31) >> 5;
-        const size_t np = size_t(W) * 32;
+        const size_t np = size_t(W) * 32, nc = size_t(n) + 2;
         size_t o = 0;
         adj = o; o = a16(o + size_t(n) * stride);
-        arrA = o; o = a16(o + np * 2);
-        arrB = o; o = a16(o + np * 2);
-        segtot = o; o = a16(o + np * 2);
-        ord = o; o = a16(o + np * 2);
-        pos = o; o = a16(o + np * 2);
-        U = o; o = a16(o + size_t(W) * 4);
-        bnd = o; o = a16(o + size_t(W + 2) * 4);
-        Fw = o; o = a16(o + size_t(W) * 4);
-        Bw = o; o = a16(o + size_t(W + 1) * 4);
-        cin = o; o = a16(o + size_t(W) * 4);
-        lbin = o; o = a16(o + size_t(W) * 4);
-        total = o;
+        ord = o; o = a16(o + size_t(n) * 4);
+        pos = o; o = a16(o + size_t(n) * 4);
+        par = o; o = a16(o + size_t(n) * 4);
+        uni = o;
+        size_t u = o;
+        arrA = u; u = a16(u + np * 2);
+        arrB = u; u = a16(u + np * 2);
+        segtot = u; u = a16(u + np * 2);
+        U = u; u = a16(u + size_t(W) * 4);
+        bnd = u; u = a16(u + size_t(W + 2) * 4);
+        Fw = u; u = a16(u + size_t(W) * 4);
+        Bw = u; u = a16(u + size_t(W + 1) * 4);
+        cin = u; u = a16(u + size_t(W) * 4);
+        lbin = u; u = a16(u + size_t(W) * 4);
+        arr_end = u;
+        cap = 2 * n + 64;
+        u = o;
+        cls = u; u = a16(u + size_t(n) * 2);
+        slot = u; u = a16(u + size_t(cap) * 2);
+        c_head = u; u = a16(u + nc * 4);
+        c_end = u; u = a16(u + nc * 4);
+        c_live = u; u = a16(u + nc * 2);
+        c_prev = u; u = a16(u + nc * 2);
+        c_next = u; u = a16(u + nc * 2);
+        c_tgt = u; u = a16(u + nc * 2);
+        c_cnt = u; u = a16(u + nc * 2);
+        c_split = u; u = a16(u + nc * 4);
+        freel = u; u = a16(u + nc * 2);
+        touched = u; u = a16(u + nc * 2);
+        scratch = u; u = a16(u + size_t(n) * 2);
+        nbuf = u; u = a16(u + size_t(n) * 2);
+        slot_end = u;
+        total = arr_end > slot_end ? arr_end : slot_end;
     }
 };
 
-}  // namespace
-
-__global__ void __launch_bounds__(32)
-batch_chordal_kernel(const uint8_t *__restrict__ adj_all, int n, int stride, int32_t *__restrict__ orders,
-                     int32_t *__restrict__ witness) {
-    extern __shared__ __align__(16) uint8_t smem[];
-    const BatchLayout L(n, stride);
-    const int lane = threadIdx.x;
+// Arrangement LexBFS (LOWEST_INDEX) for one graph in one warp; see lexbfs_dense.cu.
+__device__ void arrangement_lexbfs_warp(const uint32_t *A32, int n, int sw, uint8_t *smem, const BatchLayout &L,
+                                        int32_t *ord, int32_t *pos) {
+    const int lane = threadIdx.x & 31;
     const int W = (n + 31) >> 5;
-    const int sw = stride >> 2;  // row pitch in 32-bit words
-    const long long g = blockIdx.x;
-    uint32_t *A32 = (uint32_t *)(smem + L.adj);
     uint16_t *arrA = (uint16_t *)(smem + L.arrA);
     uint16_t *arrB = (uint16_t *)(smem + L.arrB);
     uint16_t *segtot = (uint16_t *)(smem + L.segtot);
-    uint16_t *ord = (uint16_t *)(smem + L.ord);
-    uint16_t *pos = (uint16_t *)(smem + L.pos);
     uint32_t *U = (uint32_t *)(smem + L.U);
     uint32_t *bnd = (uint32_t *)(smem + L.bnd);
     uint32_t *Fw = (uint32_t *)(smem + L.Fw);
     uint32_t *Bw = (uint32_t *)(smem + L.Bw);
     uint32_t *cin = (uint32_t *)(smem + L.cin);
     int32_t *lbin = (int32_t *)(smem + L.lbin);
-
-    // ---- stage the adjacency (one coalesced pass, 128-bit loads) ----------
-    {
-        const uint4 *src = reinterpret_cast<const uint4 *>(adj_all + g * (long long)n * stride);
-        uint4 *dst = reinterpret_cast<uint4 *>(A32);
-        const int n16 = (n * stride) >> 4;
-        int k = lane;
-        for (; k + 96 < n16; k += 128) {
-            uint4 a = __ldg(src + k), b = __ldg(src + k + 32), c = __ldg(src + k + 64), d = __ldg(src + k + 96);
-            dst[k] = a; dst[k + 32] = b; dst[k + 64] = c; dst[k + 96] = d;
-        }
-        for (; k < n16; k += 32) dst[k] = __ldg(src + k);
-    }
     for (int w = lane; w < W; w += 32) {
         U[w] = (w == W - 1 && (n & 31)) ? mask_below(n & 31) : CH_FULL;
         bnd[w] = 0;
@@ -84,8 +98,6 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, int n, int stride, int
         bnd[0] |= 1u;
     }
     __syncwarp();
-
-    // ---- LexBFS (LOWEST_INDEX) -------------------------------------------
     int tail = 1;
     uint16_t *A = arrA, *An = arrB;
     for (int i = 0; i < n; ++i) {
@@ -105,8 +117,8 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, int n, int stride, int
         }
         const int x = A[i];
         if (lane == 0) {
-            ord[i] = (uint16_t)x;
-            pos[x] = (uint16_t)i;
+            ord[i] = x;
+            pos[x] = i;
         }
         const uint32_t *rowx = A32 + x * sw;
         const int R = tail - (i + 1);
@@ -121,7 +133,6 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, int n, int stride, int
             if (lane == 0) { Fw[q] = fw; Bw[q] = bw; }
         }
         uint32_t ext = lane < W ? (rowx[lane] & U[lane]) : 0u;
-        // early exit: nothing unreached and every reached class a singleton
         bool pred = true;
         if (lane < W) {
             if (U[lane]) pred = false;
@@ -138,13 +149,12 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, int n, int stride, int
         if (__all_sync(CH_FULL, pred)) {
             for (int p = i + 1 + lane; p < n; p += 32) {
                 int v = A[p];
-                ord[p] = (uint16_t)v;
-                pos[v] = (uint16_t)p;
+                ord[p] = v;
+                pos[v] = p;
             }
             break;
         }
         __syncwarp();
-        // word-level segmented scan (lane = relative word)
         uint32_t F = 0, B = 0;
         if (lane < Q) { F = Fw[lane]; B = Bw[lane]; }
         int iflag = B != 0;
@@ -243,35 +253,105 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, int n, int stride, int
         An = t2;
     }
     __syncwarp();
+}
+
+}  // namespace
+
+__global__ void __launch_bounds__(32)
+batch_chordal_kernel(const uint8_t *__restrict__ adj_all, int n, int stride, int32_t *__restrict__ orders,
+                     int32_t *__restrict__ witness) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const BatchLayout L(n, stride);
+    const int lane = threadIdx.x;
+    const int W = (n + 31) >> 5;
+    const int sw = stride >> 2;  // row pitch in 32-bit words
+    const long long g = blockIdx.x;
+    uint32_t *A32 = (uint32_t *)(smem + L.adj);
+    int32_t *ord = (int32_t *)(smem + L.ord);
+    int32_t *pos = (int32_t *)(smem + L.pos);
+    int32_t *par = (int32_t *)(smem + L.par);
+
+    // ---- stage the adjacency (one coalesced pass, 128-bit loads), count bits ---
+    int bits = 0;
+    {
+        const uint4 *src = reinterpret_cast<const uint4 *>(adj_all + g * (long long)n * stride);
+        uint4 *dst = reinterpret_cast<uint4 *>(A32);
+        const int n16 = (n * stride) >> 4;
+        int k = lane;
+        for (; k + 96 < n16; k += 128) {
+            uint4 a = __ldg(src + k), b = __ldg(src + k + 32), c = __ldg(src + k + 64), d = __ldg(src + k + 96);
+            dst[k] = a; dst[k + 32] = b; dst[k + 64] = c; dst[k + 96] = d;
+            bits += __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w) + __popc(b.x) + __popc(b.y) +
+                    __popc(b.z) + __popc(b.w) + __popc(c.x) + __popc(c.y) + __popc(c.z) + __popc(c.w) +
+                    __popc(d.x) + __popc(d.y) + __popc(d.z) + __popc(d.w);
+        }
+        for (; k < n16; k += 32) {
+            uint4 a = __ldg(src + k);
+            dst[k] = a;
+            bits += __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
+        }
+    }
+    bits = __reduce_add_sync(CH_FULL, bits);  // = 2m
+    __syncwarp();
+
+    // ---- LexBFS -------------------------------------------------------------------
+    const bool dense = (long long)bits * 8 > (long long)n * n;  // m > n^2/16
+    bool have_parent = false;
+    if (dense) {
+        arrangement_lexbfs_warp(A32, n, sw, smem, L, ord, pos);
+    } else {
+        SlotMem<uint16_t> M;
+        M.cls = (uint16_t *)(smem + L.cls);
+        M.slot_v = (uint16_t *)(smem + L.slot);
+        M.c_head = (int32_t *)(smem + L.c_head);
+        M.c_end = (int32_t *)(smem + L.c_end);
+        M.c_live = (uint16_t *)(smem + L.c_live);
+        M.c_prev = (uint16_t *)(smem + L.c_prev);
+        M.c_next = (uint16_t *)(smem + L.c_next);
+        M.c_tgt = (uint16_t *)(smem + L.c_tgt);
+        M.c_cnt = (uint16_t *)(smem + L.c_cnt);
+        M.c_split = (int32_t *)(smem + L.c_split);
+        M.freel = (uint16_t *)(smem + L.freel);
+        M.touched = (uint16_t *)(smem + L.touched);
+        M.scratch = (uint16_t *)(smem + L.scratch);
+        M.cap = L.cap;
+        BitsetSource<uint16_t> src{A32, sw, W, (uint16_t *)(smem + L.nbuf)};
+        slot_lexbfs<uint16_t, CHORDAL_TIE_ASCENDING>(src, n, M, ord, pos, par, 0, 0);
+        have_parent = true;
+    }
+    __syncwarp();
 
     // ---- write the order ---------------------------------------------------
     int32_t *og = orders + g * n;
     for (int k = lane; k < n; k += 32) og[k] = ord[k];
 
-    // ---- PEO check: lanes stride over vertices ---------------------------------
+    // ---- PEO check: lanes stride over vertices -----------------------------------
     unsigned long long best = ~0ULL;
     for (int v = lane; v < n; v += 32) {
         const int pv = pos[v];
         if (pv == 0) continue;
         const uint32_t *rv = A32 + v * sw;
-        int parent = -1;
-        const int lim = pv > 64 ? pv - 64 : 0;
-        for (int q = pv - 1; q >= lim; --q) {
-            int u = ord[q];
-            if ((rv[u >> 5] >> (u & 31)) & 1u) { parent = u; break; }
-        }
-        if (parent < 0 && lim > 0) {
-            int bp = -1;
-            for (int w = 0; w < W; ++w) {
-                uint32_t m = rv[w];
-                while (m) {
-                    int b = __ffs(m) - 1;
-                    m &= m - 1;
-                    int pu = pos[32 * w + b];
-                    if (pu < pv && pu > bp) bp = pu;
-                }
+        int parent = have_parent ? par[v] : -2;
+        if (parent == -2) {  // not produced by the search: backward scan, then full pass
+            parent = -1;
+            const int lim = pv > 64 ? pv - 64 : 0;
+            for (int q = pv - 1; q >= lim; --q) {
+                int u = ord[q];
+                if ((rv[u >> 5] >> (u & 31)) & 1u) { parent = u; break; }
             }
-            if (bp >= 0) parent = ord[bp];
+            if (parent < 0 && lim > 0) {
+                int bp = -1;
+                for (int w = 0; w < W; ++w) {
+                    uint32_t m = rv[w];
+                    while (m) {
+                        int b = __ffs(m) - 1;
+                        m &= m - 1;
+                        int pu = pos[32 * w + b];
+                        if (pu < pv && pu > bp) bp = pu;
+                    }
+                }
+                if (bp >= 0) parent = ord[bp];
+            }
         }
         if (parent < 0) continue;
         const unsigned long long k64 = ((unsigned long long)parent << 32) | (unsigned)v;

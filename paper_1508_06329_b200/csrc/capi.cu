@@ -11,8 +11,17 @@ int launch_lexbfs_dense(const uint8_t *, int64_t, int64_t, int32_t, uint64_t, ui
                         int32_t *, cudaStream_t);
 int launch_positions(const int32_t *, int64_t, int32_t *, cudaStream_t);
 int launch_key_init(uint64_t *, cudaStream_t);
-int launch_peo_dense_key(const uint8_t *, int64_t, int64_t, const int32_t *, const int32_t *, int64_t,
-                         int64_t, uint64_t *, cudaStream_t);
+int launch_peo_dense_key(const uint8_t *, int64_t, int64_t, const int32_t *, const int32_t *, const int32_t *,
+                         int64_t, int64_t, uint64_t *, cudaStream_t);
+size_t csr_workspace_bytes(int64_t);
+int launch_lexbfs_csr(const int64_t *, const int32_t *, int64_t, int32_t, uint64_t, uint64_t, int32_t *, int32_t *,
+                      int32_t *, void *, cudaStream_t);
+int launch_peo_csr_key(const int64_t *, const int32_t *, int64_t, const int32_t *, const int32_t *, int64_t, int64_t,
+                       uint64_t *, cudaStream_t);
+int launch_peo_csr_witness(const int64_t *, const int32_t *, const int32_t *, const uint64_t *, int32_t *,
+                           cudaStream_t);
+int launch_dense_degrees(const uint8_t *, int64_t, int64_t, int64_t *, cudaStream_t);
+int launch_dense_fill(const uint8_t *, int64_t, int64_t, const int64_t *, int32_t *, int64_t, cudaStream_t);
 int launch_peo_dense_witness(const uint8_t *, int64_t, int64_t, const int32_t *, const uint64_t *,
                              int32_t *, cudaStream_t);
 int launch_permute_dense(const uint8_t *, int64_t, int64_t, const int32_t *, uint8_t *, cudaStream_t);
@@ -68,15 +77,77 @@ const char *chordal_strerror(int status) {
     }
 }
 
-int chordal_lexbfs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int32_t tie_rule,
-                         uint64_t seed, int32_t *order_dev, int32_t *pos_dev, void *stream) {
+// Engine choice for a dense-stored graph: the arrangement engine when the
+// graph is dense enough that classes shatter into singletons within a few
+// steps (m > n^2/16), the O(deg) slot engine on a device-built CSR otherwise.
+static bool use_arrangement(int64_t n, int64_t m) { return n <= 64 || m * 16 > n * n; }
+
+struct DenseWs {  // workspace carve-up (bytes) of the dense entry points
+    size_t key, parent, indptr, indices, slot, total;
+    DenseWs(int64_t n, int64_t m) {
+        auto a = [](size_t x) { return (x + 255) & ~size_t(255); };
+        size_t o = 0;
+        key = o; o = a(o + 16);
+        parent = o; o = a(o + sizeof(int32_t) * (size_t)n);
+        indptr = indices = slot = o;
+        if (!use_arrangement(n, m)) {
+            indptr = o; o = a(o + sizeof(int64_t) * (size_t)(n + 1));
+            indices = o; o = a(o + sizeof(int32_t) * (size_t)(2 * m + 1));
+            slot = o; o = a(o + csr_workspace_bytes(n));
+        }
+        total = o;
+    }
+};
+
+static int count_edges_sync(const uint8_t *adj, int64_t n, int64_t stride, cudaStream_t s, int64_t *m_out) {
+    int64_t *ip = nullptr;
+    if (cudaMallocAsync((void **)&ip, sizeof(int64_t) * (n + 1), s) != cudaSuccess) return CHORDAL_ENOMEM;
+    int rc = launch_dense_degrees(adj, n, stride, ip, s);
+    int64_t tot = 0;
+    if (rc == CHORDAL_OK &&
+        cudaMemcpyAsync(&tot, ip + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s) != cudaSuccess)
+        rc = CHORDAL_ECUDA;
+    cudaFreeAsync(ip, s);
+    if (cudaStreamSynchronize(s) != cudaSuccess && rc == CHORDAL_OK) rc = CHORDAL_ECUDA;
+    *m_out = tot / 2;
+    return rc;
+}
+
+size_t chordal_dense_workspace_bytes(int64_t n, int64_t m) {
+    if (n < 0 || m < 0) return 0;
+    return DenseWs(n, m).total;
+}
+
+int chordal_lexbfs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int64_t m, int32_t tie_rule,
+                         uint64_t seed, int32_t *order_dev, int32_t *pos_dev, int32_t *parent_dev, void *ws,
+                         size_t ws_bytes, void *stream) {
     int rc = check_dense(adj_dev, n, stride);
     if (rc) return rc;
     if (n == 0) return CHORDAL_OK;
     if (!order_dev || !pos_dev) return CHORDAL_EINVAL;
     if (tie_rule < 0 || tie_rule > 2) return CHORDAL_EINVAL;
-    return launch_lexbfs_dense(adj_dev, n, stride, tie_rule, seed, current_cell(crc32_str("current")),
-                               order_dev, pos_dev, as_stream(stream));
+    cudaStream_t s = as_stream(stream);
+    if (m < 0) {
+        rc = count_edges_sync(adj_dev, n, stride, s, &m);
+        if (rc) return rc;
+    }
+    const DenseWs L(n, m);
+    const uint64_t cell = current_cell(crc32_str("current"));
+    if (use_arrangement(n, m)) {
+        if (parent_dev && cudaMemsetAsync(parent_dev, 0xFF, sizeof(int32_t) * n, s) != cudaSuccess)
+            return CHORDAL_ECUDA;  // the arrangement engine leaves parents to the PEO check
+        return launch_lexbfs_dense(adj_dev, n, stride, tie_rule, seed, cell, order_dev, pos_dev, s);
+    }
+    if (!ws || ws_bytes < L.total) return CHORDAL_EINVAL;
+    uint8_t *w = reinterpret_cast<uint8_t *>(ws);
+    int64_t *indptr = reinterpret_cast<int64_t *>(w + L.indptr);
+    int32_t *indices = reinterpret_cast<int32_t *>(w + L.indices);
+    rc = launch_dense_degrees(adj_dev, n, stride, indptr, s);
+    if (rc) return rc;
+    rc = launch_dense_fill(adj_dev, n, stride, indptr, indices, 2 * m + 1, s);
+    if (rc) return rc;
+    return launch_lexbfs_csr(indptr, indices, n, tie_rule, seed, cell, order_dev, pos_dev, parent_dev,
+                             w + L.slot, s);
 }
 
 int chordal_positions(const int32_t *order_dev, int64_t n, int32_t *pos_dev, void *stream) {
@@ -89,14 +160,14 @@ int chordal_key_init(uint64_t *key_dev, void *stream) {
     return launch_key_init(key_dev, as_stream(stream));
 }
 
-int chordal_peo_dense_key(const uint8_t *adj_dev, int64_t n, int64_t stride,
-                          const int32_t *order_dev, const int32_t *pos_dev, int64_t v_begin,
-                          int64_t v_end, uint64_t *key_dev, void *stream) {
+int chordal_peo_dense_key(const uint8_t *adj_dev, int64_t n, int64_t stride, const int32_t *order_dev,
+                          const int32_t *pos_dev, const int32_t *parent_dev, int64_t v_begin, int64_t v_end,
+                          uint64_t *key_dev, void *stream) {
     int rc = check_dense(adj_dev, n, stride);
     if (rc) return rc;
     if (n == 0) return CHORDAL_OK;
     if (!order_dev || !pos_dev || !key_dev) return CHORDAL_EINVAL;
-    return launch_peo_dense_key(adj_dev, n, stride, order_dev, pos_dev, v_begin, v_end, key_dev,
+    return launch_peo_dense_key(adj_dev, n, stride, order_dev, pos_dev, parent_dev, v_begin, v_end, key_dev,
                                 as_stream(stream));
 }
 
@@ -120,21 +191,36 @@ int chordal_peo_dense_witness(const uint8_t *adj_dev, int64_t n, int64_t stride,
 }
 
 int chordal_peo_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, const int32_t *order_dev,
-                      const int32_t *pos_dev, uint64_t *key_dev, int32_t *witness_dev,
+                      const int32_t *pos_dev, const int32_t *parent_dev, uint64_t *key_dev, int32_t *witness_dev,
                       void *stream) {
     int rc = chordal_key_init(key_dev, stream);
     if (rc) return rc;
-    rc = chordal_peo_dense_key(adj_dev, n, stride, order_dev, pos_dev, 0, n, key_dev, stream);
+    rc = chordal_peo_dense_key(adj_dev, n, stride, order_dev, pos_dev, parent_dev, 0, n, key_dev, stream);
     if (rc) return rc;
     return chordal_peo_dense_witness(adj_dev, n, stride, pos_dev, key_dev, witness_dev, stream);
 }
 
-int chordal_is_chordal_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int32_t tie_rule,
-                             uint64_t seed, int32_t *order_dev, int32_t *pos_dev,
-                             uint64_t *key_dev, int32_t *witness_dev, void *stream) {
-    int rc = chordal_lexbfs_dense(adj_dev, n, stride, tie_rule, seed, order_dev, pos_dev, stream);
+int chordal_is_chordal_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int64_t m, int32_t tie_rule,
+                             uint64_t seed, int32_t *order_dev, int32_t *pos_dev, void *ws, size_t ws_bytes,
+                             int32_t *witness_dev, void *stream) {
+    cudaStream_t s = as_stream(stream);
+    if (n > 0 && m < 0) {
+        int rc0 = check_dense(adj_dev, n, stride);
+        if (rc0) return rc0;
+        rc0 = count_edges_sync(adj_dev, n, stride, s, &m);
+        if (rc0) return rc0;
+    }
+    const DenseWs L(n, m < 0 ? 0 : m);
+    if (!ws || ws_bytes < L.total) return CHORDAL_EINVAL;
+    uint8_t *w = reinterpret_cast<uint8_t *>(ws);
+    uint64_t *key = reinterpret_cast<uint64_t *>(w + L.key);
+    int32_t *parent = reinterpret_cast<int32_t *>(w + L.parent);
+    int rc = chordal_lexbfs_dense(adj_dev, n, stride, m, tie_rule, seed, order_dev, pos_dev, parent, ws, ws_bytes,
+                                  stream);
     if (rc) return rc;
-    return chordal_peo_dense(adj_dev, n, stride, order_dev, pos_dev, key_dev, witness_dev, stream);
+    const bool have_parent = n > 0 && !use_arrangement(n, m);
+    return chordal_peo_dense(adj_dev, n, stride, order_dev, pos_dev, have_parent ? parent : nullptr, key,
+                             witness_dev, stream);
 }
 
 int chordal_is_chordal_dense_host(const uint8_t *adj_host, int64_t n, int64_t row_bytes,
@@ -151,26 +237,26 @@ int chordal_is_chordal_dense_host(const uint8_t *adj_host, int64_t n, int64_t ro
     const int64_t stride = (((n + 7) / 8) + 15) / 16 * 16;
     cudaStream_t s;
     if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return CHORDAL_ECUDA;
-    const size_t adj_bytes = (size_t)n * stride;
-    const size_t small = 16 + 12 + 2 * sizeof(int32_t) * (size_t)n;
-    uint8_t *dev = nullptr;
+    const size_t adj_bytes = ((size_t)n * stride + 255) & ~size_t(255);
+    uint8_t *adj = nullptr, *ws = nullptr;
+    int32_t *order = nullptr;
     int rc = CHORDAL_OK;
-    if (cudaMallocAsync((void **)&dev, adj_bytes + small + 256, s) != cudaSuccess) {
-        cudaStreamDestroy(s);
-        return CHORDAL_ENOMEM;
-    }
-    uint8_t *adj = dev;
-    uint64_t *key = reinterpret_cast<uint64_t *>(dev + ((adj_bytes + 15) & ~size_t(15)));
-    int32_t *wit = reinterpret_cast<int32_t *>(key + 2);
-    int32_t *order = wit + 4;
-    int32_t *pos = order + n;
+    int64_t m = -1;
     do {
-        if (stride != row_bytes) {
-            if (cudaMemsetAsync(adj, 0, adj_bytes, s) != cudaSuccess) { rc = CHORDAL_ECUDA; break; }
+        if (cudaMallocAsync((void **)&adj, adj_bytes + sizeof(int32_t) * (2 * n + 4), s) != cudaSuccess) {
+            rc = CHORDAL_ENOMEM;
+            break;
         }
-        if (cudaMemcpy2DAsync(adj, stride, adj_host, row_bytes, (n + 7) / 8, n,
-                              cudaMemcpyHostToDevice, s) != cudaSuccess) { rc = CHORDAL_ECUDA; break; }
-        rc = chordal_is_chordal_dense(adj, n, stride, tie_rule, seed, order, pos, key, wit, s);
+        order = reinterpret_cast<int32_t *>(adj + adj_bytes);
+        if (stride != row_bytes && cudaMemsetAsync(adj, 0, adj_bytes, s) != cudaSuccess) { rc = CHORDAL_ECUDA; break; }
+        if (cudaMemcpy2DAsync(adj, stride, adj_host, row_bytes, (n + 7) / 8, n, cudaMemcpyHostToDevice, s) !=
+            cudaSuccess) { rc = CHORDAL_ECUDA; break; }
+        rc = count_edges_sync(adj, n, stride, s, &m);
+        if (rc) break;
+        const size_t wsb = DenseWs(n, m).total;
+        if (cudaMallocAsync((void **)&ws, wsb + 16, s) != cudaSuccess) { rc = CHORDAL_ENOMEM; break; }
+        int32_t *wit = reinterpret_cast<int32_t *>(ws + wsb);
+        rc = chordal_is_chordal_dense(adj, n, stride, m, tie_rule, seed, order, order + n, ws, wsb, wit, s);
         if (rc) break;
         if (cudaMemcpyAsync(order_host, order, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
             cudaMemcpyAsync(witness_host, wit, sizeof(int32_t) * 3, cudaMemcpyDeviceToHost, s) != cudaSuccess) {
@@ -178,11 +264,71 @@ int chordal_is_chordal_dense_host(const uint8_t *adj_host, int64_t n, int64_t ro
             break;
         }
     } while (0);
-    cudaFreeAsync(dev, s);
+    if (ws) cudaFreeAsync(ws, s);
+    if (adj) cudaFreeAsync(adj, s);
     if (cudaStreamSynchronize(s) != cudaSuccess && rc == CHORDAL_OK) rc = CHORDAL_ECUDA;
     cudaStreamDestroy(s);
     if (rc == CHORDAL_OK) *chordal_out = witness_host[0] < 0 ? 1 : 0;
     return rc;
+}
+
+// ---- CSR -------------------------------------------------------------------
+
+size_t chordal_lexbfs_csr_workspace_bytes(int64_t n) { return n <= 0 ? 0 : csr_workspace_bytes(n); }
+
+int chordal_lexbfs_csr(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, int32_t tie_rule,
+                       uint64_t seed, int32_t *order_dev, int32_t *pos_dev, int32_t *parent_dev, void *ws,
+                       size_t ws_bytes, void *stream) {
+    if (n < 0) return CHORDAL_EINVAL;
+    if (n == 0) return CHORDAL_OK;
+    if (n > 0x7FFFFFF0LL / 2) return CHORDAL_ETOOLARGE;
+    if (!indptr_dev || !indices_dev || !order_dev || !pos_dev || !ws) return CHORDAL_EINVAL;
+    if (ws_bytes < csr_workspace_bytes(n)) return CHORDAL_EINVAL;
+    if (tie_rule < 0 || tie_rule > 2) return CHORDAL_EINVAL;
+    return launch_lexbfs_csr(indptr_dev, indices_dev, n, tie_rule, seed, current_cell(crc32_str("current")),
+                             order_dev, pos_dev, parent_dev, ws, as_stream(stream));
+}
+
+int chordal_peo_csr_key(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, const int32_t *pos_dev,
+                        const int32_t *parent_dev, int64_t v_begin, int64_t v_end, uint64_t *key_dev, void *stream) {
+    if (n < 0) return CHORDAL_EINVAL;
+    if (n == 0) return CHORDAL_OK;
+    if (!indptr_dev || !indices_dev || !pos_dev || !key_dev) return CHORDAL_EINVAL;
+    return launch_peo_csr_key(indptr_dev, indices_dev, n, pos_dev, parent_dev, v_begin, v_end, key_dev,
+                              as_stream(stream));
+}
+
+int chordal_peo_csr_witness(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n,
+                            const int32_t *pos_dev, const uint64_t *key_dev, int32_t *witness_dev, void *stream) {
+    if (n < 0 || !key_dev || !witness_dev) return CHORDAL_EINVAL;
+    if (n == 0) {
+        static const int32_t none[3] = {-1, -1, -1};
+        return cudaMemcpyAsync(witness_dev, none, sizeof(none), cudaMemcpyHostToDevice, as_stream(stream)) ==
+                       cudaSuccess ? CHORDAL_OK : CHORDAL_ECUDA;
+    }
+    if (!indptr_dev || !indices_dev || !pos_dev) return CHORDAL_EINVAL;
+    return launch_peo_csr_witness(indptr_dev, indices_dev, pos_dev, key_dev, witness_dev, as_stream(stream));
+}
+
+int chordal_peo_csr(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, const int32_t *pos_dev,
+                    const int32_t *parent_dev, uint64_t *key_dev, int32_t *witness_dev, void *stream) {
+    int rc = chordal_key_init(key_dev, stream);
+    if (rc) return rc;
+    rc = chordal_peo_csr_key(indptr_dev, indices_dev, n, pos_dev, parent_dev, 0, n, key_dev, stream);
+    if (rc) return rc;
+    return chordal_peo_csr_witness(indptr_dev, indices_dev, n, pos_dev, key_dev, witness_dev, stream);
+}
+
+int chordal_dense_to_csr(const uint8_t *adj_dev, int64_t n, int64_t stride, int64_t *indptr_dev,
+                         int32_t *indices_dev, void *stream) {
+    int rc = check_dense(adj_dev, n, stride);
+    if (rc) return rc;
+    if (!indptr_dev) return CHORDAL_EINVAL;
+    if (n == 0) return cudaMemsetAsync(indptr_dev, 0, sizeof(int64_t), as_stream(stream)) == cudaSuccess
+                           ? CHORDAL_OK : CHORDAL_ECUDA;
+    rc = launch_dense_degrees(adj_dev, n, stride, indptr_dev, as_stream(stream));
+    if (rc || !indices_dev) return rc;
+    return launch_dense_fill(adj_dev, n, stride, indptr_dev, indices_dev, INT64_MAX, as_stream(stream));
 }
 
 int chordal_permute_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, const int32_t *perm_dev,

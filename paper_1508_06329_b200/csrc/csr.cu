@@ -1,0 +1,315 @@
+// csr.cu -- sparse (CSR) chordality test: LexBFS via the slot engine with its
+// state in global memory (L2-resident), a vertex-parallel CSR PEO check, and
+// the bitset -> CSR conversion used to route sparse dense-stored graphs here.
+//
+// Replaces, for adjacency-list inputs, lexbfs_partition(method="linked")
+// (search.py:500-532) and _is_peo_lists (peo.py:100-149) -- the pair the
+// reference runs on graphs that only expose n, m and adjacency_lists0()
+// (the N = 10^6 configuration).
+#include "common.cuh"
+#include "slot_engine.cuh"
+
+namespace chordal {
+
+namespace {
+
+struct CsrWs {  // int32 workspace carve-up for the global-state slot engine
+    size_t cls, slot, c_head, c_end, c_live, c_prev, c_next, c_tgt, c_cnt, c_split, freel, touched, scratch, total;
+    int cap;
+    __host__ __device__ explicit CsrWs(long long n) {
+        const long long nc = n + 2;
+        cap = (int)(2 * n + 64);
+        size_t o = 0;
+        auto take = [&](long long words) { size_t r = o; o += (size_t)((words + 3) & ~3LL); return r; };
+        cls = take(n);
+        slot = take(cap);
+        c_head = take(nc);
+        c_end = take(nc);
+        c_live = take(nc);
+        c_prev = take(nc);
+        c_next = take(nc);
+        c_tgt = take(nc);
+        c_cnt = take(nc);
+        c_split = take(nc);
+        freel = take(nc);
+        touched = take(nc);
+        scratch = take(n);
+        total = o;  // in int32 words
+    }
+};
+
+__device__ __forceinline__ bool contains(const int32_t *__restrict__ a, int64_t lo, int64_t hi, int key) {
+    // lower_bound then equality test
+    int64_t l = lo, h = hi;
+    while (l < h) {
+        int64_t mid = (l + h) >> 1;
+        if (__ldg(a + mid) < key) l = mid + 1; else h = mid;
+    }
+    return l < hi && __ldg(a + l) == key;
+}
+
+}  // namespace
+
+template <int MODE>
+__global__ void __launch_bounds__(32, 1)
+lexbfs_csr_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices, int n, int32_t *ws,
+                  int32_t *__restrict__ order, int32_t *__restrict__ pos, int32_t *__restrict__ parent, uint64_t seed,
+                  uint64_t cell) {
+    const CsrWs L(n);
+    SlotMem<int32_t> M;
+    M.cls = ws + L.cls;
+    M.slot_v = ws + L.slot;
+    M.c_head = ws + L.c_head;
+    M.c_end = ws + L.c_end;
+    M.c_live = ws + L.c_live;
+    M.c_prev = ws + L.c_prev;
+    M.c_next = ws + L.c_next;
+    M.c_tgt = ws + L.c_tgt;
+    M.c_cnt = ws + L.c_cnt;
+    M.c_split = ws + L.c_split;
+    M.freel = ws + L.freel;
+    M.touched = ws + L.touched;
+    M.scratch = ws + L.scratch;
+    M.cap = L.cap;
+    CsrSource src{indptr, indices};
+    slot_lexbfs<int32_t, MODE>(src, n, M, order, pos, parent, seed, cell);
+}
+
+// ---------------------------------------------------------------------------
+// PEO check on CSR: one warp per vertex v in [v_begin, v_end).
+//   parent  given (from LexBFS) or the neighbour with the greatest position
+//           before pos(v) (peo.py:106-121);
+//   stray   some z in N(v), z != p, pos(z) < pos(p), z not in N(p) -- each
+//           candidate is looked up in p's sorted list by binary search.
+__global__ void __launch_bounds__(256)
+peo_csr_key_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices, int n,
+                   const int32_t *__restrict__ pos, const int32_t *__restrict__ parent_in, int v_begin, int v_end,
+                   unsigned long long *__restrict__ key) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    for (int v = v_begin + gw; v < v_end; v += nw) {
+        const int pv = __ldg(pos + v);
+        const int64_t b = __ldg(indptr + v), e = __ldg(indptr + v + 1);
+        int p = parent_in ? __ldg(parent_in + v) : -2;
+        if (p == -2) {  // unknown: max position among the neighbours preceding v
+            int best = -1;
+            for (int64_t k = b + lane; k < e; k += 32) {
+                int pu = __ldg(pos + __ldg(indices + k));
+                if (pu < pv && pu > best) best = pu;
+            }
+#pragma unroll
+            for (int d = 16; d >= 1; d >>= 1) best = max(best, __shfl_xor_sync(CH_FULL, best, d));
+            p = -1;
+            if (best >= 0) {
+                // the neighbour at that position
+                for (int64_t k = b + lane; k < e; k += 32) {
+                    int u = __ldg(indices + k);
+                    if (__ldg(pos + u) == best) p = u;
+                }
+#pragma unroll
+                for (int d = 16; d >= 1; d >>= 1) p = max(p, __shfl_xor_sync(CH_FULL, p, d));
+            }
+        }
+        if (p < 0) continue;
+        const unsigned long long k64 = ((unsigned long long)p << 32) | (unsigned)v;
+        if (k64 >= *(volatile unsigned long long *)key) continue;
+        const int pp = __ldg(pos + p);
+        const int64_t pb = __ldg(indptr + p), pe = __ldg(indptr + p + 1);
+        bool viol = false;
+        for (int64_t k0 = b; k0 < e; k0 += 32) {
+            int64_t k = k0 + lane;
+            if (k < e) {
+                int z = __ldg(indices + k);
+                if (z != p && __ldg(pos + z) < pp && !contains(indices, pb, pe, z)) viol = true;
+            }
+            if (__any_sync(CH_FULL, viol)) { viol = true; break; }
+        }
+        if (viol && lane == 0) atomicMin(key, k64);
+    }
+}
+
+__global__ void peo_csr_witness_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
+                                       const int32_t *__restrict__ pos, const unsigned long long *__restrict__ key,
+                                       int32_t *__restrict__ witness) {
+    const int lane = threadIdx.x & 31;
+    const unsigned long long k64 = *key;
+    if (k64 == ~0ULL) {
+        if (lane < 3) witness[lane] = -1;
+        return;
+    }
+    const int p = (int)(k64 >> 32), v = (int)(k64 & 0xFFFFFFFFu);
+    const int pp = pos[p];
+    const int64_t b = indptr[v], e = indptr[v + 1], pb = indptr[p], pe = indptr[p + 1];
+    int z = -1;
+    for (int64_t k0 = b; k0 < e; k0 += 32) {  // N(v) ascending: the first hit is the smallest z
+        int64_t k = k0 + lane;
+        bool hit = false;
+        int zz = 0;
+        if (k < e) {
+            zz = indices[k];
+            hit = zz != p && pos[zz] < pp && !contains(indices, pb, pe, zz);
+        }
+        uint32_t m = __ballot_sync(CH_FULL, hit);
+        if (m) {
+            z = __shfl_sync(CH_FULL, zz, __ffs(m) - 1);
+            break;
+        }
+    }
+    if (lane == 0) {
+        witness[0] = v;
+        witness[1] = p;
+        witness[2] = z;
+    }
+}
+
+// ---------------------------------------------------------------------------
+// bitset rows -> CSR (ascending per row)
+__global__ void row_degrees_kernel(const uint8_t *__restrict__ adj, int n, long long stride,
+                                   int64_t *__restrict__ deg) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    const int words = (n + 31) >> 5;
+    for (int r = gw; r < n; r += nw) {
+        const uint32_t *row = reinterpret_cast<const uint32_t *>(adj + (long long)r * stride);
+        int c = 0;
+        for (int w = lane; w < words; w += 32) c += __popc(__ldg(row + w));
+        c = __reduce_add_sync(CH_FULL, c);
+        if (lane == 0) deg[r + 1] = c;
+    }
+}
+
+// single-block inclusive scan of deg[1..n] in place -> indptr (deg[0] = 0)
+__global__ void scan_degrees_kernel(int64_t *__restrict__ indptr, int n) {
+    __shared__ int64_t wsum[32];
+    __shared__ int64_t carry;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) { carry = 0; indptr[0] = 0; }
+    __syncthreads();
+    for (int base = 0; base < n; base += blockDim.x) {
+        int i = base + tid;
+        int64_t v = i < n ? indptr[i + 1] : 0;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            int64_t o = __shfl_up_sync(CH_FULL, v, d);
+            if (lane >= d) v += o;
+        }
+        if (lane == 31) wsum[warp] = v;
+        __syncthreads();
+        if (warp == 0) {
+            int64_t s = lane < (int)(blockDim.x >> 5) ? wsum[lane] : 0;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                int64_t o = __shfl_up_sync(CH_FULL, s, d);
+                if (lane >= d) s += o;
+            }
+            wsum[lane] = s;
+        }
+        __syncthreads();
+        int64_t pre = carry + (warp > 0 ? wsum[warp - 1] : 0);
+        if (i < n) indptr[i + 1] = v + pre;
+        __syncthreads();
+        if (tid == blockDim.x - 1) carry = pre + v;
+        __syncthreads();
+    }
+}
+
+__global__ void fill_indices_kernel(const uint8_t *__restrict__ adj, int n, long long stride,
+                                    const int64_t *__restrict__ indptr, int32_t *__restrict__ indices,
+                                    long long cap) {
+    const int lane = threadIdx.x & 31;
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    const int words = (n + 31) >> 5;
+    for (int r = gw; r < n; r += nw) {
+        const uint32_t *row = reinterpret_cast<const uint32_t *>(adj + (long long)r * stride);
+        int64_t at = indptr[r];
+        for (int w0 = 0; w0 < words; w0 += 32) {
+            int w = w0 + lane;
+            uint32_t x = w < words ? __ldg(row + w) : 0u;
+            int c = __popc(x), incl = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                int o = __shfl_up_sync(CH_FULL, incl, d);
+                if (lane >= d) incl += o;
+            }
+            int64_t o = at + incl - c;
+            while (x) {
+                int b = __ffs(x) - 1;
+                x &= x - 1;
+                if (o < cap) indices[o] = 32 * w + b;  // never write past the caller's buffer
+                ++o;
+            }
+            at += __shfl_sync(CH_FULL, incl, 31);
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
+size_t csr_workspace_bytes(int64_t n) { return CsrWs(n).total * sizeof(int32_t); }
+
+int launch_lexbfs_csr(const int64_t *indptr, const int32_t *indices, int64_t n, int32_t tie_rule, uint64_t seed,
+                      uint64_t cell, int32_t *order, int32_t *pos, int32_t *parent, void *ws, cudaStream_t stream) {
+    int32_t *w = reinterpret_cast<int32_t *>(ws);
+    switch (tie_rule) {
+        case CHORDAL_TIE_ASCENDING:
+            lexbfs_csr_kernel<CHORDAL_TIE_ASCENDING><<<1, 32, 0, stream>>>(indptr, indices, (int)n, w, order, pos,
+                                                                             parent, seed, cell);
+            break;
+        case CHORDAL_TIE_DESCENDING:
+            lexbfs_csr_kernel<CHORDAL_TIE_DESCENDING><<<1, 32, 0, stream>>>(indptr, indices, (int)n, w, order, pos,
+                                                                              parent, seed, cell);
+            break;
+        case CHORDAL_TIE_SEEDED_ARB:
+            lexbfs_csr_kernel<CHORDAL_TIE_SEEDED_ARB><<<1, 32, 0, stream>>>(indptr, indices, (int)n, w, order, pos,
+                                                                              parent, seed, cell);
+            break;
+        default:
+            return CHORDAL_EINVAL;
+    }
+    CH_LAUNCH_CHECK();
+    return CHORDAL_OK;
+}
+
+int launch_peo_csr_key(const int64_t *indptr, const int32_t *indices, int64_t n, const int32_t *pos,
+                       const int32_t *parent, int64_t v_begin, int64_t v_end, uint64_t *key, cudaStream_t stream) {
+    if (v_begin < 0) v_begin = 0;
+    if (v_end > n) v_end = n;
+    if (v_end <= v_begin) return CHORDAL_OK;
+    long long blocks = ((v_end - v_begin) * 32 + 255) / 256;
+    if (blocks > 148LL * 16) blocks = 148LL * 16;
+    peo_csr_key_kernel<<<(int)blocks, 256, 0, stream>>>(indptr, indices, (int)n, pos, parent, (int)v_begin,
+                                                        (int)v_end, reinterpret_cast<unsigned long long *>(key));
+    CH_LAUNCH_CHECK();
+    return CHORDAL_OK;
+}
+
+int launch_peo_csr_witness(const int64_t *indptr, const int32_t *indices, const int32_t *pos, const uint64_t *key,
+                           int32_t *witness, cudaStream_t stream) {
+    peo_csr_witness_kernel<<<1, 32, 0, stream>>>(indptr, indices, pos,
+                                                 reinterpret_cast<const unsigned long long *>(key), witness);
+    CH_LAUNCH_CHECK();
+    return CHORDAL_OK;
+}
+
+int launch_dense_degrees(const uint8_t *adj, int64_t n, int64_t stride, int64_t *indptr, cudaStream_t stream) {
+    long long blocks = (n * 32 + 255) / 256;
+    if (blocks > 148LL * 16) blocks = 148LL * 16;
+    row_degrees_kernel<<<(int)blocks, 256, 0, stream>>>(adj, (int)n, stride, indptr);
+    CH_LAUNCH_CHECK();
+    scan_degrees_kernel<<<1, 1024, 0, stream>>>(indptr, (int)n);
+    CH_LAUNCH_CHECK();
+    return CHORDAL_OK;
+}
+
+int launch_dense_fill(const uint8_t *adj, int64_t n, int64_t stride, const int64_t *indptr, int32_t *indices,
+                      int64_t cap, cudaStream_t stream) {
+    long long blocks = (n * 32 + 255) / 256;
+    if (blocks > 148LL * 16) blocks = 148LL * 16;
+    fill_indices_kernel<<<(int)blocks, 256, 0, stream>>>(adj, (int)n, stride, indptr, indices, cap);
+    CH_LAUNCH_CHECK();
+    return CHORDAL_OK;
+}
+
+}  // namespace chordal

@@ -38,8 +38,9 @@ __device__ __forceinline__ bool row_bit(const uint32_t *row, int v) {
 
 __global__ void __launch_bounds__(256)
 peo_dense_key_kernel(const uint8_t *__restrict__ adj, int n, long long stride,
-                     const int32_t *__restrict__ order, const int32_t *__restrict__ pos, int v_begin,
-                     int v_end, unsigned long long *__restrict__ key) {
+                     const int32_t *__restrict__ order, const int32_t *__restrict__ pos,
+                     const int32_t *__restrict__ parent_in, int v_begin, int v_end,
+                     unsigned long long *__restrict__ key) {
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -48,10 +49,11 @@ peo_dense_key_kernel(const uint8_t *__restrict__ adj, int n, long long stride,
         const int pv = __ldg(pos + v);
         if (pv == 0) continue;
         const uint32_t *rowv = reinterpret_cast<const uint32_t *>(adj + (long long)v * stride);
-        // ---- parent: backward scan over the latest positions --------------
-        int parent = -1;
-        bool exhausted = false;
-        for (int r = 0; r < kBackRounds; ++r) {
+        // ---- parent: given by the search, else backward scan ---------------
+        int parent = parent_in ? __ldg(parent_in + v) : -2;  // -2: unknown, search it
+        bool exhausted = parent != -2;
+        if (parent == -2) parent = -1;
+        for (int r = 0; r < kBackRounds && !exhausted; ++r) {
             int q = pv - 1 - (32 * r + lane);
             bool hit = q >= 0 && row_bit(rowv, __ldg(order + q));
             uint32_t m = __ballot_sync(CH_FULL, hit);
@@ -168,7 +170,7 @@ int launch_key_init(uint64_t *key, cudaStream_t stream) {
 }
 
 int launch_peo_dense_key(const uint8_t *adj, int64_t n, int64_t stride, const int32_t *order,
-                         const int32_t *pos, int64_t v_begin, int64_t v_end, uint64_t *key,
+                         const int32_t *pos, const int32_t *parent, int64_t v_begin, int64_t v_end, uint64_t *key,
                          cudaStream_t stream) {
     if (v_begin < 0) v_begin = 0;
     if (v_end > n) v_end = n;
@@ -179,7 +181,7 @@ int launch_peo_dense_key(const uint8_t *adj, int64_t n, int64_t stride, const in
     const int64_t cap = 148LL * 16;
     if (blocks > cap) blocks = cap;
     peo_dense_key_kernel<<<(int)blocks, threads, 0, stream>>>(
-        adj, (int)n, stride, order, pos, (int)v_begin, (int)v_end,
+        adj, (int)n, stride, order, pos, parent, (int)v_begin, (int)v_end,
         reinterpret_cast<unsigned long long *>(key));
     CH_LAUNCH_CHECK();
     return CHORDAL_OK;

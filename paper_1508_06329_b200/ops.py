@@ -3,6 +3,7 @@
 Every function here launches CUDA work on the current torch stream and
 returns device tensors; the reference-shaped entry points in ``search``,
 ``peo`` and ``parallel`` convert to numpy / 1-based types at the edge.
+PyTorch only allocates memory and provides the stream.
 """
 
 from __future__ import annotations
@@ -20,20 +21,35 @@ def _i32(torch, n, dev):
     return torch.empty(max(n, 1), dtype=torch.int32, device=dev)
 
 
-def lexbfs(rows: DeviceRows, tie_rule: int = _native.TIE_ASCENDING, seed: int = 0, stream=None):
-    """LexBFS on device rows -> (order int32[n], pos int32[n]) device tensors."""
+def _ws(torch, nbytes, dev):
+    return torch.empty(max(int(nbytes), 16), dtype=torch.uint8, device=dev)
+
+
+def lexbfs(rows: DeviceRows, tie_rule: int = _native.TIE_ASCENDING, seed: int = 0, m: int = -1, stream=None,
+           want_parent: bool = False):
+    """LexBFS on device rows -> (order, pos[, parent]) int32 device tensors.
+
+    ``m`` is the edge count (chooses the engine); -1 lets the library count it.
+    """
     torch = _native.require_cuda()
-    n = rows.n
-    order = _i32(torch, n, rows.data.device)
-    pos = _i32(torch, n, rows.data.device)
+    n, dev = rows.n, rows.data.device
+    order, pos, parent = _i32(torch, n, dev), _i32(torch, n, dev), _i32(torch, n, dev)
     if n:
+        mm = m if m >= 0 else rows.m
+        ws = _ws(torch, lib.chordal_dense_workspace_bytes(n, mm) if mm >= 0 else _dense_ws_upper(n), dev)
         check(
-            lib.chordal_lexbfs_dense(
-                rows.ptr, n, rows.stride, tie_rule, seed & U64_MAX, ptr(order), ptr(pos), stream_ptr(stream)
-            ),
+            lib.chordal_lexbfs_dense(rows.ptr, n, rows.stride, mm, tie_rule, seed & U64_MAX, ptr(order), ptr(pos),
+                                     ptr(parent), ptr(ws), ws.numel(), stream_ptr(stream)),
             "chordal_lexbfs_dense",
         )
+    if want_parent:
+        return order[:n], pos[:n], parent[:n]
     return order[:n], pos[:n]
+
+
+def _dense_ws_upper(n: int) -> int:
+    """Workspace large enough for any m (the sparse engine only runs for m <= n^2/16)."""
+    return int(lib.chordal_dense_workspace_bytes(n, n * n // 16))
 
 
 def permute(rows: DeviceRows, perm0: np.ndarray, stream=None) -> DeviceRows:
@@ -43,7 +59,7 @@ def permute(rows: DeviceRows, perm0: np.ndarray, stream=None) -> DeviceRows:
     out = torch.empty_like(rows.data)
     check(lib.chordal_permute_dense(rows.ptr, rows.n, rows.stride, ptr(p), ptr(out), stream_ptr(stream)),
           "chordal_permute_dense")
-    return DeviceRows(rows.n, rows.stride, out)
+    return DeviceRows(rows.n, rows.stride, out, rows.m)
 
 
 def positions(order, stream=None):
@@ -55,24 +71,27 @@ def positions(order, stream=None):
     return pos[:n]
 
 
-def peo(rows: DeviceRows, order, pos, stream=None):
+def peo(rows: DeviceRows, order, pos, parent=None, stream=None):
     """PEO check -> witness int32[3] device tensor ((-1,-1,-1) when a PEO)."""
     torch = _native.require_cuda()
     key = torch.empty(1, dtype=torch.int64, device=rows.data.device)
     wit = torch.empty(4, dtype=torch.int32, device=rows.data.device)
+    n = rows.n
     check(
-        lib.chordal_peo_dense(rows.ptr, rows.n, rows.stride, ptr(order) if rows.n else None,
-                              ptr(pos) if rows.n else None, ptr(key), ptr(wit), stream_ptr(stream)),
+        lib.chordal_peo_dense(rows.ptr, n, rows.stride, ptr(order) if n else None, ptr(pos) if n else None,
+                              ptr(parent) if (n and parent is not None) else None, ptr(key), ptr(wit),
+                              stream_ptr(stream)),
         "chordal_peo_dense",
     )
     return wit[:3]
 
 
-def peo_key(rows: DeviceRows, order, pos, v_begin: int, v_end: int, key, stream=None):
+def peo_key(rows: DeviceRows, order, pos, v_begin: int, v_end: int, key, parent=None, stream=None):
     """Accumulate the minimum violation key of v in [v_begin, v_end) into ``key`` (int64[1])."""
     check(
-        lib.chordal_peo_dense_key(rows.ptr, rows.n, rows.stride, ptr(order), ptr(pos), v_begin, v_end,
-                                  ptr(key), stream_ptr(stream)),
+        lib.chordal_peo_dense_key(rows.ptr, rows.n, rows.stride, ptr(order), ptr(pos),
+                                  ptr(parent) if parent is not None else None, v_begin, v_end, ptr(key),
+                                  stream_ptr(stream)),
         "chordal_peo_dense_key",
     )
 
@@ -92,21 +111,92 @@ def peo_witness(rows: DeviceRows, pos, key, stream=None):
     return wit[:3]
 
 
-def is_chordal(rows: DeviceRows, tie_rule: int = _native.TIE_ASCENDING, seed: int = 0, stream=None):
+def is_chordal(rows: DeviceRows, tie_rule: int = _native.TIE_ASCENDING, seed: int = 0, m: int = -1, stream=None,
+               ws=None):
     """Fused pipeline -> (order, pos, witness) device tensors."""
     torch = _native.require_cuda()
-    n = rows.n
-    dev = rows.data.device
-    order = _i32(torch, n, dev)
-    pos = _i32(torch, n, dev)
-    key = torch.empty(1, dtype=torch.int64, device=dev)
+    n, dev = rows.n, rows.data.device
+    order, pos = _i32(torch, n, dev), _i32(torch, n, dev)
     wit = torch.empty(4, dtype=torch.int32, device=dev)
+    mm = m if m >= 0 else rows.m
+    if ws is None:
+        ws = _ws(torch, lib.chordal_dense_workspace_bytes(n, mm) if mm >= 0 else _dense_ws_upper(n), dev)
     check(
-        lib.chordal_is_chordal_dense(rows.ptr, n, rows.stride, tie_rule, seed & U64_MAX, ptr(order), ptr(pos),
-                                     ptr(key), ptr(wit), stream_ptr(stream)),
+        lib.chordal_is_chordal_dense(rows.ptr, n, rows.stride, mm, tie_rule, seed & U64_MAX, ptr(order), ptr(pos),
+                                     ptr(ws), ws.numel(), ptr(wit), stream_ptr(stream)),
         "chordal_is_chordal_dense",
     )
     return order[:n], pos[:n], wit[:3]
+
+
+def dense_workspace(n: int, m: int, device="cuda"):
+    torch = _native.require_cuda()
+    return _ws(torch, lib.chordal_dense_workspace_bytes(n, m) if m >= 0 else _dense_ws_upper(n), device)
+
+
+# ---------------------------------------------------------------- CSR ------
+
+
+def lexbfs_csr(indptr, indices, n: int, tie_rule: int = _native.TIE_ASCENDING, seed: int = 0, stream=None):
+    """LexBFS on device CSR -> (order, pos, parent) int32 device tensors."""
+    torch = _native.require_cuda()
+    dev = indptr.device
+    order, pos, parent = _i32(torch, n, dev), _i32(torch, n, dev), _i32(torch, n, dev)
+    if n:
+        ws = _ws(torch, lib.chordal_lexbfs_csr_workspace_bytes(n), dev)
+        check(
+            lib.chordal_lexbfs_csr(ptr(indptr), ptr(indices), n, tie_rule, seed & U64_MAX, ptr(order), ptr(pos),
+                                   ptr(parent), ptr(ws), ws.numel(), stream_ptr(stream)),
+            "chordal_lexbfs_csr",
+        )
+    return order[:n], pos[:n], parent[:n]
+
+
+def peo_csr(indptr, indices, n: int, pos, parent=None, stream=None):
+    torch = _native.require_cuda()
+    dev = indptr.device
+    key = torch.empty(1, dtype=torch.int64, device=dev)
+    wit = torch.empty(4, dtype=torch.int32, device=dev)
+    check(
+        lib.chordal_peo_csr(ptr(indptr), ptr(indices), n, ptr(pos) if n else None,
+                            ptr(parent) if (n and parent is not None) else None, ptr(key), ptr(wit),
+                            stream_ptr(stream)),
+        "chordal_peo_csr",
+    )
+    return wit[:3]
+
+
+def peo_csr_key(indptr, indices, n: int, pos, v_begin: int, v_end: int, key, parent=None, stream=None):
+    check(
+        lib.chordal_peo_csr_key(ptr(indptr), ptr(indices), n, ptr(pos), ptr(parent) if parent is not None else None,
+                                v_begin, v_end, ptr(key), stream_ptr(stream)),
+        "chordal_peo_csr_key",
+    )
+
+
+def peo_csr_witness(indptr, indices, n: int, pos, key, stream=None):
+    torch = _native.require_cuda()
+    wit = torch.empty(4, dtype=torch.int32, device=indptr.device)
+    check(lib.chordal_peo_csr_witness(ptr(indptr), ptr(indices), n, ptr(pos) if n else None, ptr(key), ptr(wit),
+                                      stream_ptr(stream)), "chordal_peo_csr_witness")
+    return wit[:3]
+
+
+def dense_to_csr(rows: DeviceRows, stream=None):
+    """Packed rows -> (indptr int64[n+1], indices int32[2m]) on the device."""
+    torch = _native.require_cuda()
+    n, dev = rows.n, rows.data.device
+    indptr = torch.empty(n + 1, dtype=torch.int64, device=dev)
+    check(lib.chordal_dense_to_csr(rows.ptr, n, rows.stride, ptr(indptr), None, stream_ptr(stream)),
+          "chordal_dense_to_csr")
+    nnz = int(indptr[n].item())
+    indices = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+    check(lib.chordal_dense_to_csr(rows.ptr, n, rows.stride, ptr(indptr), ptr(indices), stream_ptr(stream)),
+          "chordal_dense_to_csr")
+    return indptr, indices[:nnz]
+
+
+# -------------------------------------------------------------- batches ----
 
 
 def is_chordal_batch(adj, n: int, stride: int, stream=None):

@@ -16,9 +16,7 @@ of kernels 2-4 (set splices, counters) never change the order.
 
 from __future__ import annotations
 
-from .. import _native, ops
-from ..device import device_rows
-from ..errors import GraphTooLarge
+from .. import pipeline
 from ..graph import VertexOrdering
 from .engine import Arbitration
 
@@ -43,11 +41,4 @@ def parallel_lexbfs(g, arb: Arbitration, *, backend: str = "auto", workers: int 
     in the reference too, test_parallel_lexbfs.py:98-137, 152-184).
     """
     _check_backend(backend, audit, debug_labels, adj_reuse)
-    n = int(g.n)
-    if n == 0:
-        return VertexOrdering(())
-    if n > _native.DENSE_LEXBFS_MAX_N:
-        raise GraphTooLarge(f"n={n} exceeds the dense LexBFS kernel capacity {_native.DENSE_LEXBFS_MAX_N}")
-    rows = device_rows(g)
-    order, pos = ops.lexbfs(rows, arb.tie_rule, arb.seed or 0)
-    return VertexOrdering._trusted(order.cpu().numpy(), pos.cpu().numpy())
+    return pipeline.lexbfs(g, arb.tie_rule, arb.seed or 0)

@@ -10,11 +10,10 @@ extracts from the parallel ordering (parallel/peo.py:113).
 
 from __future__ import annotations
 
-from .. import _native, ops
-from ..device import device_rows
-from ..errors import GraphTooLarge, InvalidOrdering
-from ..graph import VertexOrdering, as_ordering
-from ..peo import ChordalityVerdict, WitnessTriple, _device_order
+from .. import pipeline
+from ..errors import InvalidOrdering
+from ..graph import as_ordering
+from ..peo import ChordalityVerdict, WitnessTriple
 from .engine import Arbitration
 from .lexbfs import _check_backend
 
@@ -27,23 +26,14 @@ def parallel_peo_test(g, ordering, *, backend: str = "auto", workers: int = 1) -
     _check_backend(backend, False, False, False)
     if g.n == 0:
         return True
-    rows = device_rows(g)
-    order, pos = _device_order(o, rows.data.device)
-    return ops.witness_tuple(ops.peo(rows, order, pos)) is None
+    return pipeline.peo_witness(g, o) is None
 
 
 def parallel_is_chordal(g, arb: Arbitration, *, backend: str = "auto",
                         workers: int = 1) -> ChordalityVerdict:
     """Parallel LexBFS followed by the parallel PEO test (parallel/peo.py:98-114)."""
     _check_backend(backend, False, False, False)
-    n = int(g.n)
-    if n == 0:
-        return ChordalityVerdict(True, peo=VertexOrdering(()))
-    if n > _native.DENSE_LEXBFS_MAX_N:
-        raise GraphTooLarge(f"n={n} exceeds the dense LexBFS kernel capacity {_native.DENSE_LEXBFS_MAX_N}")
-    rows = device_rows(g)
-    order, pos, wit = ops.is_chordal(rows, arb.tie_rule, arb.seed or 0)
-    w0 = ops.witness_tuple(wit)
+    order, w0 = pipeline.is_chordal(g, arb.tie_rule, arb.seed or 0)
     if w0 is None:
-        return ChordalityVerdict(True, peo=VertexOrdering._trusted(order.cpu().numpy(), pos.cpu().numpy()))
+        return ChordalityVerdict(True, peo=order)
     return ChordalityVerdict(False, witness=WitnessTriple(w0[0] + 1, w0[1] + 1, w0[2] + 1))

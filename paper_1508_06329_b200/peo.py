@@ -16,8 +16,7 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import _native, ops
-from .device import device_rows
+from . import _native, ops, pipeline
 from .errors import InvalidOrdering
 from .graph import VertexOrdering, as_ordering
 from .search import LOWEST_INDEX, TieBreak, lexbfs_labels, lexbfs_partition
@@ -106,9 +105,7 @@ def is_peo(g, ordering, *, stats: ScanStats | None = None, method: str = "auto")
         if stats is not None:
             stats.reads, stats.budget = 0, 0
         return True, None
-    rows = device_rows(g)
-    order, pos = _device_order(o, rows.data.device)
-    w0 = ops.witness_tuple(ops.peo(rows, order, pos))
+    w0 = pipeline.peo_witness(g, o)
     if stats is not None:
         stats.reads = _list_scan_reads(g, o, w0)
         stats.budget = 8 * int(g.m)
@@ -167,13 +164,7 @@ def is_chordal(g, algo: str = "partition", tie_break: TieBreak = LOWEST_INDEX, *
         order = fn(g, tie_break, method=lex_method)
         ok, w = is_peo(g, order)
         return ChordalityVerdict(True, peo=order) if ok else ChordalityVerdict(False, witness=w)
-    if n > _native.DENSE_LEXBFS_MAX_N:
-        from .errors import GraphTooLarge
-
-        raise GraphTooLarge(f"n={n} exceeds the dense LexBFS kernel capacity; use the CSR path")
-    rows = device_rows(g)
-    order, pos, wit = ops.is_chordal(rows, _native.TIE_ASCENDING)
-    w0 = ops.witness_tuple(wit)
+    order, w0 = pipeline.is_chordal(g, _native.TIE_ASCENDING)
     if w0 is None:
-        return ChordalityVerdict(True, peo=VertexOrdering._trusted(order.cpu().numpy(), pos.cpu().numpy()))
+        return ChordalityVerdict(True, peo=order)
     return ChordalityVerdict(False, witness=_witness(w0))

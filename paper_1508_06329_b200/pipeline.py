@@ -1,0 +1,55 @@
+"""Engine dispatch shared by the reference-shaped entry points.
+
+Dense inputs (``_packed`` rows) go through chordal_lexbfs_dense /
+chordal_is_chordal_dense (which pick the arrangement or slot engine by
+density); CSR inputs through the CSR kernels.  Everything returns host
+numpy arrays (0-based) at the end -- the only device->host copies of a call.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native, ops
+from .csr import device_csr, is_csr
+from .device import device_rows
+from .graph import VertexOrdering
+
+
+def lexbfs(g, tie_rule: int, seed: int = 0) -> VertexOrdering:
+    n = int(g.n)
+    if n == 0:
+        return VertexOrdering(())
+    if is_csr(g):
+        ip, ix = device_csr(g)
+        order, pos, _ = ops.lexbfs_csr(ip, ix, n, tie_rule, seed)
+    else:
+        order, pos = ops.lexbfs(device_rows(g), tie_rule, seed)
+    return VertexOrdering._trusted(order.cpu().numpy(), pos.cpu().numpy())
+
+
+def peo_witness(g, o: VertexOrdering):
+    """0-based witness of the PEO test of ordering ``o`` (None when a PEO)."""
+    torch = _native.require_cuda()
+    if is_csr(g):
+        ip, ix = device_csr(g)
+        order = torch.as_tensor(np.ascontiguousarray(o.order0, dtype=np.int32)).to(ip.device)
+        return ops.witness_tuple(ops.peo_csr(ip, ix, int(g.n), ops.positions(order)))
+    rows = device_rows(g)
+    order = torch.as_tensor(np.ascontiguousarray(o.order0, dtype=np.int32)).to(rows.data.device)
+    return ops.witness_tuple(ops.peo(rows, order, ops.positions(order)))
+
+
+def is_chordal(g, tie_rule: int, seed: int = 0):
+    """LexBFS + PEO test on the device: (VertexOrdering, 0-based witness or None)."""
+    n = int(g.n)
+    if n == 0:
+        return VertexOrdering(()), None
+    if is_csr(g):
+        ip, ix = device_csr(g)
+        order, pos, parent = ops.lexbfs_csr(ip, ix, n, tie_rule, seed)
+        wit = ops.peo_csr(ip, ix, n, pos, parent)
+    else:
+        order, pos, wit = ops.is_chordal(device_rows(g), tie_rule, seed)
+    w0 = ops.witness_tuple(wit)
+    return VertexOrdering._trusted(order.cpu().numpy(), pos.cpu().numpy()), w0

@@ -21,9 +21,9 @@ from dataclasses import dataclass
 
 import numpy as np
 
-from . import _native, ops
+from . import _native, ops, pipeline
+from .csr import is_csr
 from .device import device_rows
-from .errors import GraphTooLarge
 from .graph import VertexOrdering
 
 _ARRAY_MIN_N = 1024  # the reference's auto-dispatch threshold (search.py:29)
@@ -73,26 +73,19 @@ class LexLabel:
 
 def _run_lexbfs(g, tie_break: TieBreak, label: str, method: str) -> VertexOrdering:
     n = int(g.n)
-    if n == 0:
-        return VertexOrdering(())
-    if n > _native.DENSE_LEXBFS_MAX_N:
-        raise GraphTooLarge(
-            f"n={n} exceeds the dense LexBFS kernel capacity {_native.DENSE_LEXBFS_MAX_N}; use the CSR path"
-        )
-    rows = device_rows(g)
     if tie_break.seed is None:
-        order, pos = ops.lexbfs(rows, _native.TIE_ASCENDING)
-        return VertexOrdering._trusted(order.cpu().numpy(), pos.cpu().numpy())
-    if method != "array":
+        return pipeline.lexbfs(g, _native.TIE_ASCENDING)
+    if method != "array" or is_csr(g):
         raise NotImplementedError(
             "seeded tie-breaks of the linked reference methods (n < 1024 under method='auto') "
-            "are not replayed on the GPU yet; pass method='array'"
+            "are not replayed on the GPU yet; pass method='array' with a dense graph"
         )
+    if n == 0:
+        return VertexOrdering(())
     initial = np.asarray(tie_break.generator(label).permutation(n), dtype=np.int64)
-    perm = ops.permute(rows, initial)
+    perm = ops.permute(device_rows(g), initial)
     order_r, _ = ops.lexbfs(perm, _native.TIE_ASCENDING)
-    order0 = initial[order_r.cpu().numpy()]
-    return VertexOrdering._trusted(order0)
+    return VertexOrdering._trusted(initial[order_r.cpu().numpy()])
 
 
 def lexbfs_labels(g, tie_break: TieBreak = LOWEST_INDEX, *, debug: bool = False,

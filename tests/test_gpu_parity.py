@@ -353,7 +353,88 @@ def test_edge_cases():
     star = P.Graph.from_edge_list(32768, [(1, k) for k in range(2, 32769)], cap=32768)
     v = P.is_chordal(star)
     assert v.chordal and o0(v.peo) == list(range(32768))
+    # sparse graphs beyond the arrangement kernel's SMEM capacity take the slot engine
+    assert o0(P.lexbfs_partition(P.Graph.from_edge_list(32769, [], cap=40000))) == list(range(32769))
+    dense = P.Graph._from_packed(32800, gen_dense_random_device(32800, 0.5, 1)[0, :, :4100].cpu().numpy())
     with pytest.raises(P.GraphTooLarge):
-        P.lexbfs_partition(P.Graph.from_edge_list(32769, [], cap=40000))
+        P.lexbfs_partition(dense)
     with pytest.raises(P.GraphTooLarge):
         P.is_chordal_batch([P.Graph.from_edge_list(1025, [])])
+
+
+# ------------------------------------------------------------------- CSR ----
+
+
+def _csr_cases():
+    from paper_1508_06329_b200.csr import CSRGraph
+    from paper_1508_06329_b200.generate import chordal_random_edges
+
+    out = []
+    for n, k, seed in ((50, 3, 1), (700, 8, 2), (5000, 8, 3), (20000, 4, 4)):
+        u, v = chordal_random_edges(n, k, seed)
+        out.append((f"chordal{n}", CSRGraph.from_edges0(n, u, v)))
+        g = CSRGraph.from_edges0(n, u, v)
+        h, _ = remove_first_chord(P.Graph._from_packed(n, gen_chordal_random(n, k, seed, cap=n)._packed)) \
+            if n <= 5000 else (None, None)
+        if h is not None:
+            out.append((f"chordal{n}-chord", CSRGraph.from_dense(h)))
+    for n, p, seed in ((300, 0.02, 5), (3000, 0.002, 6)):
+        out.append((f"sparse{n}", CSRGraph.from_dense(gen_dense_random(n, p, seed))))
+    return out
+
+
+@pytest.mark.parametrize("name,g", _csr_cases(), ids=[c[0] for c in _csr_cases()])
+def test_csr_against_oracle(name, g):
+    n = g.n
+    order = oracle.lexbfs_partition_csr(g.indptr, g.indices, n)
+    ok, w = oracle.is_peo_csr(g.indptr, g.indices, n, order)
+    assert o0(P.lexbfs_partition(g)) == order.tolist()
+    v = P.is_chordal(g)
+    assert v.chordal == ok and w0(v.witness) == (None if w is None else list(w))
+    perm = np.random.default_rng(n).permutation(n)
+    ok2, w2 = oracle.is_peo_csr(g.indptr, g.indices, n, perm)
+    okg, wg = P.is_peo(g, P.VertexOrdering.from_zero_based(perm))
+    assert okg == ok2 and w0(wg) == (None if w2 is None else list(w2))
+    if n <= 5000:  # the arbitrated rules against the dense oracle
+        from paper_1508_06329_b200.graph import row_width
+
+        rows = np.zeros((n, n), dtype=bool)
+        for a in range(n):
+            rows[a, g.indices[g.indptr[a]:g.indptr[a + 1]]] = True
+        packed = np.packbits(rows, axis=1, bitorder="little")
+        for arb, mode, seed in ((DESC, oracle.ARB_DESCENDING, 0), (Arbitration.seeded(3), oracle.ARB_SEEDED, 3)):
+            assert o0(P.parallel_lexbfs(g, arb)) == oracle.lexbfs_arbitrated(packed, n, mode, seed).tolist()
+        assert packed.shape[1] == row_width(n)
+
+
+def test_dense_to_csr_roundtrip():
+    from paper_1508_06329_b200 import ops
+    from paper_1508_06329_b200.csr import CSRGraph
+
+    for g in (gen_chordal_random(3000, 8, 1), gen_dense_random(777, 0.3, 2), P.Graph.from_edge_list(5, [])):
+        from paper_1508_06329_b200.device import device_rows
+
+        ip, ix = ops.dense_to_csr(device_rows(g))
+        ref = CSRGraph.from_dense(g)
+        assert ip.cpu().numpy().tolist() == ref.indptr.tolist()
+        assert ix.cpu().numpy().tolist() == ref.indices.tolist()
+
+
+@pytest.mark.slow
+@pytest.mark.skipif("5" not in CONFIGS, reason="configs.json not generated")
+def test_config5_csr_million():
+    from paper_1508_06329_b200.csr import CSRGraph
+    from paper_1508_06329_b200.generate import chordal_random_edges
+
+    exp = CONFIGS["5"]
+    u, v = chordal_random_edges(exp["n"], exp["k"], exp["seed"])
+    g = CSRGraph.from_edges0(exp["n"], u, v)
+    assert sha(g.indptr) == exp["indptr_sha256"] and sha(g.indices) == exp["indices_sha256"]
+    vd = P.is_chordal(g)
+    assert vd.chordal and sha(vd.peo.order0.astype(np.int32)) == exp["order_sha256"]
+    a, b = exp["nonchordal"]["removed_edge0"]
+    keep = ~(((u == a) & (v == b)) | ((u == b) & (v == a)))
+    h = CSRGraph.from_edges0(exp["n"], u[keep], v[keep])
+    vn = P.is_chordal(h)
+    assert not vn.chordal and w0(vn.witness) == exp["nonchordal"]["witness"]
+    assert sha(P.lexbfs_partition(h).order0.astype(np.int32)) == exp["nonchordal"]["order_sha256"]
