@@ -1,8 +1,10 @@
 // batch.cu -- is_chordal over many small independent graphs (n <= 1024).
 //
-// One warp (= one CTA) per graph.  The graph's packed adjacency is staged in
-// shared memory once (a single pass over HBM, edges counted on the way), then
-// the warp runs one of two LexBFS engines and the PEO check.  Replaces
+// One warp (= one CTA) per graph.  A first coalesced pass over the graph's
+// packed rows counts the edges and pulls the rows from HBM into L2; the warp
+// then runs one of two LexBFS engines and the PEO check, reading rows through
+// L1/L2 while only the ~19 KB of search state lives in shared memory (so ~11
+// graphs are in flight per SM to hide the per-step latency).  Replaces
 // is_chordal (peo.py:177-202) called once per graph by the reference's bench
 // loop (bench.py:86-95).
 //
@@ -22,23 +24,22 @@ namespace chordal {
 
 namespace {
 
-struct BatchLayout {
-    size_t adj, ord, pos, par, uni, total;
+struct BatchLayout {  // shared memory per graph (one warp); the adjacency stays in global memory
+    size_t ord, pos, par, uni, total;
     // arrangement engine (inside uni)
-    size_t arrA, arrB, segtot, U, bnd, Fw, Bw, cin, lbin, arr_end;
+    size_t arrA, arrB, segtot, U, bnd, Fw, Bw, cin, lbin, rowbuf, arr_end;
     // slot engine (inside uni)
     size_t cls, slot, c_head, c_end, c_live, c_prev, c_next, c_tgt, c_cnt, c_split, freel, touched, scratch, nbuf,
         slot_end;
     int cap;
     __host__ __device__ static size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
-    __host__ __device__ BatchLayout(int n, int stride) {
+    __host__ __device__ BatchLayout(int n) {
         const int W = (n + 31) >> 5;
         const size_t np = size_t(W) * 32, nc = size_t(n) + 2;
         size_t o = 0;
-        adj = o; o = a16(o + size_t(n) * stride);
-        ord = o; o = a16(o + size_t(n) * 4);
-        pos = o; o = a16(o + size_t(n) * 4);
-        par = o; o = a16(o + size_t(n) * 4);
+        ord = o; o = a16(o + size_t(n) * 2);
+        pos = o; o = a16(o + size_t(n) * 2);
+        par = o; o = a16(o + size_t(n) * 2);
         uni = o;
         size_t u = o;
         arrA = u; u = a16(u + np * 2);
@@ -50,19 +51,20 @@ struct BatchLayout {
         Bw = u; u = a16(u + size_t(W + 1) * 4);
         cin = u; u = a16(u + size_t(W) * 4);
         lbin = u; u = a16(u + size_t(W) * 4);
+        rowbuf = u; u = a16(u + size_t(W) * 4);
         arr_end = u;
         cap = 2 * n + 64;
         u = o;
         cls = u; u = a16(u + size_t(n) * 2);
         slot = u; u = a16(u + size_t(cap) * 2);
-        c_head = u; u = a16(u + nc * 4);
-        c_end = u; u = a16(u + nc * 4);
+        c_head = u; u = a16(u + nc * 2);
+        c_end = u; u = a16(u + nc * 2);
         c_live = u; u = a16(u + nc * 2);
         c_prev = u; u = a16(u + nc * 2);
         c_next = u; u = a16(u + nc * 2);
         c_tgt = u; u = a16(u + nc * 2);
         c_cnt = u; u = a16(u + nc * 2);
-        c_split = u; u = a16(u + nc * 4);
+        c_split = u; u = a16(u + nc * 2);
         freel = u; u = a16(u + nc * 2);
         touched = u; u = a16(u + nc * 2);
         scratch = u; u = a16(u + size_t(n) * 2);
@@ -73,8 +75,8 @@ struct BatchLayout {
 };
 
 // Arrangement LexBFS (LOWEST_INDEX) for one graph in one warp; see lexbfs_dense.cu.
-__device__ void arrangement_lexbfs_warp(const uint32_t *A32, int n, int sw, uint8_t *smem, const BatchLayout &L,
-                                        int32_t *ord, int32_t *pos) {
+__device__ void arrangement_lexbfs_warp(const uint32_t *__restrict__ A32, int n, int sw, uint8_t *smem,
+                                        const BatchLayout &L, uint16_t *ord, uint16_t *pos) {
     const int lane = threadIdx.x & 31;
     const int W = (n + 31) >> 5;
     uint16_t *arrA = (uint16_t *)(smem + L.arrA);
@@ -86,6 +88,7 @@ __device__ void arrangement_lexbfs_warp(const uint32_t *A32, int n, int sw, uint
     uint32_t *Bw = (uint32_t *)(smem + L.Bw);
     uint32_t *cin = (uint32_t *)(smem + L.cin);
     int32_t *lbin = (int32_t *)(smem + L.lbin);
+    uint32_t *rowbuf = (uint32_t *)(smem + L.rowbuf);
     for (int w = lane; w < W; w += 32) {
         U[w] = (w == W - 1 && (n & 31)) ? mask_below(n & 31) : CH_FULL;
         bnd[w] = 0;
@@ -117,10 +120,12 @@ __device__ void arrangement_lexbfs_warp(const uint32_t *A32, int n, int sw, uint
         }
         const int x = A[i];
         if (lane == 0) {
-            ord[i] = x;
-            pos[x] = i;
+            ord[i] = (uint16_t)x;
+            pos[x] = (uint16_t)i;
         }
-        const uint32_t *rowx = A32 + x * sw;
+        if (lane < W) rowbuf[lane] = __ldg(A32 + x * sw + lane);  // pivot row: one L2 round trip
+        __syncwarp();
+        const uint32_t *rowx = rowbuf;
         const int R = tail - (i + 1);
         const int Q = (R + 31) >> 5;
         for (int q = 0; q < Q; ++q) {
@@ -149,8 +154,8 @@ __device__ void arrangement_lexbfs_warp(const uint32_t *A32, int n, int sw, uint
         if (__all_sync(CH_FULL, pred)) {
             for (int p = i + 1 + lane; p < n; p += 32) {
                 int v = A[p];
-                ord[p] = v;
-                pos[v] = p;
+                ord[p] = (uint16_t)v;
+                pos[v] = (uint16_t)p;
             }
             break;
         }
@@ -261,38 +266,35 @@ __global__ void __launch_bounds__(32)
 batch_chordal_kernel(const uint8_t *__restrict__ adj_all, int n, int stride, int32_t *__restrict__ orders,
                      int32_t *__restrict__ witness) {
     extern __shared__ __align__(16) uint8_t smem[];
-    const BatchLayout L(n, stride);
+    const BatchLayout L(n);
     const int lane = threadIdx.x;
     const int W = (n + 31) >> 5;
     const int sw = stride >> 2;  // row pitch in 32-bit words
     const long long g = blockIdx.x;
-    uint32_t *A32 = (uint32_t *)(smem + L.adj);
-    int32_t *ord = (int32_t *)(smem + L.ord);
-    int32_t *pos = (int32_t *)(smem + L.pos);
-    int32_t *par = (int32_t *)(smem + L.par);
+    const uint32_t *A32 = reinterpret_cast<const uint32_t *>(adj_all + g * (long long)n * stride);
+    uint16_t *ord = (uint16_t *)(smem + L.ord);
+    uint16_t *pos = (uint16_t *)(smem + L.pos);
+    uint16_t *par = (uint16_t *)(smem + L.par);
 
-    // ---- stage the adjacency (one coalesced pass, 128-bit loads), count bits ---
+    // ---- one coalesced 128-bit pass over the graph: edge count (engine choice)
+    //      and the HBM -> L2 fill for the row reads that follow ------------------
     int bits = 0;
     {
-        const uint4 *src = reinterpret_cast<const uint4 *>(adj_all + g * (long long)n * stride);
-        uint4 *dst = reinterpret_cast<uint4 *>(A32);
+        const uint4 *src = reinterpret_cast<const uint4 *>(A32);
         const int n16 = (n * stride) >> 4;
         int k = lane;
         for (; k + 96 < n16; k += 128) {
             uint4 a = __ldg(src + k), b = __ldg(src + k + 32), c = __ldg(src + k + 64), d = __ldg(src + k + 96);
-            dst[k] = a; dst[k + 32] = b; dst[k + 64] = c; dst[k + 96] = d;
             bits += __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w) + __popc(b.x) + __popc(b.y) +
                     __popc(b.z) + __popc(b.w) + __popc(c.x) + __popc(c.y) + __popc(c.z) + __popc(c.w) +
                     __popc(d.x) + __popc(d.y) + __popc(d.z) + __popc(d.w);
         }
         for (; k < n16; k += 32) {
             uint4 a = __ldg(src + k);
-            dst[k] = a;
             bits += __popc(a.x) + __popc(a.y) + __popc(a.z) + __popc(a.w);
         }
     }
     bits = __reduce_add_sync(CH_FULL, bits);  // = 2m
-    __syncwarp();
 
     // ---- LexBFS -------------------------------------------------------------------
     const bool dense = (long long)bits * 8 > (long long)n * n;  // m > n^2/16
@@ -303,14 +305,14 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, int n, int stride, int
         SlotMem<uint16_t> M;
         M.cls = (uint16_t *)(smem + L.cls);
         M.slot_v = (uint16_t *)(smem + L.slot);
-        M.c_head = (int32_t *)(smem + L.c_head);
-        M.c_end = (int32_t *)(smem + L.c_end);
+        M.c_head = (uint16_t *)(smem + L.c_head);
+        M.c_end = (uint16_t *)(smem + L.c_end);
         M.c_live = (uint16_t *)(smem + L.c_live);
         M.c_prev = (uint16_t *)(smem + L.c_prev);
         M.c_next = (uint16_t *)(smem + L.c_next);
         M.c_tgt = (uint16_t *)(smem + L.c_tgt);
         M.c_cnt = (uint16_t *)(smem + L.c_cnt);
-        M.c_split = (int32_t *)(smem + L.c_split);
+        M.c_split = (uint16_t *)(smem + L.c_split);
         M.freel = (uint16_t *)(smem + L.freel);
         M.touched = (uint16_t *)(smem + L.touched);
         M.scratch = (uint16_t *)(smem + L.scratch);
@@ -330,8 +332,8 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, int n, int stride, int
     for (int v = lane; v < n; v += 32) {
         const int pv = pos[v];
         if (pv == 0) continue;
-        const uint32_t *rv = A32 + v * sw;
-        int parent = have_parent ? par[v] : -2;
+        const uint32_t *__restrict__ rv = A32 + v * sw;
+        int parent = have_parent ? (int)(int16_t)par[v] : -2;
         if (parent == -2) {  // not produced by the search: backward scan, then full pass
             parent = -1;
             const int lim = pv > 64 ? pv - 64 : 0;
@@ -405,7 +407,7 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, int n, int stride, int
 
 int launch_batch(const uint8_t *adj, int64_t batch, int64_t n, int64_t stride, int32_t *orders,
                  int32_t *witness, cudaStream_t stream) {
-    const BatchLayout L((int)n, (int)stride);
+    const BatchLayout L((int)n);
     if (L.total > 227 * 1024) return CHORDAL_ETOOLARGE;
     cudaError_t e = cudaFuncSetAttribute(batch_chordal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                          (int)L.total);

@@ -44,10 +44,10 @@ template <typename I>
 struct SlotMem {
     I *cls;       // [n]   class of vertex, VISITED once consumed
     I *slot_v;    // [cap] vertex stored in a slot
-    int32_t *c_head, *c_end;        // [n+2] segment bounds (slot indices)
+    I *c_head, *c_end;              // [n+2] segment bounds (slot indices < cap)
     I *c_live, *c_prev, *c_next;    // [n+2]
     I *c_tgt, *c_cnt;               // [n+2] per-step split target / mover count
-    int32_t *c_split;               // [n+2] step that last touched the class
+    I *c_split;                     // [n+2] step that last touched the class
     I *freel;     // [n+2] free class ids
     I *touched;   // [n+2] classes touched in the current step
     I *scratch;   // [n]   compaction / neighbour staging buffer
@@ -133,8 +133,8 @@ __device__ int compact(const SlotMem<I> &M, int chead, int lane) {
         }
         __syncwarp();
         if (lane == 0) {
-            M.c_head[c] = start;
-            M.c_end[c] = top;
+            M.c_head[c] = (I)start;
+            M.c_end[c] = (I)top;
         }
     }
     __syncwarp();
@@ -145,12 +145,13 @@ __device__ int compact(const SlotMem<I> &M, int chead, int lane) {
 
 }  // namespace slot_detail
 
-// One warp runs the whole search.  Returns the number of positions written.
-// order[i], pos[v] (optional), parent[v] (optional, -1 for roots) are written.
+// One warp runs the whole search.  order[i], pos[v] (optional) and parent[v]
+// (optional; (I)-1 for roots, (I)-2 when left to the PEO check) are written,
+// in the engine's index type I.
 // MODE: CHORDAL_TIE_ASCENDING / DESCENDING / SEEDED_ARB.
 template <typename I, int MODE, typename Src>
-__device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I> &M, int32_t *__restrict__ order,
-                            int32_t *__restrict__ pos, int32_t *__restrict__ parent, uint64_t seed, uint64_t cell) {
+__device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I> &M, I *__restrict__ order, I *__restrict__ pos,
+                            I *__restrict__ parent, uint64_t seed, uint64_t cell) {
     using C = SlotConst<I>;
     const int lane = threadIdx.x & 31;
     // ---- initial partition: one class, segment in tie order ------------------
@@ -159,16 +160,16 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I> &M, int32_t 
         int sv = v;
         if (MODE == CHORDAL_TIE_DESCENDING) sv = v == 0 ? 0 : n - v;  // [0, n-1, ..., 1]
         M.slot_v[v] = (I)sv;
-        if (parent) parent[v] = -1;
+        if (parent) parent[v] = (I)-1;
     }
     for (int c = lane; c < n + 1; c += 32) M.freel[c] = (I)(n - c);  // pop from the top -> 1, 2, ...
     if (lane == 0) {
-        M.c_head[0] = 0;
-        M.c_end[0] = n;
+        M.c_head[0] = (I)0;
+        M.c_end[0] = (I)n;
         M.c_live[0] = (I)n;
         M.c_prev[0] = C::NIL;
         M.c_next[0] = C::NIL;
-        M.c_split[0] = -1;
+        M.c_split[0] = C::NIL;  // never equals a step index
     }
     __syncwarp();
     int chead = 0, nfree = n, top = n, nclasses = 1, nunv = n;
@@ -216,10 +217,10 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I> &M, int32_t 
         const int x = (int)M.slot_v[xs];
         __syncwarp();
         if (lane == 0) {
-            if (MODE != CHORDAL_TIE_SEEDED_ARB || xs == M.c_head[c0]) M.c_head[c0] = xs + 1;
+            if (MODE != CHORDAL_TIE_SEEDED_ARB || xs == (int)M.c_head[c0]) M.c_head[c0] = (I)(xs + 1);
             M.cls[x] = C::VISITED;
-            order[i] = x;
-            if (pos) pos[x] = i;
+            order[i] = (I)x;
+            if (pos) pos[x] = (I)i;
         }
         --nunv;
         const int live0 = (int)M.c_live[c0] - 1;
@@ -253,11 +254,11 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I> &M, int32_t 
                 }
                 if (lane == 0) {
                     int v = (int)M.slot_v[xs2];
-                    order[k] = v;
-                    if (pos) pos[v] = k;
+                    order[k] = (I)v;
+                    if (pos) pos[v] = (I)k;
                     // the skipped steps would still have refreshed this vertex's
                     // parent: leave it to the PEO check (PARENT_UNKNOWN)
-                    if (parent) parent[v] = -2;
+                    if (parent) parent[v] = (I)-2;
                     M.cls[v] = C::VISITED;
                 }
             }
@@ -274,15 +275,15 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I> &M, int32_t 
             int y = ok ? src.get(e) : 0;
             int c = ok ? (int)M.cls[y] : (int)C::VISITED;
             ok = ok && c != (int)C::VISITED;
-            if (ok && parent) parent[y] = x;
+            if (ok && parent) parent[y] = (I)x;
             uint32_t vm = __ballot_sync(CH_FULL, ok);
             uint32_t peers = __match_any_sync(CH_FULL, ok ? c : -1) & vm;
             bool leader = ok && (peers & lt) == 0;
             // first touch of a class in this step?
-            bool fresh = leader && M.c_split[c] != i;
+            bool fresh = leader && (int)M.c_split[c] != i;
             uint32_t fm = __ballot_sync(CH_FULL, fresh);
             if (fresh) {
-                M.c_split[c] = i;
+                M.c_split[c] = (I)i;
                 M.c_cnt[c] = (I)0;
                 M.touched[ntouch + __popc(fm & lt)] = (I)c;
             }
@@ -329,10 +330,10 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I> &M, int32_t 
                 if (split) {
                     const int d = (int)M.freel[nfree - 1 - rank];
                     const int start = top + incl - kk;
-                    M.c_head[d] = start;
-                    M.c_end[d] = start + k;
+                    M.c_head[d] = (I)start;
+                    M.c_end[d] = (I)(start + k);
                     M.c_live[d] = (I)k;
-                    M.c_split[d] = i;
+                    M.c_split[d] = (I)i;
                     M.c_cnt[d] = (I)0;
                     M.c_live[c] = (I)((int)M.c_live[c] - k);
                     M.c_tgt[c] = (I)d;
@@ -381,7 +382,7 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I> &M, int32_t 
             uint32_t peers = __match_any_sync(CH_FULL, ok ? c : -1) & vm;
             if (ok) {
                 int r = (int)M.c_cnt[c] + __popc(peers & lt);
-                M.slot_v[M.c_head[d] + r] = (I)y;
+                M.slot_v[(int)M.c_head[d] + r] = (I)y;
             }
             __syncwarp();
             if (ok) {
