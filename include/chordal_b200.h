@@ -73,7 +73,9 @@ size_t chordal_dense_workspace_bytes(int64_t n, int64_t m);
  * lexbfs_labels (search.py:262-268) and parallel_lexbfs (parallel/lexbfs.py:
  * 234-243).  Writes order_dev[n] (vertex at each position), pos_dev[n]
  * (position of each vertex) and, if parent_dev is not NULL, the PEO parent of
- * every vertex (-1 for none; all -1 when the dense engine ran, see below).
+ * every vertex (-1 for none, -2 for "not computed": all -2 when the dense
+ * engine ran, see below); the PEO checks accept -2 entries and search those
+ * parents themselves.
  * m is the edge count (Graph.m); pass m < 0 to let the call count the edges,
  * which synchronises `stream` once.  Engines: graphs with m > n^2/16 run the
  * persistent single-CTA arrangement kernel (n <= 32768); sparser graphs are

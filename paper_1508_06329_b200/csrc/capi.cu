@@ -10,6 +10,7 @@ namespace chordal {
 int launch_lexbfs_dense(const uint8_t *, int64_t, int64_t, int32_t, uint64_t, uint64_t, int32_t *,
                         int32_t *, cudaStream_t);
 int launch_positions(const int32_t *, int64_t, int32_t *, cudaStream_t);
+int launch_fill_i32(int32_t *, int64_t, int32_t, cudaStream_t);
 int launch_key_init(uint64_t *, cudaStream_t);
 int launch_peo_dense_key(const uint8_t *, int64_t, int64_t, const int32_t *, const int32_t *, const int32_t *,
                          int64_t, int64_t, uint64_t *, cudaStream_t);
@@ -134,8 +135,10 @@ int chordal_lexbfs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int6
     const DenseWs L(n, m);
     const uint64_t cell = current_cell(crc32_str("current"));
     if (use_arrangement(n, m)) {
-        if (parent_dev && cudaMemsetAsync(parent_dev, 0xFF, sizeof(int32_t) * n, s) != cudaSuccess)
-            return CHORDAL_ECUDA;  // the arrangement engine leaves parents to the PEO check
+        if (parent_dev) {  // the arrangement engine leaves parents to the PEO check (-2 = unknown)
+            rc = launch_fill_i32(parent_dev, n, -2, s);
+            if (rc) return rc;
+        }
         return launch_lexbfs_dense(adj_dev, n, stride, tie_rule, seed, cell, order_dev, pos_dev, s);
     }
     if (!ws || ws_bytes < L.total) return CHORDAL_EINVAL;

@@ -506,3 +506,21 @@ int launch_permute_dense(const uint8_t *adj, int64_t n, int64_t stride, const in
 }
 
 }  // namespace chordal
+
+namespace chordal {
+
+__global__ void fill_i32_kernel(int32_t *__restrict__ p, long long n, int32_t value) {
+    for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+        p[i] = value;
+}
+
+int launch_fill_i32(int32_t *p, int64_t n, int32_t value, cudaStream_t stream) {
+    if (n <= 0) return CHORDAL_OK;
+    long long blocks = (n + 255) / 256;
+    if (blocks > 148LL * 8) blocks = 148LL * 8;
+    fill_i32_kernel<<<(int)blocks, 256, 0, stream>>>(p, n, value);
+    CH_LAUNCH_CHECK();
+    return CHORDAL_OK;
+}
+
+}  // namespace chordal
