@@ -35,8 +35,8 @@ def lexbfs(rows: DeviceRows, tie_rule: int = _native.TIE_ASCENDING, seed: int = 
     n, dev = rows.n, rows.data.device
     order, pos, parent = _i32(torch, n, dev), _i32(torch, n, dev), _i32(torch, n, dev)
     if n:
-        mm = m if m >= 0 else rows.m
-        ws = _ws(torch, lib.chordal_dense_workspace_bytes(n, mm) if mm >= 0 else _dense_ws_upper(n), dev)
+        mm = m if m >= 0 else (rows.m if rows.m >= 0 else count_edges(rows, stream))
+        ws = _ws(torch, lib.chordal_dense_workspace_bytes(n, mm), dev)
         check(
             lib.chordal_lexbfs_dense(rows.ptr, n, rows.stride, mm, tie_rule, seed & U64_MAX, ptr(order), ptr(pos),
                                      ptr(parent), ptr(ws), ws.numel(), stream_ptr(stream)),
@@ -47,9 +47,14 @@ def lexbfs(rows: DeviceRows, tie_rule: int = _native.TIE_ASCENDING, seed: int = 
     return order[:n], pos[:n]
 
 
-def _dense_ws_upper(n: int) -> int:
-    """Workspace large enough for any m (the sparse engine only runs for m <= n^2/16)."""
-    return int(lib.chordal_dense_workspace_bytes(n, n * n // 16))
+def count_edges(rows: DeviceRows, stream=None) -> int:
+    """Edge count of device rows (one popcount pass + a 8-byte read-back)."""
+    torch = _native.require_cuda()
+    indptr = torch.empty(rows.n + 1, dtype=torch.int64, device=rows.data.device)
+    check(lib.chordal_dense_to_csr(rows.ptr, rows.n, rows.stride, ptr(indptr), None, stream_ptr(stream)),
+          "chordal_dense_to_csr")
+    rows.m = int(indptr[rows.n].item()) // 2
+    return rows.m
 
 
 def permute(rows: DeviceRows, perm0: np.ndarray, stream=None) -> DeviceRows:
@@ -118,9 +123,9 @@ def is_chordal(rows: DeviceRows, tie_rule: int = _native.TIE_ASCENDING, seed: in
     n, dev = rows.n, rows.data.device
     order, pos = _i32(torch, n, dev), _i32(torch, n, dev)
     wit = torch.empty(4, dtype=torch.int32, device=dev)
-    mm = m if m >= 0 else rows.m
+    mm = m if m >= 0 else (rows.m if rows.m >= 0 or n == 0 else count_edges(rows, stream))
     if ws is None:
-        ws = _ws(torch, lib.chordal_dense_workspace_bytes(n, mm) if mm >= 0 else _dense_ws_upper(n), dev)
+        ws = _ws(torch, lib.chordal_dense_workspace_bytes(n, max(mm, 0)), dev)
     check(
         lib.chordal_is_chordal_dense(rows.ptr, n, rows.stride, mm, tie_rule, seed & U64_MAX, ptr(order), ptr(pos),
                                      ptr(ws), ws.numel(), ptr(wit), stream_ptr(stream)),
@@ -131,7 +136,7 @@ def is_chordal(rows: DeviceRows, tie_rule: int = _native.TIE_ASCENDING, seed: in
 
 def dense_workspace(n: int, m: int, device="cuda"):
     torch = _native.require_cuda()
-    return _ws(torch, lib.chordal_dense_workspace_bytes(n, m) if m >= 0 else _dense_ws_upper(n), device)
+    return _ws(torch, lib.chordal_dense_workspace_bytes(n, m), device)
 
 
 # ---------------------------------------------------------------- CSR ------

@@ -355,9 +355,12 @@ def test_edge_cases():
     assert v.chordal and o0(v.peo) == list(range(32768))
     # sparse graphs beyond the arrangement kernel's SMEM capacity take the slot engine
     assert o0(P.lexbfs_partition(P.Graph.from_edge_list(32769, [], cap=40000))) == list(range(32769))
-    dense = P.Graph._from_packed(32800, gen_dense_random_device(32800, 0.5, 1)[0, :, :4100].cpu().numpy())
-    with pytest.raises(P.GraphTooLarge):
-        P.lexbfs_partition(dense)
+    # dense graphs beyond it too (CSR slot engine, early exit once classes are singletons)
+    dense = P.Graph._from_packed(32800, gen_dense_random_device(32800, 0.5, 1)[0, :, :4100].cpu().numpy(),)
+    ok, order, w = oracle.is_chordal(dense._packed, 32800)
+    v = P.is_chordal(dense)
+    assert not ok and not v.chordal and w0(v.witness) == list(w)
+    assert o0(P.lexbfs_partition(dense)) == order.tolist()
     with pytest.raises(P.GraphTooLarge):
         P.is_chordal_batch([P.Graph.from_edge_list(1025, [])])
 
