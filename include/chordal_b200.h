@@ -131,13 +131,15 @@ int chordal_is_chordal_dense_host(const uint8_t *adj_host, int64_t n, int64_t ro
 
 /* ---- CSR single graph (the N = 10^6 configuration) ---------------------- */
 
-/* Workspace of chordal_lexbfs_csr (about 60 bytes per vertex). */
-size_t chordal_lexbfs_csr_workspace_bytes(int64_t n);
+/* Workspace of chordal_lexbfs_csr for n vertices and m edges (m = indptr[n]/2;
+ * about 50 bytes per vertex + 4 per edge). */
+size_t chordal_lexbfs_csr_workspace_bytes(int64_t n, int64_t m);
 
-/* LexBFS on CSR adjacency with the slot engine (state in global memory):
+/* LexBFS on CSR adjacency with the slot engine:
  * lexbfs_partition(g, method="linked") (search.py:500-532) on a graph that
- * exposes adjacency_lists0().  parent_dev optional. */
-int chordal_lexbfs_csr(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, int32_t tie_rule,
+ * exposes adjacency_lists0().  For n <= 32768 the per-neighbour state lives in
+ * shared memory, above that in global memory.  parent_dev optional. */
+int chordal_lexbfs_csr(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, int64_t m, int32_t tie_rule,
                        uint64_t seed, int32_t *order_dev, int32_t *pos_dev, int32_t *parent_dev, void *ws,
                        size_t ws_bytes, void *stream);
 

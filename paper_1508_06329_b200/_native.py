@@ -35,8 +35,8 @@ SIGNATURES = {
     "chordal_peo_dense": [_P, _I64, _I64, _P, _P, _P, _P, _P, _P],
     "chordal_is_chordal_dense": [_P, _I64, _I64, _I64, _I32, _U64, _P, _P, _P, _SZ, _P, _P],
     "chordal_is_chordal_dense_host": [_P, _I64, _I64, _I32, _U64, _P, _P, _P],
-    "chordal_lexbfs_csr_workspace_bytes": [_I64],
-    "chordal_lexbfs_csr": [_P, _P, _I64, _I32, _U64, _P, _P, _P, _P, _SZ, _P],
+    "chordal_lexbfs_csr_workspace_bytes": [_I64, _I64],
+    "chordal_lexbfs_csr": [_P, _P, _I64, _I64, _I32, _U64, _P, _P, _P, _P, _SZ, _P],
     "chordal_peo_csr_key": [_P, _P, _I64, _P, _P, _I64, _I64, _P, _P],
     "chordal_peo_csr_witness": [_P, _P, _I64, _P, _P, _P, _P],
     "chordal_peo_csr": [_P, _P, _I64, _P, _P, _P, _P, _P],

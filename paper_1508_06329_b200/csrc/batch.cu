@@ -29,7 +29,7 @@ struct BatchLayout {  // shared memory per graph (one warp); the adjacency stays
     // arrangement engine (inside uni)
     size_t arrA, arrB, segtot, U, bnd, Fw, Bw, cin, lbin, rowbuf, arr_end;
     // slot engine (inside uni)
-    size_t cls, slot, c_head, c_end, c_live, c_prev, c_next, c_tgt, c_cnt, c_split, freel, touched, scratch, nbuf,
+    size_t cls, slot, c_head, c_end, c_live, c_prev, c_next, c_tgt, c_cnt, freel, touched, scratch, nbuf,
         slot_end;
     int cap;
     __host__ __device__ static size_t a16(size_t x) { return (x + 15) & ~size_t(15); }
@@ -56,7 +56,7 @@ struct BatchLayout {  // shared memory per graph (one warp); the adjacency stays
         cap = 2 * n + 64;
         u = o;
         cls = u; u = a16(u + size_t(n) * 2);
-        slot = u; u = a16(u + size_t(cap) * 2);
+        slot = u; u = a16(u + size_t(cap + slot_detail::kSlotPad) * 2);
         c_head = u; u = a16(u + nc * 2);
         c_end = u; u = a16(u + nc * 2);
         c_live = u; u = a16(u + nc * 2);
@@ -64,7 +64,6 @@ struct BatchLayout {  // shared memory per graph (one warp); the adjacency stays
         c_next = u; u = a16(u + nc * 2);
         c_tgt = u; u = a16(u + nc * 2);
         c_cnt = u; u = a16(u + nc * 2);
-        c_split = u; u = a16(u + nc * 2);
         freel = u; u = a16(u + nc * 2);
         touched = u; u = a16(u + nc * 2);
         scratch = u; u = a16(u + size_t(n) * 2);
@@ -302,7 +301,7 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, int n, int stride, int
     if (dense) {
         arrangement_lexbfs_warp(A32, n, sw, smem, L, ord, pos);
     } else {
-        SlotMem<uint16_t> M;
+        SlotMem<uint16_t, uint16_t> M;
         M.cls = (uint16_t *)(smem + L.cls);
         M.slot_v = (uint16_t *)(smem + L.slot);
         M.c_head = (uint16_t *)(smem + L.c_head);
@@ -312,13 +311,13 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, int n, int stride, int
         M.c_next = (uint16_t *)(smem + L.c_next);
         M.c_tgt = (uint16_t *)(smem + L.c_tgt);
         M.c_cnt = (uint16_t *)(smem + L.c_cnt);
-        M.c_split = (uint16_t *)(smem + L.c_split);
         M.freel = (uint16_t *)(smem + L.freel);
         M.touched = (uint16_t *)(smem + L.touched);
         M.scratch = (uint16_t *)(smem + L.scratch);
         M.cap = L.cap;
         BitsetSource<uint16_t> src{A32, sw, W, (uint16_t *)(smem + L.nbuf)};
-        slot_lexbfs<uint16_t, CHORDAL_TIE_ASCENDING>(src, n, M, ord, pos, par, 0, 0);
+        slot_lexbfs<uint16_t, uint16_t, CHORDAL_TIE_ASCENDING, BitsetSource<uint16_t>, uint16_t>(src, n, M, ord, pos,
+                                                                                                 par, 0, 0);
         have_parent = true;
     }
     __syncwarp();

@@ -14,8 +14,9 @@ int launch_fill_i32(int32_t *, int64_t, int32_t, cudaStream_t);
 int launch_key_init(uint64_t *, cudaStream_t);
 int launch_peo_dense_key(const uint8_t *, int64_t, int64_t, const int32_t *, const int32_t *, const int32_t *,
                          int64_t, int64_t, uint64_t *, cudaStream_t);
-size_t csr_workspace_bytes(int64_t);
-int launch_lexbfs_csr(const int64_t *, const int32_t *, int64_t, int32_t, uint64_t, uint64_t, int32_t *, int32_t *,
+size_t csr_workspace_bytes(int64_t, int64_t);
+int launch_lexbfs_csr(const int64_t *, const int32_t *, int64_t, int64_t, int32_t, uint64_t, uint64_t, int32_t *,
+                      int32_t *,
                       int32_t *, void *, cudaStream_t);
 int launch_peo_csr_key(const int64_t *, const int32_t *, int64_t, const int32_t *, const int32_t *, int64_t, int64_t,
                        uint64_t *, cudaStream_t);
@@ -78,14 +79,15 @@ const char *chordal_strerror(int status) {
     }
 }
 
-// Engine choice for a dense-stored graph.  The slot engine keeps its state in
-// global memory here, so every 32-neighbour chunk pays L2 latency; it wins
-// for low average degree (measured: N=8192 k=8 chordal 14 ms vs 56 ms), the
-// SMEM-resident arrangement engine wins above (N=32768 k=1024: 352 ms vs
-// 1.8 s) and for dense graphs, whose classes shatter within a few steps.
+// Engine choice for a dense-stored graph (measured on B200, tools/engine_compare.py):
+// the one-warp slot engine costs ~2 us per step plus ~0.5 us per 32 unvisited
+// neighbours, the single-CTA arrangement engine ~10 us per step at n = 32768
+// but exits early once classes are singletons.  Slot wins up to average degree
+// ~100 (n=32768 k=64: 81 vs 353 ms; n=8192 k=8: 15 vs 56 ms), arrangement for
+// very high degree (n=32768 k=1024, avg 1005: 355 vs 447 ms) and dense graphs.
 static bool use_arrangement(int64_t n, int64_t m) {
     if (n > CHORDAL_DENSE_LEXBFS_MAX_N) return false;
-    return n <= 64 || m > 16 * n;
+    return n <= 64 || m > 256 * n;
 }
 
 struct DenseWs {  // workspace carve-up (bytes) of the dense entry points
@@ -99,7 +101,7 @@ struct DenseWs {  // workspace carve-up (bytes) of the dense entry points
         if (!use_arrangement(n, m)) {
             indptr = o; o = a(o + sizeof(int64_t) * (size_t)(n + 1));
             indices = o; o = a(o + sizeof(int32_t) * (size_t)(2 * m + 1));
-            slot = o; o = a(o + csr_workspace_bytes(n));
+            slot = o; o = a(o + csr_workspace_bytes(n, m));
         }
         total = o;
     }
@@ -154,7 +156,7 @@ int chordal_lexbfs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int6
     if (rc) return rc;
     rc = launch_dense_fill(adj_dev, n, stride, indptr, indices, 2 * m + 1, s);
     if (rc) return rc;
-    return launch_lexbfs_csr(indptr, indices, n, tie_rule, seed, cell, order_dev, pos_dev, parent_dev,
+    return launch_lexbfs_csr(indptr, indices, n, m, tie_rule, seed, cell, order_dev, pos_dev, parent_dev,
                              w + L.slot, s);
 }
 
@@ -282,18 +284,20 @@ int chordal_is_chordal_dense_host(const uint8_t *adj_host, int64_t n, int64_t ro
 
 // ---- CSR -------------------------------------------------------------------
 
-size_t chordal_lexbfs_csr_workspace_bytes(int64_t n) { return n <= 0 ? 0 : csr_workspace_bytes(n); }
+size_t chordal_lexbfs_csr_workspace_bytes(int64_t n, int64_t m) {
+    return (n <= 0 || m < 0) ? 0 : csr_workspace_bytes(n, m);
+}
 
-int chordal_lexbfs_csr(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, int32_t tie_rule,
+int chordal_lexbfs_csr(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, int64_t m, int32_t tie_rule,
                        uint64_t seed, int32_t *order_dev, int32_t *pos_dev, int32_t *parent_dev, void *ws,
                        size_t ws_bytes, void *stream) {
-    if (n < 0) return CHORDAL_EINVAL;
+    if (n < 0 || m < 0) return CHORDAL_EINVAL;
     if (n == 0) return CHORDAL_OK;
     if (n > 0x7FFFFFF0LL / 2) return CHORDAL_ETOOLARGE;
     if (!indptr_dev || !indices_dev || !order_dev || !pos_dev || !ws) return CHORDAL_EINVAL;
-    if (ws_bytes < csr_workspace_bytes(n)) return CHORDAL_EINVAL;
+    if (ws_bytes < csr_workspace_bytes(n, m)) return CHORDAL_EINVAL;
     if (tie_rule < 0 || tie_rule > 2) return CHORDAL_EINVAL;
-    return launch_lexbfs_csr(indptr_dev, indices_dev, n, tie_rule, seed, current_cell(crc32_str("current")),
+    return launch_lexbfs_csr(indptr_dev, indices_dev, n, m, tie_rule, seed, current_cell(crc32_str("current")),
                              order_dev, pos_dev, parent_dev, ws, as_stream(stream));
 }
 

@@ -13,30 +13,39 @@ namespace chordal {
 
 namespace {
 
-struct CsrWs {  // int32 workspace carve-up for the global-state slot engine
-    size_t cls, slot, c_head, c_end, c_live, c_prev, c_next, c_tgt, c_cnt, c_split, freel, touched, scratch, total;
-    int cap;
-    __host__ __device__ explicit CsrWs(long long n) {
+// Workspace carve-up (bytes) of the slot engine's global-memory state: isz /
+// ssz = bytes of the vertex/class (I) and slot (S) index types.  The slot
+// capacity n + m + 64 covers every move of the search (each edge moves at most
+// one endpoint, once), so compaction never runs for single graphs.
+struct CsrWs {
+    size_t cls, slot, c_head, c_end, c_live, c_prev, c_next, c_tgt, c_cnt, freel, touched, scratch, total;
+    long long cap;
+    __host__ __device__ CsrWs(long long n, long long m, int isz, int ssz) {
         const long long nc = n + 2;
-        cap = (int)(2 * n + 64);
+        cap = n + m + 64;
         size_t o = 0;
-        auto take = [&](long long words) { size_t r = o; o += (size_t)((words + 3) & ~3LL); return r; };
-        cls = take(n);
-        slot = take(cap);
-        c_head = take(nc);
-        c_end = take(nc);
-        c_live = take(nc);
-        c_prev = take(nc);
-        c_next = take(nc);
-        c_tgt = take(nc);
-        c_cnt = take(nc);
-        c_split = take(nc);
-        freel = take(nc);
-        touched = take(nc);
-        scratch = take(n);
-        total = o;  // in int32 words
+        auto take = [&](long long elems, int sz) { size_t r = o; o += ((size_t)elems * sz + 15) & ~size_t(15); return r; };
+        cls = take(n, isz);
+        slot = take(cap + slot_detail::kSlotPad, isz);
+        c_head = take(nc, ssz);
+        c_end = take(nc, ssz);
+        c_live = take(nc, isz);
+        c_prev = take(nc, isz);
+        c_next = take(nc, isz);
+        c_tgt = take(nc, isz);
+        c_cnt = take(nc, isz);
+        freel = take(nc, isz);
+        touched = take(nc, isz);
+        scratch = take(n, isz);
+        total = o;
     }
 };
+
+// u16 vertex/class ids (NIL = 0xFFFF) for n <= 32768; the per-neighbour arrays
+// (cls, c_cnt, c_tgt) then fit in shared memory next to the staging buffer.
+constexpr long long kSmemMaxN = 32768;
+constexpr int kNbrBuf = 4096;  // neighbour-list staging entries
+inline size_t smem16_bytes(long long n) { return (size_t)(3 * n + 24 + kNbrBuf) * sizeof(uint16_t) + 64; }
 
 __device__ __forceinline__ bool contains(const int32_t *__restrict__ a, int64_t lo, int64_t hi, int key) {
     // lower_bound then equality test
@@ -50,29 +59,57 @@ __device__ __forceinline__ bool contains(const int32_t *__restrict__ a, int64_t 
 
 }  // namespace
 
+template <typename I, typename S>
+__device__ __forceinline__ SlotMem<I, S> carve(uint8_t *ws, const CsrWs &L) {
+    SlotMem<I, S> M;
+    M.cls = reinterpret_cast<I *>(ws + L.cls);
+    M.slot_v = reinterpret_cast<I *>(ws + L.slot);
+    M.c_head = reinterpret_cast<S *>(ws + L.c_head);
+    M.c_end = reinterpret_cast<S *>(ws + L.c_end);
+    M.c_live = reinterpret_cast<I *>(ws + L.c_live);
+    M.c_prev = reinterpret_cast<I *>(ws + L.c_prev);
+    M.c_next = reinterpret_cast<I *>(ws + L.c_next);
+    M.c_tgt = reinterpret_cast<I *>(ws + L.c_tgt);
+    M.c_cnt = reinterpret_cast<I *>(ws + L.c_cnt);
+    M.freel = reinterpret_cast<I *>(ws + L.freel);
+    M.touched = reinterpret_cast<I *>(ws + L.touched);
+    M.scratch = reinterpret_cast<I *>(ws + L.scratch);
+    M.cap = L.cap;
+    return M;
+}
+
+// Any n: all state in global memory (L2-resident), int32 ids; neighbour lists
+// staged through shared memory.
 template <int MODE>
 __global__ void __launch_bounds__(32, 1)
-lexbfs_csr_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices, int n, int32_t *ws,
-                  int32_t *__restrict__ order, int32_t *__restrict__ pos, int32_t *__restrict__ parent, uint64_t seed,
-                  uint64_t cell) {
-    const CsrWs L(n);
-    SlotMem<int32_t> M;
-    M.cls = ws + L.cls;
-    M.slot_v = ws + L.slot;
-    M.c_head = ws + L.c_head;
-    M.c_end = ws + L.c_end;
-    M.c_live = ws + L.c_live;
-    M.c_prev = ws + L.c_prev;
-    M.c_next = ws + L.c_next;
-    M.c_tgt = ws + L.c_tgt;
-    M.c_cnt = ws + L.c_cnt;
-    M.c_split = ws + L.c_split;
-    M.freel = ws + L.freel;
-    M.touched = ws + L.touched;
-    M.scratch = ws + L.scratch;
-    M.cap = L.cap;
-    CsrSource src{indptr, indices};
-    slot_lexbfs<int32_t, MODE>(src, n, M, order, pos, parent, seed, cell);
+lexbfs_csr_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices, int n, long long m,
+                  uint8_t *ws, int32_t *__restrict__ order, int32_t *__restrict__ pos, int32_t *__restrict__ parent,
+                  uint64_t seed, uint64_t cell) {
+    __shared__ int32_t nbuf[kNbrBuf];
+    const CsrWs L(n, m, 4, 4);
+    const SlotMem<int32_t, int32_t> M = carve<int32_t, int32_t>(ws, L);
+    CsrStagedSource<int32_t> src{indptr, indices, nbuf, kNbrBuf, 0};
+    slot_lexbfs<int32_t, int32_t, MODE, CsrStagedSource<int32_t>, int32_t>(src, n, M, order, pos, parent, seed, cell);
+}
+
+// n <= 32768: u16 ids; cls / c_cnt / c_tgt (192 KB at n = 32768) and the
+// neighbour staging buffer live in shared memory, so a 32-neighbour chunk
+// costs shared-memory latency only; class bookkeeping stays in global memory.
+template <int MODE>
+__global__ void __launch_bounds__(32, 1)
+lexbfs_csr_smem_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices, int n, long long m,
+                       uint8_t *ws, int32_t *__restrict__ order, int32_t *__restrict__ pos,
+                       int32_t *__restrict__ parent, uint64_t seed, uint64_t cell) {
+    extern __shared__ __align__(16) uint16_t sm16[];
+    const CsrWs L(n, m, 2, 4);
+    SlotMem<uint16_t, int32_t> M = carve<uint16_t, int32_t>(ws, L);
+    M.cls = sm16;
+    M.c_cnt = sm16 + ((n + 7) & ~7);
+    M.c_tgt = M.c_cnt + ((n + 2 + 7) & ~7);
+    uint16_t *nbuf = M.c_tgt + ((n + 2 + 7) & ~7);
+    CsrStagedSource<uint16_t> src{indptr, indices, nbuf, kNbrBuf, 0};
+    slot_lexbfs<uint16_t, int32_t, MODE, CsrStagedSource<uint16_t>, int32_t>(src, n, M, order, pos, parent, seed,
+                                                                              cell);
 }
 
 // ---------------------------------------------------------------------------
@@ -247,29 +284,43 @@ __global__ void fill_indices_kernel(const uint8_t *__restrict__ adj, int n, long
 }
 
 // ---------------------------------------------------------------------------
-size_t csr_workspace_bytes(int64_t n) { return CsrWs(n).total * sizeof(int32_t); }
+size_t csr_workspace_bytes(int64_t n, int64_t m) { return CsrWs(n, m, 4, 4).total; }
 
-int launch_lexbfs_csr(const int64_t *indptr, const int32_t *indices, int64_t n, int32_t tie_rule, uint64_t seed,
-                      uint64_t cell, int32_t *order, int32_t *pos, int32_t *parent, void *ws, cudaStream_t stream) {
-    int32_t *w = reinterpret_cast<int32_t *>(ws);
-    switch (tie_rule) {
-        case CHORDAL_TIE_ASCENDING:
-            lexbfs_csr_kernel<CHORDAL_TIE_ASCENDING><<<1, 32, 0, stream>>>(indptr, indices, (int)n, w, order, pos,
-                                                                             parent, seed, cell);
-            break;
-        case CHORDAL_TIE_DESCENDING:
-            lexbfs_csr_kernel<CHORDAL_TIE_DESCENDING><<<1, 32, 0, stream>>>(indptr, indices, (int)n, w, order, pos,
-                                                                              parent, seed, cell);
-            break;
-        case CHORDAL_TIE_SEEDED_ARB:
-            lexbfs_csr_kernel<CHORDAL_TIE_SEEDED_ARB><<<1, 32, 0, stream>>>(indptr, indices, (int)n, w, order, pos,
-                                                                              parent, seed, cell);
-            break;
-        default:
-            return CHORDAL_EINVAL;
+template <int MODE>
+static int launch_csr_mode(const int64_t *indptr, const int32_t *indices, int64_t n, int64_t m, uint64_t seed,
+                           uint64_t cell, int32_t *order, int32_t *pos, int32_t *parent, void *ws,
+                           cudaStream_t stream) {
+    uint8_t *w = reinterpret_cast<uint8_t *>(ws);
+    if (n <= kSmemMaxN) {
+        const size_t sm = smem16_bytes(n);
+        if (cudaFuncSetAttribute(lexbfs_csr_smem_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sm) != cudaSuccess)
+            return CHORDAL_ECUDA;
+        lexbfs_csr_smem_kernel<MODE><<<1, 32, sm, stream>>>(indptr, indices, (int)n, m, w, order, pos, parent, seed,
+                                                            cell);
+    } else {
+        lexbfs_csr_kernel<MODE><<<1, 32, 0, stream>>>(indptr, indices, (int)n, m, w, order, pos, parent, seed, cell);
     }
     CH_LAUNCH_CHECK();
     return CHORDAL_OK;
+}
+
+int launch_lexbfs_csr(const int64_t *indptr, const int32_t *indices, int64_t n, int64_t m, int32_t tie_rule,
+                      uint64_t seed, uint64_t cell, int32_t *order, int32_t *pos, int32_t *parent, void *ws,
+                      cudaStream_t stream) {
+    switch (tie_rule) {
+        case CHORDAL_TIE_ASCENDING:
+            return launch_csr_mode<CHORDAL_TIE_ASCENDING>(indptr, indices, n, m, seed, cell, order, pos, parent, ws,
+                                                          stream);
+        case CHORDAL_TIE_DESCENDING:
+            return launch_csr_mode<CHORDAL_TIE_DESCENDING>(indptr, indices, n, m, seed, cell, order, pos, parent, ws,
+                                                           stream);
+        case CHORDAL_TIE_SEEDED_ARB:
+            return launch_csr_mode<CHORDAL_TIE_SEEDED_ARB>(indptr, indices, n, m, seed, cell, order, pos, parent, ws,
+                                                           stream);
+        default:
+            return CHORDAL_EINVAL;
+    }
 }
 
 int launch_peo_csr_key(const int64_t *indptr, const int32_t *indices, int64_t n, const int32_t *pos,

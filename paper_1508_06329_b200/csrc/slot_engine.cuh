@@ -18,13 +18,14 @@
 //             skips dead slots 32 at a time);
 //             pass 1 over x's unvisited neighbours (chunks of 32 lanes):
 //               __match_any_sync groups lanes by class, leaders accumulate
-//               per-class move counts;
+//               per-class move counts (c_cnt == 0 marks an untouched class);
 //             allocate: a class whose members all move keeps its place (the
 //               "whole class moves in one hop" case, search.py:448-453);
 //               otherwise a new class d with a fresh segment of exactly the
-//               moved count is linked before c;
-//             pass 2 places each mover at d.head + (running count of earlier
-//               movers of c) -- the ascending-id order of the reference.
+//               moved count is linked before c -- all splits of a step at
+//               once (each insertion touches only its own cells);
+//             pass 2 places each mover at d's next free slot -- chunk order is
+//               ascending id, the reference's insertion order.
 //   early exit once #classes == #unvisited (every class a singleton): the
 //             rest of the order is the class list.
 // parent[y] = x is recorded for every unvisited neighbour y of x, so after
@@ -34,51 +35,94 @@
 // for the PEO check to compute.
 //
 // All state is addressed through plain pointers: the batch kernel passes
-// shared-memory arrays, the single-graph kernel global (L2-resident) ones.
+// shared-memory arrays, the single-graph kernels a mix of shared (the arrays
+// touched per neighbour) and global ones.  I is the vertex/class index type,
+// S the slot index type.
 #pragma once
 #include "common.cuh"
 
 namespace chordal {
 
-template <typename I>
+template <typename I, typename S>
 struct SlotMem {
-    I *cls;       // [n]   class of vertex, VISITED once consumed
-    I *slot_v;    // [cap] vertex stored in a slot
-    I *c_head, *c_end;              // [n+2] segment bounds (slot indices < cap)
-    I *c_live, *c_prev, *c_next;    // [n+2]
-    I *c_tgt, *c_cnt;               // [n+2] per-step split target / mover count
-    I *c_split;                     // [n+2] step that last touched the class
-    I *freel;     // [n+2] free class ids
-    I *touched;   // [n+2] classes touched in the current step
-    I *scratch;   // [n]   compaction / neighbour staging buffer
-    int32_t cap;  // slot capacity (>= 2n + 32: compaction leaves <= n live slots)
+    I *cls;                        // [n]   class of vertex, VISITED once consumed
+    I *slot_v;                     // [cap + kSlotPad] vertex stored in a slot (16-byte aligned)
+    S *c_head, *c_end;             // [n+2] segment bounds (slot indices < cap)
+    I *c_live, *c_prev, *c_next;   // [n+2]
+    I *c_tgt;                      // [n+2] split target of a touched class
+    I *c_cnt;                      // [n+2] movers (pass 1) / next free slot - step base (pass 2); 0 between steps
+    I *freel;                      // [n+2] free class ids
+    I *touched;                    // [n+2] classes touched in the current step
+    I *scratch;                    // [n]   compaction buffer
+    long long cap;                 // slot capacity (>= 2n + 32: compaction leaves <= n live slots)
 };
 
 template <typename I>
 struct SlotConst {
-    static constexpr I NIL = (I)~(I)0;      // no class / no link
+    static constexpr I NIL = (I)~(I)0;  // no class / no link
     static constexpr I VISITED = (I)~(I)0;
 };
 
-// Neighbour sources.  prepare(x, b, e) is warp-collective and yields the
-// ascending neighbour list of x as entries [b, e) read back with get(e).
-struct CsrSource {  // CSR rows in global memory
+// ---------------------------------------------------------------------------
+// Neighbour sources.  bounds(x) gives the ascending list as entries [b, e);
+// the engine walks it in blocks of at most capacity() entries, calling the
+// warp-collective stage(lo, hi) before reading entries of [lo, hi) with get().
+
+struct CsrSource {  // CSR rows read in place from global memory
     const int64_t *indptr;
     const int32_t *indices;
-    __device__ __forceinline__ void prepare(int x, int64_t &b, int64_t &e) const {
+    __device__ __forceinline__ void bounds(int x, int64_t &b, int64_t &e) const {
         b = __ldg(indptr + x);
         e = __ldg(indptr + x + 1);
     }
+    __device__ __forceinline__ int capacity() const { return 0x7FFFFFFF; }
+    __device__ __forceinline__ void stage(int64_t, int64_t) const {}
     __device__ __forceinline__ int get(int64_t e) const { return __ldg(indices + e); }
 };
 
+// CSR rows staged through a shared-memory buffer: each block of the pivot's
+// list is fetched with one burst of independent loads (one memory round trip
+// per block instead of one per 32-neighbour chunk).
+template <typename T>
+struct CsrStagedSource {
+    const int64_t *indptr;
+    const int32_t *indices;
+    T *buf;      // shared memory, bufcap entries
+    int bufcap;
+    mutable int64_t base;
+    __device__ __forceinline__ void bounds(int x, int64_t &b, int64_t &e) const {
+        b = __ldg(indptr + x);
+        e = __ldg(indptr + x + 1);
+    }
+    __device__ __forceinline__ int capacity() const { return bufcap; }
+    __device__ __forceinline__ void stage(int64_t lo, int64_t hi) const {
+        const int lane = threadIdx.x & 31;
+        const int cnt = (int)(hi - lo);
+        const int32_t *src = indices + lo;
+        int k = lane;
+        for (; k + 224 < cnt; k += 256) {
+            int32_t a[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a[j] = __ldg(src + k + 32 * j);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) buf[k + 32 * j] = (T)a[j];
+        }
+        for (; k < cnt; k += 32) buf[k] = (T)__ldg(src + k);
+        base = lo;
+        __syncwarp();
+    }
+    __device__ __forceinline__ int get(int64_t e) const { return (int)buf[e - base]; }
+};
+
+// Packed bitset row of n <= 1024 bits (generic pointer: smem or global); the
+// neighbour ids are compacted into nbuf by bounds().
 template <typename I>
-struct BitsetSource {  // packed row of n <= 1024 bits (generic pointer: smem or global)
+struct BitsetSource {
     const uint32_t *rows;
     int sw;      // row pitch in 32-bit words
     int words;   // ceil(n/32) <= 32
-    I *nbuf;     // [n] staging of the compacted neighbour ids
-    __device__ __forceinline__ void prepare(int x, int64_t &b, int64_t &e) const {
+    I *nbuf;     // [n]
+    __device__ __forceinline__ void bounds(int x, int64_t &b, int64_t &e) const {
         const int lane = threadIdx.x & 31;
         uint32_t w = lane < words ? rows[x * sw + lane] : 0u;
         int c = __popc(w), incl = c;
@@ -97,30 +141,87 @@ struct BitsetSource {  // packed row of n <= 1024 bits (generic pointer: smem or
         e = __shfl_sync(CH_FULL, incl, 31);
         __syncwarp();
     }
+    __device__ __forceinline__ int capacity() const { return 0x7FFFFFFF; }
+    __device__ __forceinline__ void stage(int64_t, int64_t) const {}
     __device__ __forceinline__ int get(int64_t e) const { return (int)nbuf[e]; }
 };
 
 namespace slot_detail {
 
-template <typename I>
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
     return m;
 }
 
+// Visits x's neighbour list in tie order (ascending; descending for the
+// DESCENDING rule) as chunks of 32 lanes: fn(valid, y).
+template <int MODE, typename Src, typename Fn>
+__device__ __forceinline__ void for_each_chunk(const Src &src, int64_t b, int64_t e, Fn &&fn) {
+    const int lane = threadIdx.x & 31;
+    const int64_t cap = src.capacity();
+    if (MODE == CHORDAL_TIE_DESCENDING) {
+        for (int64_t hi = e; hi > b; hi -= cap) {
+            const int64_t lo = hi - cap > b ? hi - cap : b;
+            src.stage(lo, hi);
+            for (int64_t c0 = hi; c0 > lo; c0 -= 32) {
+                const int64_t k = c0 - 1 - lane;
+                const bool ok = k >= lo;
+                fn(ok, ok ? src.get(k) : 0);
+            }
+        }
+    } else {
+        for (int64_t lo = b; lo < e; lo += cap) {
+            const int64_t hi = lo + cap < e ? lo + cap : e;
+            src.stage(lo, hi);
+            for (int64_t c0 = lo; c0 < hi; c0 += 32) {
+                const int64_t k = c0 + lane;
+                const bool ok = k < hi;
+                fn(ok, ok ? src.get(k) : 0);
+            }
+        }
+    }
+}
+
+// First live slot of class c in [h, e): each lane tests V = 16/sizeof(I)
+// consecutive slots fetched with one 16-byte load, so a warp skips 32*V dead
+// slots per memory round trip.  The slot array is padded by kSlotPad entries
+// and 16-byte aligned, so the over-read past e stays inside the allocation.
+constexpr int kSlotPad = 256;  // >= 32 * V for V = 8 (u16) and 4 (int32)
+template <typename I, typename S>
+__device__ __forceinline__ long long first_live(const SlotMem<I, S> &M, int c, long long h, long long e) {
+    constexpr int V = 16 / sizeof(I);
+    const int lane = threadIdx.x & 31;
+    for (long long base = h & ~(long long)(V - 1);; base += 32 * V) {
+        const long long s0 = base + (long long)lane * V;
+        const uint4 raw = *reinterpret_cast<const uint4 *>(M.slot_v + s0);
+        const I *vals = reinterpret_cast<const I *>(&raw);
+        int first = V;
+#pragma unroll
+        for (int j = V - 1; j >= 0; --j) {
+            const long long s = s0 + j;
+            if (s >= h && s < e && (int)M.cls[(int)vals[j]] == c) first = j;
+        }
+        const uint32_t m = __ballot_sync(CH_FULL, first < V);
+        if (m) {
+            const int src = __ffs(m) - 1;
+            return base + (long long)src * V + __shfl_sync(CH_FULL, first, src);
+        }
+    }
+}
+
 // Compacts the live members of every class (in class order) to the front of
 // the slot array.  Runs when the bump pointer would overflow.  Live members
 // are first gathered into scratch (size n) and then copied back, so segments
 // of classes not yet visited are never overwritten.
-template <typename I>
-__device__ int compact(const SlotMem<I> &M, int chead, int lane) {
-    int top = 0;
+template <typename I, typename S>
+__device__ long long compact(const SlotMem<I, S> &M, int chead, int lane) {
+    long long top = 0;
     for (int c = chead; c != (int)SlotConst<I>::NIL; c = (int)M.c_next[c]) {
-        const int h = M.c_head[c], e = M.c_end[c];
-        const int start = top;
-        for (int s0 = h; s0 < e; s0 += 32) {
-            int s = s0 + lane;
+        const long long h = (long long)M.c_head[c], e = (long long)M.c_end[c];
+        const long long start = top;
+        for (long long s0 = h; s0 < e; s0 += 32) {
+            const long long s = s0 + lane;
             bool live = false;
             int v = 0;
             if (s < e) {
@@ -128,17 +229,17 @@ __device__ int compact(const SlotMem<I> &M, int chead, int lane) {
                 live = (int)M.cls[v] == c;
             }
             uint32_t m = __ballot_sync(CH_FULL, live);
-            if (live) M.scratch[top + __popc(m & lanemask_lt<I>())] = (I)v;
+            if (live) M.scratch[top + __popc(m & lanemask_lt())] = (I)v;
             top += __popc(m);
         }
         __syncwarp();
         if (lane == 0) {
-            M.c_head[c] = (I)start;
-            M.c_end[c] = (I)top;
+            M.c_head[c] = (S)start;
+            M.c_end[c] = (S)top;
         }
     }
     __syncwarp();
-    for (int t = lane; t < top; t += 32) M.slot_v[t] = M.scratch[t];
+    for (long long t = lane; t < top; t += 32) M.slot_v[t] = M.scratch[t];
     __syncwarp();
     return top;
 }
@@ -146,47 +247,48 @@ __device__ int compact(const SlotMem<I> &M, int chead, int lane) {
 }  // namespace slot_detail
 
 // One warp runs the whole search.  order[i], pos[v] (optional) and parent[v]
-// (optional; (I)-1 for roots, (I)-2 when left to the PEO check) are written,
-// in the engine's index type I.
-// MODE: CHORDAL_TIE_ASCENDING / DESCENDING / SEEDED_ARB.
-template <typename I, int MODE, typename Src>
-__device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I> &M, I *__restrict__ order, I *__restrict__ pos,
-                            I *__restrict__ parent, uint64_t seed, uint64_t cell) {
+// (optional; (O)-1 for roots, (O)-2 when left to the PEO check) are written
+// in the output type O.  MODE: CHORDAL_TIE_ASCENDING / DESCENDING / SEEDED_ARB.
+template <typename I, typename S, int MODE, typename Src, typename O>
+__device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__restrict__ order, O *__restrict__ pos,
+                            O *__restrict__ parent, uint64_t seed, uint64_t cell) {
     using C = SlotConst<I>;
     const int lane = threadIdx.x & 31;
+    const uint32_t lt = slot_detail::lanemask_lt();
     // ---- initial partition: one class, segment in tie order ------------------
     for (int v = lane; v < n; v += 32) {
         M.cls[v] = 0;
         int sv = v;
         if (MODE == CHORDAL_TIE_DESCENDING) sv = v == 0 ? 0 : n - v;  // [0, n-1, ..., 1]
         M.slot_v[v] = (I)sv;
-        if (parent) parent[v] = (I)-1;
+        if (parent) parent[v] = (O)-1;
     }
     for (int c = lane; c < n + 1; c += 32) M.freel[c] = (I)(n - c);  // pop from the top -> 1, 2, ...
+    for (int c = lane; c < n + 2; c += 32) M.c_cnt[c] = (I)0;       // "untouched" outside a step
     if (lane == 0) {
-        M.c_head[0] = (I)0;
-        M.c_end[0] = (I)n;
+        M.c_head[0] = (S)0;
+        M.c_end[0] = (S)n;
         M.c_live[0] = (I)n;
         M.c_prev[0] = C::NIL;
         M.c_next[0] = C::NIL;
-        M.c_split[0] = C::NIL;  // never equals a step index
     }
     __syncwarp();
-    int chead = 0, nfree = n, top = n, nclasses = 1, nunv = n;
-    const uint32_t lt = slot_detail::lanemask_lt<I>();
+    int chead = 0, nfree = n, nclasses = 1, nunv = n;
+    long long top = n;
 
     for (int i = 0; i < n; ++i) {
         // ---- pivot: first live slot of the head class (or hash election) ----
         const int c0 = chead;
-        int h = M.c_head[c0];
-        const int e0 = M.c_end[c0];
-        int xs = -1;
+        long long h = (long long)M.c_head[c0];
+        const long long e0 = (long long)M.c_end[c0];
+        long long xs = -1;
         if (MODE == CHORDAL_TIE_SEEDED_ARB && i > 0) {
             const uint64_t prefix = mix64_3(seed, (uint64_t)(4 * (i - 1) + 3), cell);
             uint64_t best = 0;
-            int bs = -1, bv = -1;
-            for (int s0 = h; s0 < e0; s0 += 32) {
-                int s = s0 + lane;
+            long long bs = -1;
+            int bv = -1;
+            for (long long s0 = h; s0 < e0; s0 += 32) {
+                const long long s = s0 + lane;
                 if (s < e0) {
                     int v = (int)M.slot_v[s];
                     if ((int)M.cls[v] == c0) {
@@ -198,29 +300,21 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I> &M, I *__res
 #pragma unroll
             for (int d = 16; d >= 1; d >>= 1) {
                 uint64_t b2 = __shfl_xor_sync(CH_FULL, best, d);
-                int s2 = __shfl_xor_sync(CH_FULL, bs, d), v2 = __shfl_xor_sync(CH_FULL, bv, d);
+                long long s2 = __shfl_xor_sync(CH_FULL, bs, d);
+                int v2 = __shfl_xor_sync(CH_FULL, bv, d);
                 if (s2 >= 0 && (bs < 0 || b2 > best || (b2 == best && v2 > bv))) { best = b2; bs = s2; bv = v2; }
             }
             xs = bs;
         } else {
-            for (;; h += 32) {
-                int s = h + lane;
-                bool live = false;
-                if (s < e0) live = (int)M.cls[(int)M.slot_v[s]] == c0;
-                uint32_t m = __ballot_sync(CH_FULL, live);
-                if (m) {
-                    xs = h + __ffs(m) - 1;
-                    break;
-                }
-            }
+            xs = slot_detail::first_live<I, S>(M, c0, h, e0);
         }
         const int x = (int)M.slot_v[xs];
         __syncwarp();
         if (lane == 0) {
-            if (MODE != CHORDAL_TIE_SEEDED_ARB || xs == (int)M.c_head[c0]) M.c_head[c0] = (I)(xs + 1);
+            if (MODE != CHORDAL_TIE_SEEDED_ARB || xs == (long long)M.c_head[c0]) M.c_head[c0] = (S)(xs + 1);
             M.cls[x] = C::VISITED;
-            order[i] = (I)x;
-            if (pos) pos[x] = (I)i;
+            order[i] = (O)x;
+            if (pos) pos[x] = (O)i;
         }
         --nunv;
         const int live0 = (int)M.c_live[c0] - 1;
@@ -241,24 +335,15 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I> &M, I *__res
         if (nclasses == nunv) {
             int k = i + 1;
             for (int c = chead; c != (int)C::NIL; c = (int)M.c_next[c], ++k) {
-                int hh = M.c_head[c];
-                int xs2 = -1;
-                for (;; hh += 32) {
-                    int s = hh + lane;
-                    bool live = s < M.c_end[c] && (int)M.cls[(int)M.slot_v[s]] == c;
-                    uint32_t m = __ballot_sync(CH_FULL, live);
-                    if (m) {
-                        xs2 = hh + __ffs(m) - 1;
-                        break;
-                    }
-                }
+                const long long xs2 = slot_detail::first_live<I, S>(M, c, (long long)M.c_head[c],
+                                                                   (long long)M.c_end[c]);
                 if (lane == 0) {
                     int v = (int)M.slot_v[xs2];
-                    order[k] = (I)v;
-                    if (pos) pos[v] = (I)k;
+                    order[k] = (O)v;
+                    if (pos) pos[v] = (O)k;
                     // the skipped steps would still have refreshed this vertex's
-                    // parent: leave it to the PEO check (PARENT_UNKNOWN)
-                    if (parent) parent[v] = (I)-2;
+                    // parent: leave it to the PEO check (unknown = -2)
+                    if (parent) parent[v] = (O)-2;
                     M.cls[v] = C::VISITED;
                 }
             }
@@ -267,49 +352,40 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I> &M, I *__res
         }
         // ---- pass 1: count movers per class ----------------------------------
         int64_t nb0, nb1;
-        src.prepare(x, nb0, nb1);
+        src.bounds(x, nb0, nb1);
         int ntouch = 0;
-        for (int64_t e0c = nb0; e0c < nb1; e0c += 32) {
-            int64_t e = (MODE == CHORDAL_TIE_DESCENDING) ? nb1 - 1 - (e0c - nb0) - lane : e0c + lane;
-            bool ok = (MODE == CHORDAL_TIE_DESCENDING) ? e >= nb0 : e < nb1;
-            int y = ok ? src.get(e) : 0;
+        slot_detail::for_each_chunk<MODE>(src, nb0, nb1, [&](bool ok, int y) {
             int c = ok ? (int)M.cls[y] : (int)C::VISITED;
             ok = ok && c != (int)C::VISITED;
-            if (ok && parent) parent[y] = (I)x;
-            uint32_t vm = __ballot_sync(CH_FULL, ok);
-            uint32_t peers = __match_any_sync(CH_FULL, ok ? c : -1) & vm;
-            bool leader = ok && (peers & lt) == 0;
-            // first touch of a class in this step?
-            bool fresh = leader && (int)M.c_split[c] != i;
-            uint32_t fm = __ballot_sync(CH_FULL, fresh);
-            if (fresh) {
-                M.c_split[c] = (I)i;
-                M.c_cnt[c] = (I)0;
-                M.touched[ntouch + __popc(fm & lt)] = (I)c;
-            }
+            if (ok && parent) parent[y] = (O)x;
+            const uint32_t vm = __ballot_sync(CH_FULL, ok);
+            const uint32_t peers = __match_any_sync(CH_FULL, ok ? c : -1) & vm;
+            const bool leader = ok && (peers & lt) == 0;
+            const int old = leader ? (int)M.c_cnt[c] : 0;
+            const bool fresh = leader && old == 0;  // first touch in this step
+            const uint32_t fm = __ballot_sync(CH_FULL, fresh);
+            if (fresh) M.touched[ntouch + __popc(fm & lt)] = (I)c;
             ntouch += __popc(fm);
+            if (leader) M.c_cnt[c] = (I)(old + __popc(peers));
             __syncwarp();
-            if (leader) M.c_cnt[c] = (I)((int)M.c_cnt[c] + __popc(peers));
-            __syncwarp();
-        }
+        });
         if (ntouch == 0) continue;
         // ---- allocate new classes (lanes over touched classes) -----------------
         int need = 0;
         for (int t0 = 0; t0 < ntouch; t0 += 32) {
-            int t = t0 + lane;
+            const int t = t0 + lane;
             int k = 0;
             if (t < ntouch) {
-                int c = (int)M.touched[t];
+                const int c = (int)M.touched[t];
                 k = (int)M.c_cnt[c];
                 if (k == (int)M.c_live[c]) k = 0;  // whole class moves: stays in place
             }
             need += __reduce_add_sync(CH_FULL, k);
         }
-        if (top + need > M.cap) {
-            top = slot_detail::compact<I>(M, chead, lane);
-        }
+        if (top + need > M.cap) top = slot_detail::compact<I, S>(M, chead, lane);
+        const long long top0 = top;  // pass 2 slots are top0 + c_cnt[c] + rank
         for (int t0 = 0; t0 < ntouch; t0 += 32) {
-            int t = t0 + lane;
+            const int t = t0 + lane;
             int c = 0, k = 0;
             bool split = false;
             if (t < ntouch) {
@@ -317,80 +393,72 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I> &M, I *__res
                 k = (int)M.c_cnt[c];
                 split = k != (int)M.c_live[c];
             }
-            uint32_t sm = __ballot_sync(CH_FULL, split);
-            int rank = __popc(sm & lt);
-            // segment offsets: exclusive prefix of k over splitting lanes
-            int kk = split ? k : 0, incl = kk;
+            const uint32_t sm = __ballot_sync(CH_FULL, split);
+            const int rank = __popc(sm & lt);
+            // segment offsets: inclusive prefix of k over the splitting lanes
+            const int kk = split ? k : 0;
+            int incl = kk;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
                 int o = __shfl_up_sync(CH_FULL, incl, d);
                 if (lane >= d) incl += o;
             }
-            if (t < ntouch) {
-                if (split) {
-                    const int d = (int)M.freel[nfree - 1 - rank];
-                    const int start = top + incl - kk;
-                    M.c_head[d] = (I)start;
-                    M.c_end[d] = (I)(start + k);
-                    M.c_live[d] = (I)k;
-                    M.c_split[d] = (I)i;
-                    M.c_cnt[d] = (I)0;
-                    M.c_live[c] = (I)((int)M.c_live[c] - k);
-                    M.c_tgt[c] = (I)d;
-                    M.c_cnt[c] = (I)0;  // becomes the running rank of pass 2
-                } else {
-                    M.c_tgt[c] = (I)c;
-                }
+            int pold = 0;
+            if (split) {
+                const int d = (int)M.freel[nfree - 1 - rank];
+                const long long start = top + incl - kk;
+                M.c_head[d] = (S)start;
+                M.c_end[d] = (S)(start + k);
+                M.c_live[d] = (I)k;
+                M.c_cnt[d] = (I)0;
+                M.c_live[c] = (I)((int)M.c_live[c] - k);
+                M.c_tgt[c] = (I)d;
+                M.c_cnt[c] = (I)(start - top0);  // pass 2: next free slot of the new segment
+                pold = (int)M.c_prev[c];
+            } else if (t < ntouch) {
+                M.c_tgt[c] = (I)c;
             }
             const int nsplit = __popc(sm);
             top += __shfl_sync(CH_FULL, incl, 31);
             nfree -= nsplit;
             nclasses += nsplit;
             __syncwarp();
-            // link d before c (sequential over the splitting lanes keeps the
-            // list consistent when neighbouring classes split together)
-            for (uint32_t m = sm; m; m &= m - 1) {
-                const int src_lane = __ffs(m) - 1;
-                if (lane == src_lane) {
-                    const int d = (int)M.c_tgt[c];
-                    const int p = (int)M.c_prev[c];
-                    M.c_prev[d] = (I)p;
-                    M.c_next[d] = (I)c;
-                    M.c_prev[c] = (I)d;
-                    if (p != (int)C::NIL) M.c_next[p] = (I)d;
-                }
-                __syncwarp();
+            // link d before c, all splitting lanes at once: inserting d before
+            // c reads only c.prev and writes d.prev, d.next, c.prev and
+            // (old c.prev).next -- disjoint cells for distinct c, and no
+            // insertion writes another class's .prev, so concurrent inserts
+            // (even of adjacent classes) leave a consistent list.
+            if (split) {
+                const int d = (int)M.c_tgt[c];
+                M.c_prev[d] = (I)pold;
+                M.c_next[d] = (I)c;
+                M.c_prev[c] = (I)d;
+                if (pold != (int)C::NIL) M.c_next[pold] = (I)d;
             }
             __syncwarp();
             // chead may have been split: the new class precedes it
-            if (sm) {
-                int ch = chead;
-                if (M.c_prev[ch] != C::NIL) chead = (int)M.c_prev[ch];
-            }
+            if (sm && M.c_prev[chead] != C::NIL) chead = (int)M.c_prev[chead];
         }
         __syncwarp();
         // ---- pass 2: place the movers in ascending (tie) order -----------------
-        for (int64_t e0c = nb0; e0c < nb1; e0c += 32) {
-            int64_t e = (MODE == CHORDAL_TIE_DESCENDING) ? nb1 - 1 - (e0c - nb0) - lane : e0c + lane;
-            bool ok = (MODE == CHORDAL_TIE_DESCENDING) ? e >= nb0 : e < nb1;
-            int y = ok ? src.get(e) : 0;
+        slot_detail::for_each_chunk<MODE>(src, nb0, nb1, [&](bool ok, int y) {
             int c = ok ? (int)M.cls[y] : (int)C::VISITED;
             ok = ok && c != (int)C::VISITED;
-            int d = ok ? (int)M.c_tgt[c] : 0;
+            const int d = ok ? (int)M.c_tgt[c] : 0;
             ok = ok && d != c;  // whole-class moves need no slot change
-            uint32_t vm = __ballot_sync(CH_FULL, ok);
-            uint32_t peers = __match_any_sync(CH_FULL, ok ? c : -1) & vm;
+            const uint32_t vm = __ballot_sync(CH_FULL, ok);
+            const uint32_t peers = __match_any_sync(CH_FULL, ok ? c : -1) & vm;
             if (ok) {
-                int r = (int)M.c_cnt[c] + __popc(peers & lt);
-                M.slot_v[(int)M.c_head[d] + r] = (I)y;
-            }
-            __syncwarp();
-            if (ok) {
+                const int rel = (int)M.c_cnt[c];
+                M.slot_v[top0 + rel + __popc(peers & lt)] = (I)y;
                 M.cls[y] = (I)d;
-                if ((peers & lt) == 0) M.c_cnt[c] = (I)((int)M.c_cnt[c] + __popc(peers));
+                if ((peers & lt) == 0) M.c_cnt[c] = (I)(rel + __popc(peers));
             }
             __syncwarp();
-        }
+        });
+        // ---- restore c_cnt = 0 on the classes touched in this step -------------
+        for (int t = lane; t < ntouch; t += 32) M.c_cnt[(int)M.touched[t]] = (I)0;
+        __syncwarp();
     }
 }
 

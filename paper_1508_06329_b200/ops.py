@@ -142,15 +142,18 @@ def dense_workspace(n: int, m: int, device="cuda"):
 # ---------------------------------------------------------------- CSR ------
 
 
-def lexbfs_csr(indptr, indices, n: int, tie_rule: int = _native.TIE_ASCENDING, seed: int = 0, stream=None):
+def lexbfs_csr(indptr, indices, n: int, tie_rule: int = _native.TIE_ASCENDING, seed: int = 0, stream=None,
+               m: int | None = None):
     """LexBFS on device CSR -> (order, pos, parent) int32 device tensors."""
     torch = _native.require_cuda()
     dev = indptr.device
     order, pos, parent = _i32(torch, n, dev), _i32(torch, n, dev), _i32(torch, n, dev)
     if n:
-        ws = _ws(torch, lib.chordal_lexbfs_csr_workspace_bytes(n), dev)
+        if m is None:
+            m = int(indices.numel()) // 2
+        ws = _ws(torch, lib.chordal_lexbfs_csr_workspace_bytes(n, m), dev)
         check(
-            lib.chordal_lexbfs_csr(ptr(indptr), ptr(indices), n, tie_rule, seed & U64_MAX, ptr(order), ptr(pos),
+            lib.chordal_lexbfs_csr(ptr(indptr), ptr(indices), n, m, tie_rule, seed & U64_MAX, ptr(order), ptr(pos),
                                    ptr(parent), ptr(ws), ws.numel(), stream_ptr(stream)),
             "chordal_lexbfs_csr",
         )
