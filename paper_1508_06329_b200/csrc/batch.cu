@@ -357,16 +357,33 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, int n, int stride, int
         if (parent < 0) continue;
         const unsigned long long k64 = ((unsigned long long)parent << 32) | (unsigned)v;
         if (k64 >= best) continue;
-        const uint32_t *rp = A32 + parent * sw;
         const int pp = pos[parent];
+        const uint4 *rv4 = reinterpret_cast<const uint4 *>(rv);
+        const uint4 *rp4 = reinterpret_cast<const uint4 *>(A32 + parent * sw);
         bool viol = false;
-        for (int w = 0; w < W && !viol; ++w) {
-            uint32_t m = rv[w] & ~rp[w];
-            if ((parent >> 5) == w) m &= ~(1u << (parent & 31));
-            while (m) {
-                int b = __ffs(m) - 1;
-                m &= m - 1;
-                if (pos[32 * w + b] < pp) { viol = true; break; }
+        // 16 words (two rows x four 128-bit loads, all in flight) per round
+        for (int w0 = 0; w0 < W && !viol; w0 += 16) {
+            uint32_t a[16], b[16];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+                uint4 x = make_uint4(0, 0, 0, 0), y = make_uint4(0, 0, 0, 0);
+                if (w0 + 4 * j < W) {
+                    x = __ldg(rv4 + (w0 >> 2) + j);
+                    y = __ldg(rp4 + (w0 >> 2) + j);
+                }
+                a[4 * j] = x.x; a[4 * j + 1] = x.y; a[4 * j + 2] = x.z; a[4 * j + 3] = x.w;
+                b[4 * j] = y.x; b[4 * j + 1] = y.y; b[4 * j + 2] = y.z; b[4 * j + 3] = y.w;
+            }
+#pragma unroll
+            for (int j = 0; j < 16; ++j) {
+                const int w = w0 + j;
+                uint32_t m = a[j] & ~b[j];
+                if ((parent >> 5) == w) m &= ~(1u << (parent & 31));
+                while (m && !viol) {
+                    const int bb = __ffs(m) - 1;
+                    m &= m - 1;
+                    if (pos[32 * w + bb] < pp) viol = true;
+                }
             }
         }
         if (viol) best = k64;

@@ -192,6 +192,14 @@ template <typename I, typename S>
 __device__ __forceinline__ long long first_live(const SlotMem<I, S> &M, int c, long long h, long long e) {
     constexpr int V = 16 / sizeof(I);
     const int lane = threadIdx.x & 31;
+    if (__isShared(M.slot_v)) {  // shared-memory slots: one slot per lane is cheaper
+        for (;; h += 32) {
+            const long long s = h + lane;
+            const bool live = s < e && (int)M.cls[(int)M.slot_v[s]] == c;
+            const uint32_t m = __ballot_sync(CH_FULL, live);
+            if (m) return h + __ffs(m) - 1;
+        }
+    }
     for (long long base = h & ~(long long)(V - 1);; base += 32 * V) {
         const long long s0 = base + (long long)lane * V;
         const uint4 raw = *reinterpret_cast<const uint4 *>(M.slot_v + s0);
@@ -371,18 +379,20 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
         });
         if (ntouch == 0) continue;
         // ---- allocate new classes (lanes over touched classes) -----------------
-        int need = 0;
-        for (int t0 = 0; t0 < ntouch; t0 += 32) {
-            const int t = t0 + lane;
-            int k = 0;
-            if (t < ntouch) {
-                const int c = (int)M.touched[t];
-                k = (int)M.c_cnt[c];
-                if (k == (int)M.c_live[c]) k = 0;  // whole class moves: stays in place
+        if (top + (nb1 - nb0) > M.cap) {  // the movers need at most deg(x) slots
+            int need = 0;
+            for (int t0 = 0; t0 < ntouch; t0 += 32) {
+                const int t = t0 + lane;
+                int k = 0;
+                if (t < ntouch) {
+                    const int c = (int)M.touched[t];
+                    k = (int)M.c_cnt[c];
+                    if (k == (int)M.c_live[c]) k = 0;  // whole class moves: stays in place
+                }
+                need += __reduce_add_sync(CH_FULL, k);
             }
-            need += __reduce_add_sync(CH_FULL, k);
+            if (top + need > M.cap) top = slot_detail::compact<I, S>(M, chead, lane);
         }
-        if (top + need > M.cap) top = slot_detail::compact<I, S>(M, chead, lane);
         const long long top0 = top;  // pass 2 slots are top0 + c_cnt[c] + rank
         for (int t0 = 0; t0 < ntouch; t0 += 32) {
             const int t = t0 + lane;
