@@ -287,6 +287,27 @@ def single_graph_lines(with_cpu: bool) -> dict:
     measure("c1_chordal_k8", r1, g1._packed)
     measure("c1_nonchordal", DeviceRows(1000, 128, torch.from_numpy(
         np.pad(np.array(h1._packed), ((0, 0), (0, 3)))).cuda()), h1._packed)
+    # configuration 5 (N = 10^6 CSR, chordal k = 8): drawn on the GPU, LexBFS + PEO
+    from paper_1508_06329_b200.generate import gen_chordal_random_csr_device
+
+    t0 = time.perf_counter()
+    ip5, ix5 = gen_chordal_random_csr_device(1_000_000, 8, 0)
+    torch.cuda.synchronize()
+    gen5 = time.perf_counter() - t0
+    n5 = 1_000_000
+    lex5 = time_events(lambda: ops.lexbfs_csr(ip5, ix5, n5), reps=1, warm=1)
+    o5, p5, par5 = ops.lexbfs_csr(ip5, ix5, n5)
+    peo5 = time_events(lambda: ops.peo_csr(ip5, ix5, n5, p5, par5), reps=3)
+    w5 = ops.witness_tuple(ops.peo_csr(ip5, ix5, n5, p5, par5))
+    nnz = int(ix5.numel())
+    peo5_bytes = 2 * 4 * nnz + 8 * (n5 + 1) + 12 * n5  # both rows' index lists + indptr + pos/parent/order
+    out["c5_csr_chordal_k8_n1e6"] = {
+        "n": n5, "m": nnz // 2, "ms_per_graph": lex5 + peo5, "lexbfs_ms": lex5,
+        "lexbfs_ns_per_step": lex5 * 1e6 / n5, "peo_ms": peo5, "chordal": w5 is None,
+        "device_generation_s": gen5,
+        "peo_roofline": {"bound": "hbm", "achieved_gbs": peo5_bytes / (peo5 * 1e-3) / 1e9,
+                         "frac": peo5_bytes / (peo5 * 1e-3) / 1e9 / peaks["hbm_gbs"], "algorithmic_bytes": peo5_bytes},
+    }
     if with_cpu:
         import oracle
 
@@ -295,6 +316,15 @@ def single_graph_lines(with_cpu: bool) -> dict:
             t0 = time.perf_counter()
             oracle.is_chordal(packed, n)
             cpu[name] = {"ms_per_graph": (time.perf_counter() - t0) * 1e3, "cores": 1, "kind": "port"}
+        ip_h, ix_h = ip5.cpu().numpy(), ix5.cpu().numpy()
+        t0 = time.perf_counter()
+        o_h = oracle.lexbfs_partition_csr(ip_h, ix_h, n5)
+        t1 = time.perf_counter()
+        oracle.is_peo_csr(ip_h, ix_h, n5, o_h)
+        t2 = time.perf_counter()
+        cpu["c5_csr_chordal_k8_n1e6"] = {"ms_per_graph": (t2 - t0) * 1e3, "lexbfs_ms": (t1 - t0) * 1e3,
+                                         "peo_ms": (t2 - t1) * 1e3, "cores": 1, "kind": "port",
+                                         "same_order": bool((o_h == o5.cpu().numpy()).all())}
         out["cpu_baseline"] = cpu
     return out
 
@@ -412,6 +442,12 @@ def run_ours(args, rank, world, local):
 
     peaks, peak_kind = measured_peaks()
     achieved = B * BYTES_PER_GRAPH / (ms_per_step * 1e-3) / 1e9
+    traffic = None  # DRAM bytes per launch from the committed ncu --set full capture, scaled to this shard
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        t = json.load(open(tpath)).get("batch_chordal_kernel")
+        if t:
+            traffic = (t["dram_read_bytes"] + t["dram_write_bytes"]) * B / t["graphs_per_launch"]
     line = {
         "metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
@@ -421,7 +457,8 @@ def run_ours(args, rank, world, local):
                    "graphs": args.graphs, "graphs_per_rank": B, "l2": "inputs 2 GiB > L2, no flush needed",
                    "parallelism": f"batch-shard x{world}"},
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
-                     "frac": achieved / peaks["hbm_gbs"], "traffic": None,
+                     "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
+                     "algorithmic_bytes_per_launch": B * BYTES_PER_GRAPH,
                      "kernel": "batch_chordal_kernel", "peak_kind": peak_kind,
                      "algorithmic_bytes_per_graph": BYTES_PER_GRAPH},
         "e2e": {"value": e2e_value, "unit": "graphs/s", "h2d_bytes_per_step": B * N512 * STRIDE512,

@@ -209,6 +209,13 @@ int chordal_edges_to_dense(const int32_t *u_dev, const int32_t *v_dev, int64_t m
  * seed0 + b * seed_step.  Needs k + 2 <= 10000 and a device scratch of
  * chordal_gen_chordal_random_scratch_bytes(batch, n, k) bytes. */
 size_t chordal_gen_chordal_random_scratch_bytes(int64_t batch, int64_t n, int64_t k);
+
+/* Edge-list form for one large graph (the N = 10^6 configuration, whose
+ * dense matrix would not fit): the same draws, run by one GPU thread; writes
+ * the m attachment edges (u_dev[e], v_dev[e]) -- capacity n * (k + 1) -- and
+ * *m_dev.  scratch: chordal_gen_chordal_random_scratch_bytes(1, n, k). */
+int chordal_gen_chordal_random_edges(int64_t n, int64_t k, int64_t seed, int32_t *u_dev, int32_t *v_dev,
+                                     int64_t *m_dev, void *scratch_dev, size_t scratch_bytes, void *stream);
 int chordal_gen_chordal_random(uint8_t *adj_dev, int64_t batch, int64_t n, int64_t stride, int64_t k, int64_t seed0,
                                int64_t seed_step, void *scratch_dev, size_t scratch_bytes, void *stream);
 

@@ -48,6 +48,7 @@ SIGNATURES = {
     "chordal_edges_to_dense": [_P, _P, _I64, _P, _I64, _I64, _P],
     "chordal_gen_chordal_random_scratch_bytes": [_I64, _I64, _I64],
     "chordal_gen_chordal_random": [_P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _SZ, _P],
+    "chordal_gen_chordal_random_edges": [_I64, _I64, _I64, _P, _P, _P, _P, _SZ, _P],
 }
 _RESTYPES = {
     "chordal_strerror": ctypes.c_char_p,

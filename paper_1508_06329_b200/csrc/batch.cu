@@ -123,6 +123,11 @@ __device__ void arrangement_lexbfs_warp(const uint32_t *__restrict__ A32, int n,
             pos[x] = (uint16_t)i;
         }
         if (lane < W) rowbuf[lane] = __ldg(A32 + x * sw + lane);  // pivot row: one L2 round trip
+        // speculative L1 prefetch of the row of the vertex now at position i+1
+        // (it is the next pivot whenever the refinement leaves that slot alone,
+        // e.g. once the leading classes are singletons)
+        if (lane < W && i + 1 < tail)
+            asm volatile("prefetch.global.L1 [%0];" ::"l"(A32 + (int)A[i + 1] * sw + lane));
         __syncwarp();
         const uint32_t *rowx = rowbuf;
         const int R = tail - (i + 1);

@@ -32,6 +32,8 @@ int launch_gen_dense_random(uint8_t *, int64_t, int64_t, int64_t, double, int64_
                             cudaStream_t);
 int launch_edges_to_dense(const int32_t *, const int32_t *, int64_t, uint8_t *, int64_t, int64_t, cudaStream_t);
 long long gen_chordal_scratch_words(int64_t, int64_t, int *);
+int launch_gen_chordal_edges(int64_t, int64_t, int64_t, uint32_t, int32_t *, int32_t *, int32_t *, long long *,
+                             cudaStream_t);
 int launch_gen_chordal_random(uint8_t *, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, uint32_t, int32_t *,
                               cudaStream_t);
 }  // namespace chordal
@@ -439,6 +441,15 @@ int chordal_edges_to_dense(const int32_t *u_dev, const int32_t *v_dev, int64_t m
     int rc = check_dense(adj_dev, n, stride);
     if (rc) return rc;
     return launch_edges_to_dense(u_dev, v_dev, m, adj_dev, n, stride, as_stream(stream));
+}
+
+int chordal_gen_chordal_random_edges(int64_t n, int64_t k, int64_t seed, int32_t *u_dev, int32_t *v_dev,
+                                     int64_t *m_dev, void *scratch_dev, size_t scratch_bytes, void *stream) {
+    if (n < 1 || k < 0 || k >= n || !u_dev || !v_dev || !m_dev) return CHORDAL_EINVAL;
+    if (k + 2 > 10000 || n > 0x7FFFFFFF / (k + 2)) return CHORDAL_EINVAL;
+    if (!scratch_dev || scratch_bytes < chordal_gen_chordal_random_scratch_bytes(1, n, k)) return CHORDAL_EINVAL;
+    return launch_gen_chordal_edges(n, k, seed, crc32_str("chordal-random"), reinterpret_cast<int32_t *>(scratch_dev),
+                                    u_dev, v_dev, reinterpret_cast<long long *>(m_dev), as_stream(stream));
 }
 
 size_t chordal_gen_chordal_random_scratch_bytes(int64_t batch, int64_t n, int64_t k) {

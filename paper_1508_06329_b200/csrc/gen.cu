@@ -201,6 +201,7 @@ __device__ __forceinline__ uint64_t chordal_key(long long seed, uint32_t crc) {
 }
 
 __device__ __forceinline__ void set_edge(uint8_t *g, long long stride, int a, int b) {
+    if (!g) return;  // edge-list mode: the attachment lists are the output
     reinterpret_cast<uint32_t *>(g + (long long)a * stride)[b >> 5] |= 1u << (b & 31);
     reinterpret_cast<uint32_t *>(g + (long long)b * stride)[a >> 5] |= 1u << (a & 31);
 }
@@ -212,7 +213,7 @@ __global__ void gen_chordal_kernel(uint8_t *__restrict__ adj, long long batch, i
                                    long long scratch_words, int hmask) {
     const long long b = blockIdx.x * (long long)blockDim.x + threadIdx.x;
     if (b >= batch) return;
-    uint8_t *g = adj + b * (long long)n * stride;
+    uint8_t *g = adj ? adj + b * (long long)n * stride : nullptr;
     int32_t *att_off = scratch + b * scratch_words;
     int32_t *att_len = att_off + n;
     int32_t *hs = att_len + n;
@@ -333,6 +334,42 @@ int launch_edges_to_dense(const int32_t *u, const int32_t *v, int64_t m, uint8_t
     long long blocks = (m + 255) / 256;
     if (blocks > 148LL * 32) blocks = 148LL * 32;
     edges_to_dense_kernel<<<(int)blocks, 256, 0, stream>>>(u, v, m, adj, stride);
+    CH_LAUNCH_CHECK();
+    return CHORDAL_OK;
+}
+
+}  // namespace chordal
+
+namespace chordal {
+
+// Edge list of gen_chordal_random from the generator's attachment lists:
+// vertex i attached to lst[att_off[i] .. att_off[i] + att_len[i]) -> (i, v).
+__global__ void edges_from_lists_kernel(const int32_t *__restrict__ att_off, const int32_t *__restrict__ att_len,
+                                        const int32_t *__restrict__ lst, int n, int32_t *__restrict__ u,
+                                        int32_t *__restrict__ v, long long *__restrict__ m_out) {
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const int o = i == 0 ? 0 : att_off[i], c = i == 0 ? 0 : att_len[i];
+        for (int j = 0; j < c; ++j) {
+            u[o + j] = i;
+            v[o + j] = lst[o + j];
+        }
+        if (i == n - 1) *m_out = (long long)o + c;
+    }
+}
+
+int launch_gen_chordal_edges(int64_t n, int64_t k, int64_t seed, uint32_t crc, int32_t *scratch, int32_t *u,
+                             int32_t *v, long long *m_out, cudaStream_t stream) {
+    int hmask = 0;
+    const long long words = gen_chordal_scratch_words(n, k, &hmask);
+    if (k == 0 || n == 1) {
+        return cudaMemsetAsync(m_out, 0, sizeof(long long), stream) == cudaSuccess ? CHORDAL_OK : CHORDAL_ECUDA;
+    }
+    gen_chordal_kernel<<<1, 32, 0, stream>>>(nullptr, 1, (int)n, 0, (int)k, seed, 1, crc, scratch, words, hmask);
+    CH_LAUNCH_CHECK();
+    const int32_t *att_off = scratch, *att_len = scratch + n, *lst = scratch + 2 * n + (hmask + 1);
+    long long blocks = (n + 255) / 256;
+    if (blocks > 148LL * 8) blocks = 148LL * 8;
+    edges_from_lists_kernel<<<(int)blocks, 256, 0, stream>>>(att_off, att_len, lst, (int)n, u, v, m_out);
     CH_LAUNCH_CHECK();
     return CHORDAL_OK;
 }

@@ -78,6 +78,7 @@ struct CsrSource {  // CSR rows read in place from global memory
     __device__ __forceinline__ int capacity() const { return 0x7FFFFFFF; }
     __device__ __forceinline__ void stage(int64_t, int64_t) const {}
     __device__ __forceinline__ int get(int64_t e) const { return __ldg(indices + e); }
+    __device__ __forceinline__ void prefetch(int) const {}
 };
 
 // CSR rows staged through a shared-memory buffer: each block of the pivot's
@@ -112,6 +113,7 @@ struct CsrStagedSource {
         __syncwarp();
     }
     __device__ __forceinline__ int get(int64_t e) const { return (int)buf[e - base]; }
+    __device__ __forceinline__ void prefetch(int) const {}
 };
 
 // Packed bitset row of n <= 1024 bits (generic pointer: smem or global); the
@@ -144,6 +146,11 @@ struct BitsetSource {
     __device__ __forceinline__ int capacity() const { return 0x7FFFFFFF; }
     __device__ __forceinline__ void stage(int64_t, int64_t) const {}
     __device__ __forceinline__ int get(int64_t e) const { return (int)nbuf[e]; }
+    // speculative L1 prefetch of a likely next pivot's row
+    __device__ __forceinline__ void prefetch(int v) const {
+        const int lane = threadIdx.x & 31;
+        if (lane < words) asm volatile("prefetch.global.L1 [%0];" ::"l"(rows + v * sw + lane));
+    }
 };
 
 namespace slot_detail {
@@ -317,6 +324,7 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
             xs = slot_detail::first_live<I, S>(M, c0, h, e0);
         }
         const int x = (int)M.slot_v[xs];
+        if (xs + 1 < e0) src.prefetch((int)M.slot_v[xs + 1]);  // the head class's next member
         __syncwarp();
         if (lane == 0) {
             if (MODE != CHORDAL_TIE_SEEDED_ARB || xs == (long long)M.c_head[c0]) M.c_head[c0] = (S)(xs + 1);

@@ -105,6 +105,36 @@ def gen_chordal_random_device(n: int, k: int, seeds, *, stride: int | None = Non
     return ops.gen_chordal_random(out, n, s, k, seeds.start, step)
 
 
+def gen_chordal_random_csr_device(n: int, k: int, seed: int):
+    """gen_chordal_random(n, k, seed) as device CSR (indptr int64[n+1], indices int32[2m]).
+
+    The draws run on the GPU (one thread, csrc/gen.cu, bit-exact); the edge
+    list is symmetrised and sorted with torch (input preparation, not the hot
+    path).  This is how the N = 10^6 configuration is built without the 125 GB
+    dense matrix the reference generator would allocate.
+    """
+    from . import _native
+    from ._native import check, lib, ptr, stream_ptr
+
+    torch = _native.require_cuda()
+    cap = n * (k + 1) + 1
+    u = torch.empty(cap, dtype=torch.int32, device="cuda")
+    v = torch.empty(cap, dtype=torch.int32, device="cuda")
+    m_t = torch.zeros(1, dtype=torch.int64, device="cuda")
+    nbytes = int(lib.chordal_gen_chordal_random_scratch_bytes(1, n, k))
+    scratch = torch.empty(max(nbytes, 16), dtype=torch.uint8, device="cuda")
+    check(lib.chordal_gen_chordal_random_edges(n, k, seed, ptr(u), ptr(v), ptr(m_t), ptr(scratch), nbytes,
+                                               stream_ptr()), "chordal_gen_chordal_random_edges")
+    m = int(m_t.item())
+    a = torch.cat([u[:m], v[:m]]).to(torch.int64)
+    b = torch.cat([v[:m], u[:m]]).to(torch.int64)
+    key = torch.unique(a * n + b)
+    rows = key // n
+    indptr = torch.zeros(n + 1, dtype=torch.int64, device="cuda")
+    indptr[1:] = torch.cumsum(torch.bincount(rows, minlength=n), 0)
+    return indptr, (key % n).to(torch.int32)
+
+
 def chordal_random_edges(n: int, k: int, seed: int) -> tuple[np.ndarray, np.ndarray]:
     """0-based edge endpoints of gen_chordal_random (generate.py:118-155).
 

@@ -429,10 +429,16 @@ def test_config5_csr_million():
     from paper_1508_06329_b200.csr import CSRGraph
     from paper_1508_06329_b200.generate import chordal_random_edges
 
+    from paper_1508_06329_b200.generate import gen_chordal_random_csr_device
+
     exp = CONFIGS["5"]
-    u, v = chordal_random_edges(exp["n"], exp["k"], exp["seed"])
-    g = CSRGraph.from_edges0(exp["n"], u, v)
+    ip, ix = gen_chordal_random_csr_device(exp["n"], exp["k"], exp["seed"])  # drawn on the GPU
+    g = CSRGraph(exp["n"], ip.cpu().numpy(), ix.cpu().numpy())
     assert sha(g.indptr) == exp["indptr_sha256"] and sha(g.indices) == exp["indices_sha256"]
+    u = np.repeat(np.arange(g.n), np.diff(g.indptr))
+    v = g.indices.astype(np.int64)
+    keep0 = u < v
+    u, v = u[keep0], v[keep0]
     vd = P.is_chordal(g)
     assert vd.chordal and sha(vd.peo.order0.astype(np.int32)) == exp["order_sha256"]
     a, b = exp["nonchordal"]["removed_edge0"]
@@ -441,3 +447,15 @@ def test_config5_csr_million():
     vn = P.is_chordal(h)
     assert not vn.chordal and w0(vn.witness) == exp["nonchordal"]["witness"]
     assert sha(P.lexbfs_partition(h).order0.astype(np.int32)) == exp["nonchordal"]["order_sha256"]
+
+
+def test_device_csr_generator_matches_host():
+    from paper_1508_06329_b200.csr import CSRGraph
+    from paper_1508_06329_b200.generate import chordal_random_edges, gen_chordal_random_csr_device
+
+    for n, k, seed in ((2000, 8, 3), (500, 30, 1), (64, 0, 2), (1, 0, 0)):
+        ip, ix = gen_chordal_random_csr_device(n, k, seed)
+        u, v = chordal_random_edges(n, k, seed)
+        ref = CSRGraph.from_edges0(n, u, v)
+        assert ip.cpu().numpy().tolist() == ref.indptr.tolist()
+        assert ix.cpu().numpy().tolist() == ref.indices.tolist()
