@@ -73,13 +73,14 @@ size_t chordal_dense_workspace_bytes(int64_t n, int64_t m);
  * lexbfs_labels (search.py:262-268) and parallel_lexbfs (parallel/lexbfs.py:
  * 234-243).  Writes order_dev[n] (vertex at each position), pos_dev[n]
  * (position of each vertex) and, if parent_dev is not NULL, the PEO parent of
- * every vertex (-1 for none, -2 for "not computed": all -2 when the dense
- * engine ran, see below); the PEO checks accept -2 entries and search those
- * parents themselves.
- * m is the edge count (Graph.m); pass m < 0 to let the call count the edges,
- * which synchronises `stream` once.  Engines: graphs with m > n^2/16 run the
- * persistent single-CTA arrangement kernel (n <= 32768); sparser graphs are
- * converted to CSR on the device and run the O(deg)-per-step slot kernel. */
+ * every vertex (-1 for none, -2 for "not computed": vertices placed by the
+ * early exit once every class is a singleton); the PEO checks accept -2
+ * entries and search those parents themselves.
+ * Engines: n <= 32768 runs the persistent single-CTA touched-segment kernel
+ * (state in shared memory, any density; m is ignored and may be < 0); larger
+ * graphs are converted to CSR on the device and run the O(deg)-per-step slot
+ * kernel, which needs the edge count m (Graph.m): pass m < 0 to let the call
+ * count the edges, which synchronises `stream` once. */
 int chordal_lexbfs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int64_t m, int32_t tie_rule,
                          uint64_t seed, int32_t *order_dev, int32_t *pos_dev, int32_t *parent_dev, void *ws,
                          size_t ws_bytes, void *stream);

@@ -8,7 +8,7 @@
 // is_chordal (peo.py:177-202) called once per graph by the reference's bench
 // loop (bench.py:86-95).
 //
-//   dense graphs (m > n^2/16): the arrangement engine of lexbfs_dense.cu
+//   dense graphs (m > n^2/16): a one-warp arrangement engine
 //     (reached-region arrangement + unreached bitset, stable segmented
 //     partition per step) -- random dense graphs split into singleton classes
 //     after O(log n) steps and the search exits early;
@@ -73,7 +73,8 @@ struct BatchLayout {  // shared memory per graph (one warp); the adjacency stays
     }
 };
 
-// Arrangement LexBFS (LOWEST_INDEX) for one graph in one warp; see lexbfs_dense.cu.
+// Arrangement LexBFS (LOWEST_INDEX) for one graph in one warp (the _arraylex.py:17-19
+// invariant; lexbfs_seg.cu is the single-graph form).
 __device__ void arrangement_lexbfs_warp(const uint32_t *__restrict__ A32, int n, int sw, uint8_t *smem,
                                         const BatchLayout &L, uint16_t *ord, uint16_t *pos) {
     const int lane = threadIdx.x & 31;

@@ -7,8 +7,8 @@
 #include "common.cuh"
 
 namespace chordal {
-int launch_lexbfs_dense(const uint8_t *, int64_t, int64_t, int32_t, uint64_t, uint64_t, int32_t *,
-                        int32_t *, cudaStream_t);
+int launch_lexbfs_seg(const uint8_t *, int64_t, int64_t, int32_t, uint64_t, uint64_t, int32_t *, int32_t *,
+                      int32_t *, cudaStream_t);
 int launch_positions(const int32_t *, int64_t, int32_t *, cudaStream_t);
 int launch_fill_i32(int32_t *, int64_t, int32_t, cudaStream_t);
 int launch_key_init(uint64_t *, cudaStream_t);
@@ -81,16 +81,11 @@ const char *chordal_strerror(int status) {
     }
 }
 
-// Engine choice for a dense-stored graph (measured on B200, tools/engine_compare.py):
-// the one-warp slot engine costs ~2 us per step plus ~0.5 us per 32 unvisited
-// neighbours, the single-CTA arrangement engine ~10 us per step at n = 32768
-// but exits early once classes are singletons.  Slot wins up to average degree
-// ~100 (n=32768 k=64: 81 vs 353 ms; n=8192 k=8: 15 vs 56 ms), arrangement for
-// very high degree (n=32768 k=1024, avg 1005: 355 vs 447 ms) and dense graphs.
-static bool use_arrangement(int64_t n, int64_t m) {
-    if (n > CHORDAL_DENSE_LEXBFS_MAX_N) return false;
-    return n <= 64 || m > 256 * n;
-}
+// Engine choice for a dense-stored graph: n <= 32768 runs the single-CTA
+// touched-segment arrangement kernel (lexbfs_seg.cu, state in shared memory,
+// O(deg/32 + movers + split classes) per step, any density); larger graphs are
+// converted to CSR on the device and run the slot engine.
+static bool use_seg(int64_t n) { return n <= CHORDAL_DENSE_LEXBFS_MAX_N; }
 
 struct DenseWs {  // workspace carve-up (bytes) of the dense entry points
     size_t key, parent, indptr, indices, slot, total;
@@ -100,7 +95,7 @@ struct DenseWs {  // workspace carve-up (bytes) of the dense entry points
         key = o; o = a(o + 16);
         parent = o; o = a(o + sizeof(int32_t) * (size_t)n);
         indptr = indices = slot = o;
-        if (!use_arrangement(n, m)) {
+        if (!use_seg(n)) {
             indptr = o; o = a(o + sizeof(int64_t) * (size_t)(n + 1));
             indices = o; o = a(o + sizeof(int32_t) * (size_t)(2 * m + 1));
             slot = o; o = a(o + csr_workspace_bytes(n, m));
@@ -137,19 +132,14 @@ int chordal_lexbfs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int6
     if (!order_dev || !pos_dev) return CHORDAL_EINVAL;
     if (tie_rule < 0 || tie_rule > 2) return CHORDAL_EINVAL;
     cudaStream_t s = as_stream(stream);
+    const uint64_t cell = current_cell(crc32_str("current"));
+    if (use_seg(n))
+        return launch_lexbfs_seg(adj_dev, n, stride, tie_rule, seed, cell, order_dev, pos_dev, parent_dev, s);
     if (m < 0) {
         rc = count_edges_sync(adj_dev, n, stride, s, &m);
         if (rc) return rc;
     }
     const DenseWs L(n, m);
-    const uint64_t cell = current_cell(crc32_str("current"));
-    if (use_arrangement(n, m)) {
-        if (parent_dev) {  // the arrangement engine leaves parents to the PEO check (-2 = unknown)
-            rc = launch_fill_i32(parent_dev, n, -2, s);
-            if (rc) return rc;
-        }
-        return launch_lexbfs_dense(adj_dev, n, stride, tie_rule, seed, cell, order_dev, pos_dev, s);
-    }
     if (!ws || ws_bytes < L.total) return CHORDAL_EINVAL;
     uint8_t *w = reinterpret_cast<uint8_t *>(ws);
     int64_t *indptr = reinterpret_cast<int64_t *>(w + L.indptr);
@@ -216,7 +206,7 @@ int chordal_is_chordal_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, 
                              uint64_t seed, int32_t *order_dev, int32_t *pos_dev, void *ws, size_t ws_bytes,
                              int32_t *witness_dev, void *stream) {
     cudaStream_t s = as_stream(stream);
-    if (n > 0 && m < 0) {
+    if (n > 0 && m < 0 && !use_seg(n)) {
         int rc0 = check_dense(adj_dev, n, stride);
         if (rc0) return rc0;
         rc0 = count_edges_sync(adj_dev, n, stride, s, &m);
@@ -230,9 +220,8 @@ int chordal_is_chordal_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, 
     int rc = chordal_lexbfs_dense(adj_dev, n, stride, m, tie_rule, seed, order_dev, pos_dev, parent, ws, ws_bytes,
                                   stream);
     if (rc) return rc;
-    const bool have_parent = n > 0 && !use_arrangement(n, m);
-    return chordal_peo_dense(adj_dev, n, stride, order_dev, pos_dev, have_parent ? parent : nullptr, key,
-                             witness_dev, stream);
+    return chordal_peo_dense(adj_dev, n, stride, order_dev, pos_dev, n > 0 ? parent : nullptr, key, witness_dev,
+                             stream);
 }
 
 int chordal_is_chordal_dense_host(const uint8_t *adj_host, int64_t n, int64_t row_bytes,
@@ -263,8 +252,10 @@ int chordal_is_chordal_dense_host(const uint8_t *adj_host, int64_t n, int64_t ro
         if (stride != row_bytes && cudaMemsetAsync(adj, 0, adj_bytes, s) != cudaSuccess) { rc = CHORDAL_ECUDA; break; }
         if (cudaMemcpy2DAsync(adj, stride, adj_host, row_bytes, (n + 7) / 8, n, cudaMemcpyHostToDevice, s) !=
             cudaSuccess) { rc = CHORDAL_ECUDA; break; }
-        rc = count_edges_sync(adj, n, stride, s, &m);
-        if (rc) break;
+        if (!use_seg(n)) {
+            rc = count_edges_sync(adj, n, stride, s, &m);
+            if (rc) break;
+        }
         const size_t wsb = DenseWs(n, m).total;
         if (cudaMallocAsync((void **)&ws, wsb + 16, s) != cudaSuccess) { rc = CHORDAL_ENOMEM; break; }
         int32_t *wit = reinterpret_cast<int32_t *>(ws + wsb);

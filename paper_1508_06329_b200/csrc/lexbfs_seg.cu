@@ -1,0 +1,696 @@
+// lexbfs_seg.cu -- single-CTA persistent LexBFS over a packed adjacency bitset
+// whose per-step cost is O(deg(x)/32 + movers + |split classes|), not O(n).
+//
+// Replaces, for dense-stored graphs with n <= 32768:
+//   lexbfs_partition / PartitionList   search.py:328-532
+//   lexbfs_labels / _LabelChain        search.py:152-310
+//   lexbfs_array                        _arraylex.py:22-65
+//   parallel_lexbfs + kernels 1-4      parallel/lexbfs.py:37-262 (the paper's
+//                                      one-launch-per-step loop)
+//
+// State, all in shared memory (u16 vertex ids and positions, 215 KB at n=32768):
+//   A[]    the arrangement: A[0..i) is the order so far, A[i..tail) the
+//          reached unvisited vertices in priority order -- label classes in
+//          descending label order, each a contiguous run sorted by the tie
+//          rule (the _arraylex.py:17-19 invariant: the first unconsumed
+//          position is the next pivot).
+//   P[]    position of every reached vertex in A.
+//   U, RA  vertex bitsets: unreached (the empty-label class, never stored in
+//          A) and reached-unvisited.
+//   bnd    class-start bits over positions.
+//
+// Step i, pivot x = A[i], one thread per 32-bit word of x's row:
+//   1. movers: row & RA -> flag bit P[y] in F (positions); row & U = the newly
+//      reached vertices (appended after the tail as one class, tie order);
+//      parent[y] = x for both (the PEO parent: last visited neighbour).
+//   2. (only if some reached vertex moved) word-level scans over positions:
+//      prefix count of F, last class start before each word, first class
+//      start after it.  Any class [s, e) then knows its mover count
+//      T = cnt(e) - cnt(s) in O(1).
+//   3. words of classes with 0 < T < |class| (a real split; T == |class| is
+//      the "whole class moves" case of search.py:448-453 and needs nothing)
+//      are listed and stably partitioned: movers first (they form the new,
+//      higher class placed before the remainder, search.py:440-463).
+// Early exit: once every vertex is reached and every class is a singleton the
+// rest of the order is the arrangement itself (G(n, 0.5) exits after a few
+// dozen steps).
+//
+// The next pivot's row is loaded speculatively (guess: A[i+1] as it stands at
+// the start of step i -- right whenever the head class is not split), so the
+// row fetch of step i+1 overlaps step i.
+#include "common.cuh"
+
+namespace chordal {
+
+#ifdef SEG_PROFILE
+// Per-phase cycle counters of thread 0 (tools/seg_profile.cu only):
+// [0] steps [1] full-path steps [2] phase 1 [3] short tail [4] scans [5] 3a
+// [6] 3b [7] 3c + end [8] steps with a row-guess hit
+__device__ unsigned long long seg_prof[16];
+#define SEG_T(k)                                          \
+    do {                                                  \
+        const long long _c = clock64();                   \
+        seg_acc[k] += (unsigned long long)(_c - seg_t0);  \
+        seg_t0 = _c;                                      \
+    } while (0)
+#else
+#define SEG_T(k) \
+    do {         \
+    } while (0)
+#endif
+
+namespace {
+
+constexpr int kSegBig = 0x7FFFFFFF;
+
+struct SegLayout {
+    size_t A, An, P, U, RA, F, NB, bnd, Pc, LB, NBq, TW, wt, misc, total;
+    __host__ __device__ static size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
+    __host__ __device__ SegLayout(int W) {
+        const size_t np = size_t(W) * 32;
+        size_t o = 0;
+        A = o; o = align16(o + np * 2);
+        An = o; o = align16(o + np * 2);
+        P = o; o = align16(o + np * 2);
+        const size_t WP = size_t(W + 3) & ~size_t(3);  // words rounded up to 128-bit groups
+        U = o; o = align16(o + WP * 4);
+        RA = o; o = align16(o + WP * 4);
+        F = o; o = align16(o + WP * 4);
+        NB = o; o = align16(o + WP * 4);
+        bnd = o; o = align16(o + (WP + 4) * 4);
+        Pc = o; o = align16(o + WP * 2);
+        LB = o; o = align16(o + WP * 2);
+        NBq = o; o = align16(o + WP * 2);
+        TW = o; o = align16(o + WP * 2);
+        wt = o; o = align16(o + 4 * 32 * 4);
+        misc = o; o = align16(o + 24 * 4);
+        total = o;
+    }
+};
+
+__device__ __forceinline__ uint4 ld_nc_v4(const uint32_t *p) {
+    return __ldg(reinterpret_cast<const uint4 *>(p));
+}
+
+__device__ __forceinline__ bool seg_better(uint64_t s1, int32_t i1, uint64_t s2, int32_t i2) {
+    return s1 > s2 || (s1 == s2 && i1 > i2);
+}
+
+template <int MODE>
+__device__ __forceinline__ uint64_t seg_tie_score(int32_t v, uint64_t prefix) {
+    if (MODE == CHORDAL_TIE_ASCENDING) return (uint64_t)(0x7FFFFFFF - v);
+    if (MODE == CHORDAL_TIE_DESCENDING) return (uint64_t)v;
+    return splitmix64(prefix ^ (uint64_t)(v + 1));  // Arbitration.choose, parallel/engine.py:47-53
+}
+
+// Block-wide (score, id) max, broadcast to every thread.  Two barriers.
+__device__ __forceinline__ void seg_block_max(uint64_t &s, int32_t &id, uint64_t *rs, int32_t *ri) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        uint64_t s2 = __shfl_xor_sync(CH_FULL, s, d);
+        int32_t i2 = __shfl_xor_sync(CH_FULL, id, d);
+        if (seg_better(s2, i2, s, id)) { s = s2; id = i2; }
+    }
+    if (lane == 0) { rs[warp] = s; ri[warp] = id; }
+    __syncthreads();
+    s = lane < nw ? rs[lane] : 0;
+    id = lane < nw ? ri[lane] : -1;
+#pragma unroll
+    for (int d = 16; d >= 1; d >>= 1) {
+        uint64_t s2 = __shfl_xor_sync(CH_FULL, s, d);
+        int32_t i2 = __shfl_xor_sync(CH_FULL, id, d);
+        if (seg_better(s2, i2, s, id)) { s = s2; id = i2; }
+    }
+    __syncthreads();
+}
+
+// Block-wide exclusive scans, thread t = word t: sums of a and e, max of h
+// (identity 0), suffix min of l (identity kSegBig).  Totals of a and e are
+// returned to every thread.  One barrier; wt (4 x 32 ints) is free again
+// after the caller's next barrier.
+__device__ __forceinline__ void seg_scan4(int a, int e, int h, int l, int *wt, int &xa, int &xe, int &xh, int &xl,
+                                          int &ta, int &te) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    int ia = a, ie = e, ih = h, il = l;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int oa = __shfl_up_sync(CH_FULL, ia, d), oe = __shfl_up_sync(CH_FULL, ie, d);
+        const int oh = __shfl_up_sync(CH_FULL, ih, d), ol = __shfl_down_sync(CH_FULL, il, d);
+        if (lane >= d) { ia += oa; ie += oe; ih = max(ih, oh); }
+        if (lane + d < 32) il = min(il, ol);
+    }
+    if (lane == 31) { wt[warp] = ia; wt[32 + warp] = ie; wt[64 + warp] = ih; }
+    if (lane == 0) wt[96 + warp] = il;
+    xa = ia - a;
+    xe = ie - e;
+    xh = __shfl_up_sync(CH_FULL, ih, 1);
+    xl = __shfl_down_sync(CH_FULL, il, 1);
+    if (lane == 0) xh = 0;
+    if (lane == 31) xl = kSegBig;
+    __syncthreads();
+    int pa = lane < NW ? wt[lane] : 0, pe = lane < NW ? wt[32 + lane] : 0;
+    int ph = lane < NW ? wt[64 + lane] : 0, pl = lane < NW ? wt[96 + lane] : kSegBig;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int oa = __shfl_up_sync(CH_FULL, pa, d), oe = __shfl_up_sync(CH_FULL, pe, d);
+        const int oh = __shfl_up_sync(CH_FULL, ph, d), ol = __shfl_down_sync(CH_FULL, pl, d);
+        if (lane >= d) { pa += oa; pe += oe; ph = max(ph, oh); }
+        if (lane + d < 32) pl = min(pl, ol);
+    }
+    ta = __shfl_sync(CH_FULL, pa, NW - 1);
+    te = __shfl_sync(CH_FULL, pe, NW - 1);
+    const int wa = __shfl_sync(CH_FULL, pa, (warp + 31) & 31), we = __shfl_sync(CH_FULL, pe, (warp + 31) & 31);
+    const int wh = __shfl_sync(CH_FULL, ph, (warp + 31) & 31), wl = __shfl_sync(CH_FULL, pl, (warp + 1) & 31);
+    if (warp > 0) { xa += wa; xe += we; xh = max(xh, wh); }
+    if (warp + 1 < NW) xl = min(xl, wl);
+}
+
+// Exclusive sum scan of e only (the append-only steps).  One barrier.
+__device__ __forceinline__ int seg_scan1(int e, int *wt, int &te) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
+    int ie = e;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int oe = __shfl_up_sync(CH_FULL, ie, d);
+        if (lane >= d) ie += oe;
+    }
+    if (lane == 31) wt[32 + warp] = ie;
+    int xe = ie - e;
+    __syncthreads();
+    int pe = lane < NW ? wt[32 + lane] : 0;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        const int oe = __shfl_up_sync(CH_FULL, pe, d);
+        if (lane >= d) pe += oe;
+    }
+    te = __shfl_sync(CH_FULL, pe, NW - 1);
+    const int we = __shfl_sync(CH_FULL, pe, (warp + 31) & 31);
+    if (warp > 0) xe += we;
+    return xe;
+}
+
+}  // namespace
+
+template <int MODE>
+__global__ void __launch_bounds__(256, 1)
+lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint64_t seed, uint64_t cell,
+                  int32_t *__restrict__ order, int32_t *__restrict__ pos_out, int32_t *__restrict__ parent) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const int W = (n + 31) >> 5;
+    const int WP = (W + 3) & ~3;
+    const SegLayout L(W);
+    uint16_t *A = (uint16_t *)(smem + L.A);
+    uint16_t *An = (uint16_t *)(smem + L.An);
+    uint16_t *P = (uint16_t *)(smem + L.P);
+    uint32_t *U = (uint32_t *)(smem + L.U);
+    uint32_t *RA = (uint32_t *)(smem + L.RA);
+    uint32_t *F = (uint32_t *)(smem + L.F);
+    uint32_t *NB = (uint32_t *)(smem + L.NB);
+    uint32_t *bnd = (uint32_t *)(smem + L.bnd);
+    uint16_t *Pc = (uint16_t *)(smem + L.Pc);
+    uint16_t *LB = (uint16_t *)(smem + L.LB);
+    uint16_t *NBq = (uint16_t *)(smem + L.NBq);
+    uint16_t *TW = (uint16_t *)(smem + L.TW);
+    int *wt = (int *)(smem + L.wt);
+    // Per-step counters in 3 rotating sets of 8: [0] any vertex newly reached,
+    // [1] #movers, [2] min / [3] max mover position, [4] #split-class words,
+    // [5] #splits.  Step i uses set i % 3 and resets set (i + 1) % 3, whose
+    // last readers (step i - 2) are two barriers behind.
+    int *misc = (int *)(smem + L.misc);
+    uint64_t *red_s = (uint64_t *)(smem + L.wt);  // block_max scratch aliases wt (never live at once)
+    int32_t *red_i = (int32_t *)(smem + L.wt + 32 * 8);
+
+    const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+    const int NT = blockDim.x, NW = NT >> 5;
+    const int w0 = 4 * t;  // this thread owns vertex / position words [w0, w0 + 4)
+    const bool own = w0 < W;
+
+    for (int w = t; w < WP; w += NT) {
+        U[w] = w < W - 1 ? CH_FULL : (w == W - 1 ? ((n & 31) ? mask_below(n & 31) : CH_FULL) : 0u);
+        RA[w] = 0;
+        F[w] = 0;
+        NB[w] = 0;
+        bnd[w] = 0;
+    }
+    if (t < 4) bnd[WP + t] = 0;
+    if (t < 24) misc[t] = (t & 7) == 2 ? kSegBig : ((t & 7) == 3 ? -1 : 0);
+    if (parent)
+        for (int v = t; v < n; v += NT) parent[v] = -1;
+    __syncthreads();
+    // Every rule starts at vertex 0 (vertex 1 in the reference: the smallest id
+    // for LOWEST_INDEX, pinned for parallel_lexbfs, parallel/lexbfs.py:173).
+    if (t == 0) {
+        A[0] = 0;
+        P[0] = 0;
+        U[0] &= ~1u;
+        bnd[0] = 1u;
+    }
+    __syncthreads();
+
+    const uint32_t *rows = reinterpret_cast<const uint32_t *>(adj);
+    const long long sw = stride >> 2;  // row pitch in words (a multiple of 4)
+#ifdef SEG_PROFILE
+    unsigned long long seg_acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+#endif
+    int tail = 1, nclasses = 1;
+    int guess = -1;
+    uint4 nxt = make_uint4(0, 0, 0, 0);
+
+    for (int i = 0; i < n; ++i) {
+        // ---- pivot ---------------------------------------------------------
+        if (i == tail) {
+            // Reached region empty: the next pivot comes from the unreached
+            // (empty-label) class -- a new component.
+            const uint64_t prefix = MODE == CHORDAL_TIE_SEEDED_ARB ? mix64_3(seed, (uint64_t)(4 * (i - 1) + 3), cell) : 0;
+            uint64_t s = 0;
+            int32_t id = -1;
+            for (int w = t; w < W; w += NT) {
+                uint32_t u = U[w];
+                if (!u) continue;
+                if (MODE == CHORDAL_TIE_ASCENDING) {
+                    const int32_t v = 32 * w + __ffs(u) - 1;
+                    const uint64_t sc = seg_tie_score<MODE>(v, prefix);
+                    if (id < 0 || seg_better(sc, v, s, id)) { s = sc; id = v; }
+                } else if (MODE == CHORDAL_TIE_DESCENDING) {
+                    const int32_t v = 32 * w + highest_bit(u);
+                    const uint64_t sc = seg_tie_score<MODE>(v, prefix);
+                    if (id < 0 || seg_better(sc, v, s, id)) { s = sc; id = v; }
+                } else {
+                    while (u) {
+                        const int b = __ffs(u) - 1;
+                        u &= u - 1;
+                        const int32_t v = 32 * w + b;
+                        const uint64_t sc = seg_tie_score<MODE>(v, prefix);
+                        if (id < 0 || seg_better(sc, v, s, id)) { s = sc; id = v; }
+                    }
+                }
+            }
+            if (id < 0) s = 0;
+            seg_block_max(s, id, red_s, red_i);
+            if (t == 0) {
+                A[i] = (uint16_t)id;
+                P[id] = (uint16_t)i;
+                U[id >> 5] &= ~(1u << (id & 31));
+                bnd[i >> 5] |= 1u << (i & 31);
+            }
+            tail = i + 1;
+            nclasses = 1;
+            __syncthreads();
+        } else if (MODE == CHORDAL_TIE_SEEDED_ARB && i > 0) {
+            // Elect within the max-label class [i, e): all its members offer
+            // themselves as `current` (parallel/lexbfs.py:216-225).
+            int e = tail;
+            for (int v0 = (i + 1) >> 5; v0 * 32 < tail; v0 += 32) {
+                const int w = v0 + lane;
+                uint32_t m = 0;
+                if (w * 32 < tail) {
+                    m = bnd[w];
+                    if (w == ((i + 1) >> 5)) m &= ~mask_below((i + 1) & 31);
+                }
+                const uint32_t any = __ballot_sync(CH_FULL, m != 0);
+                if (any) {
+                    const int src = __ffs(any) - 1;
+                    const uint32_t mm = __shfl_sync(CH_FULL, m, src);
+                    e = min(tail, (v0 + src) * 32 + __ffs(mm) - 1);
+                    break;
+                }
+            }
+            const uint64_t prefix = mix64_3(seed, (uint64_t)(4 * (i - 1) + 3), cell);
+            uint64_t s = 0;
+            int32_t id = -1, bp = -1;
+            for (int p = i + t; p < e; p += NT) {
+                const int32_t v = A[p];
+                const uint64_t sc = seg_tie_score<MODE>(v, prefix);
+                if (id < 0 || seg_better(sc, v, s, id)) { s = sc; id = v; bp = p; }
+            }
+            const int32_t my_id = id;
+            seg_block_max(s, id, red_s, red_i);
+            if (my_id == id && bp >= 0 && bp != i) {  // exactly one thread holds the winner
+                const uint16_t t0 = A[i];
+                A[i] = (uint16_t)id;
+                A[bp] = t0;
+                P[id] = (uint16_t)i;
+                P[t0] = (uint16_t)bp;
+            }
+            __syncthreads();
+        }
+
+#ifdef SEG_PROFILE
+        long long seg_t0 = clock64();
+        seg_acc[0]++;
+#endif
+        const int x = A[i];
+        const int tail0 = tail;
+        const int hpos = i + 1;  // first region position (the rest of x's class starts here)
+        // x's class was the singleton {x} iff the next position starts a class
+        const bool head_single = hpos >= tail0 || ((bnd[hpos >> 5] >> (hpos & 31)) & 1u);
+        if (head_single) --nclasses;
+        if (t == 0) {
+            order[i] = x;
+            pos_out[x] = i;
+        }
+        int *fl = misc + 8 * (i % 3);
+        // ---- phase 1: movers and newly reached vertices, 128-bit row loads --
+        uint32_t r[4] = {0u, 0u, 0u, 0u}, ext[4] = {0u, 0u, 0u, 0u};
+        int extc = 0, cnt = 0, pmn = kSegBig, pmx = -1;
+        if (own) {
+            const uint4 rw = (x == guess) ? nxt : ld_nc_v4(rows + (long long)x * sw + w0);
+            r[0] = rw.x; r[1] = rw.y; r[2] = rw.z; r[3] = rw.w;
+        }
+#ifdef SEG_PROFILE
+        const int guess_prev = guess;
+#endif
+        guess = hpos < tail0 ? (int)A[hpos] : -1;
+        if (guess >= 0 && own) nxt = ld_nc_v4(rows + (long long)guess * sw + w0);
+        if (hpos + 1 < tail0 && own && (t & 7) == 0)  // one step further ahead: warm L2
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(rows + (long long)A[hpos + 1] * sw + w0));
+        if (own) {
+            if ((x >> 7) == t) RA[x >> 5] &= ~(1u << (x & 31));
+            const uint4 ra4 = *reinterpret_cast<const uint4 *>(RA + w0);
+            const uint4 u4 = *reinterpret_cast<const uint4 *>(U + w0);
+            const uint32_t ra[4] = {ra4.x, ra4.y, ra4.z, ra4.w}, uu[4] = {u4.x, u4.y, u4.z, u4.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                uint32_t m2 = r[k] & ra[k];
+                ext[k] = r[k] & uu[k];
+                extc += __popc(ext[k]);
+                while (m2) {  // four movers per round: their position loads overlap
+                    int y[4], pp[4], c = 0;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        y[u] = 32 * (w0 + k) + __ffs(m2) - 1;
+                        if (m2) ++c;
+                        m2 &= m2 - 1;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) pp[u] = u < c ? (int)P[y[u]] : 0;
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        if (u < c) {
+                            atomicOr(&F[pp[u] >> 5], 1u << (pp[u] & 31));
+                            if (parent) parent[y[u]] = x;
+                            pmn = min(pmn, pp[u]);
+                            pmx = max(pmx, pp[u]);
+                        }
+                    }
+                    cnt += c;
+                }
+            }
+            if (extc) {
+                if (parent) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        uint32_t m3 = ext[k];
+                        while (m3) {
+                            const int b = __ffs(m3) - 1;
+                            m3 &= m3 - 1;
+                            parent[32 * (w0 + k) + b] = x;
+                        }
+                    }
+                }
+                *reinterpret_cast<uint4 *>(U + w0) = make_uint4(uu[0] & ~ext[0], uu[1] & ~ext[1], uu[2] & ~ext[2],
+                                                                uu[3] & ~ext[3]);
+                *reinterpret_cast<uint4 *>(RA + w0) = make_uint4(ra[0] | ext[0], ra[1] | ext[1], ra[2] | ext[2],
+                                                                 ra[3] | ext[3]);
+                fl[0] = 1;
+            }
+        }
+        {  // mover count and position range: one shared atomic per warp
+            const int wc = __reduce_add_sync(CH_FULL, cnt);
+            if (wc) {
+                const int wmn = (int)__reduce_min_sync(CH_FULL, (unsigned)pmn);
+                const int wmx = __reduce_max_sync(CH_FULL, pmx);
+                if (lane == 0) {
+                    atomicAdd(fl + 1, wc);
+                    atomicMin(fl + 2, wmn);
+                    atomicMax(fl + 3, wmx);
+                }
+            }
+        }
+        if (t < 8) misc[8 * ((i + 1) % 3) + t] = t == 2 ? kSegBig : (t == 3 ? -1 : 0);
+        __syncthreads();  // B1
+        SEG_T(2);
+#ifdef SEG_PROFILE
+        if (x == guess_prev) seg_acc[8]++;
+#endif
+        const bool anyE = fl[0] != 0;
+        const int cntA = fl[1];
+        const int gmn = fl[2], gmx = fl[3];
+        // Movers that fill a run of whole classes change nothing (every class
+        // they touch moves in one hop, search.py:448-453).
+        const bool full = cntA > 0 &&
+                          !(cntA == gmx - gmn + 1 && (gmn == hpos || ((bnd[gmn >> 5] >> (gmn & 31)) & 1u)) &&
+                            (gmx + 1 >= tail0 || ((bnd[(gmx + 1) >> 5] >> ((gmx + 1) & 31)) & 1u)));
+        int ktot = 0, xe = 0;
+        uint32_t nbadd[4] = {0u, 0u, 0u, 0u};
+
+        if (!full) {
+            if (anyE) xe = seg_scan1(extc, wt, ktot);
+        } else {
+#ifdef SEG_PROFILE
+            seg_acc[1]++;
+#endif
+            // A split of the head class puts its first mover (the smallest
+            // mover position gmn, if the head class reaches that far) at hpos:
+            // that is the next pivot.  Re-aim the speculative row load.
+            if (t == 0) {
+                int g = -1;
+                if (gmn > hpos && (gmn >> 5) - (hpos >> 5) < 4) {
+                    bool inhead = true;
+                    for (int q = hpos >> 5; q <= (gmn >> 5); ++q) {
+                        uint32_t bw = bnd[q];
+                        if (q == (hpos >> 5)) bw &= ~mask_below((hpos & 31) + 1);
+                        if (q == (gmn >> 5)) bw &= mask_below((gmn & 31) + 1);
+                        if (bw) inhead = false;
+                    }
+                    if (inhead) g = A[gmn];
+                }
+                fl[6] = g;
+            }
+            // ---- phase 2: word-level scans over positions -------------------------
+            // Region class starts of position word q: bnd bits in [hpos, tail0)
+            // with hpos forced.
+            auto breg = [&](int q) -> uint32_t {
+                uint32_t b = bnd[q];
+                const int lo = hpos - 32 * q;
+                if (lo > 0) b = lo >= 32 ? 0u : (b & ~mask_below(lo));
+                if (lo >= 0 && lo < 32) b |= 1u << lo;
+                return b;
+            };
+            uint32_t f[4] = {0u, 0u, 0u, 0u}, b[4] = {0u, 0u, 0u, 0u};
+            int cpre[4], hb[4], lbw[4];
+            int ctot = 0, hmax = 0, lmin = kSegBig;
+            if (own) {
+                const uint4 f4 = *reinterpret_cast<const uint4 *>(F + w0);
+                f[0] = f4.x; f[1] = f4.y; f[2] = f4.z; f[3] = f4.w;
+            }
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (own) b[k] = breg(w0 + k);
+                cpre[k] = ctot;
+                ctot += __popc(f[k]);
+                hb[k] = b[k] ? 32 * (w0 + k) + highest_bit(b[k]) : 0;
+                lbw[k] = b[k] ? 32 * (w0 + k) + __ffs(b[k]) - 1 : kSegBig;
+                hmax = max(hmax, hb[k]);
+                lmin = min(lmin, lbw[k]);
+            }
+            int xa, xh, xl, ta;
+            seg_scan4(ctot, extc, hmax, lmin, wt, xa, xe, xh, xl, ta, ktot);
+            int nbq[4], lbq[4];
+            {
+                int run = xh;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) { lbq[k] = run; run = max(run, hb[k]); }
+                run = min(xl, tail0);
+#pragma unroll
+                for (int k = 3; k >= 0; --k) { nbq[k] = run; run = min(run, lbw[k]); }
+            }
+            if (own) {
+                *reinterpret_cast<uint2 *>(Pc + w0) =
+                    make_uint2((uint32_t)(xa + cpre[0]) | ((uint32_t)(xa + cpre[1]) << 16),
+                               (uint32_t)(xa + cpre[2]) | ((uint32_t)(xa + cpre[3]) << 16));
+                *reinterpret_cast<uint2 *>(LB + w0) = make_uint2((uint32_t)lbq[0] | ((uint32_t)lbq[1] << 16),
+                                                                 (uint32_t)lbq[2] | ((uint32_t)lbq[3] << 16));
+                *reinterpret_cast<uint2 *>(NBq + w0) = make_uint2((uint32_t)nbq[0] | ((uint32_t)nbq[1] << 16),
+                                                                  (uint32_t)nbq[2] | ((uint32_t)nbq[3] << 16));
+            }
+            __syncthreads();  // B2
+            SEG_T(4);
+            {
+                const int g = fl[6];
+                if (g >= 0 && g != guess) {
+                    guess = g;
+                    if (own) nxt = ld_nc_v4(rows + (long long)g * sw + w0);
+                }
+            }
+            // movers at positions < pp
+            auto cntb = [&](int pp) -> int {
+                const int q = pp >> 5;
+                if (q >= W) return ta;
+                return (int)Pc[q] + __popc(F[q] & mask_below(pp & 31));
+            };
+            auto is_split = [&](int s, int e) -> bool {
+                const int T = cntb(e) - cntb(s);
+                return T > 0 && T < e - s;
+            };
+            // ---- phase 3a: list the words of split classes ------------------------
+            if (own) {
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int q = w0 + k;
+                    const int lo = max(32 * q, hpos), hi = min(32 * q + 32, tail0);
+                    if (lo >= hi) continue;
+                    const int lob = lo - 32 * q, hib = hi - 32 * q;
+                    const uint32_t vm = mask_below(hib) & ~mask_below(lob);
+                    // two neighbouring positions of one class, one mover and one not
+                    bool touched = (((f[k] ^ (f[k] >> 1)) & ~(b[k] >> 1)) & vm & (vm >> 1)) != 0;
+                    // a class entering from the previous word
+                    if (!touched && !((b[k] >> lob) & 1u))
+                        touched = is_split(lbq[k], b[k] ? 32 * q + __ffs(b[k]) - 1 : nbq[k]);
+                    // a class leaving into the next word
+                    if (!touched && hib == 32 && nbq[k] > 32 * q + 32 && b[k])
+                        touched = is_split(32 * q + highest_bit(b[k]), nbq[k]);
+                    if (touched) TW[atomicAdd(fl + 4, 1)] = (uint16_t)q;
+                }
+            }
+            __syncthreads();  // B2.5
+            SEG_T(5);
+            const int ntouch = fl[4];
+            // ---- phase 3b: stable partition of split classes into An --------------
+            for (int j0 = 4 * warp; j0 < ntouch; j0 += 4 * NW) {  // four words per round: loads overlap
+                int q[4], v[4], dst[4];
+                bool ok[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    q[u] = j0 + u < ntouch ? (int)TW[j0 + u] : 0;
+                    const int p = 32 * q[u] + lane;
+                    ok[u] = j0 + u < ntouch && p >= hpos && p < tail0;
+                    v[u] = A[p];
+                    dst[u] = p;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int p = 32 * q[u] + lane;
+                    const uint32_t bq = breg(q[u]);
+                    const uint32_t bl = bq & mask_below(lane + 1);
+                    const int s = bl ? 32 * q[u] + highest_bit(bl) : (int)LB[q[u]];
+                    const uint32_t above = bq & ~mask_below(lane + 1);
+                    const int e = above ? 32 * q[u] + __ffs(above) - 1 : (int)NBq[q[u]];
+                    const int cs = cntb(s);
+                    const int T = cntb(e) - cs;
+                    if (ok[u] && T > 0 && T < e - s) {
+                        const uint32_t fq = F[q[u]];
+                        const int fb = (int)Pc[q[u]] + __popc(fq & mask_below(lane)) - cs;
+                        dst[u] = ((fq >> lane) & 1u) ? s + fb : s + T + (p - s - fb);
+                        if (p == s) {
+                            atomicOr(&NB[(s + T) >> 5], 1u << ((s + T) & 31));
+                            atomicAdd(fl + 5, 1);
+                        }
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (ok[u]) An[dst[u]] = (uint16_t)v[u];
+            }
+            __syncthreads();  // B3
+            SEG_T(6);
+            nclasses += fl[5];
+            // ---- phase 3c: copy back and positions --------------------------------
+            for (int j0 = 4 * warp; j0 < ntouch; j0 += 4 * NW) {
+                int p[4], v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    p[u] = j0 + u < ntouch ? 32 * (int)TW[j0 + u] + lane : -1;
+                    v[u] = p[u] >= hpos && p[u] < tail0 ? (int)An[p[u]] : -1;
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    if (v[u] >= 0) {
+                        A[p[u]] = (uint16_t)v[u];
+                        P[v[u]] = (uint16_t)p[u];
+                    }
+                }
+            }
+            if (own) {
+                const uint4 nb4 = *reinterpret_cast<const uint4 *>(NB + w0);
+                nbadd[0] = nb4.x; nbadd[1] = nb4.y; nbadd[2] = nb4.z; nbadd[3] = nb4.w;
+                if (nb4.x | nb4.y | nb4.z | nb4.w) *reinterpret_cast<uint4 *>(NB + w0) = make_uint4(0, 0, 0, 0);
+            }
+        }
+        // ---- end of step: clear flags, new class starts, append -----------------
+        if (own) {
+            if (cntA && (w0 + 3) >= (gmn >> 5) && w0 <= (gmx >> 5))
+                *reinterpret_cast<uint4 *>(F + w0) = make_uint4(0, 0, 0, 0);
+            if (hpos < tail0 && (hpos >> 7) == t) nbadd[(hpos >> 5) & 3] |= 1u << (hpos & 31);
+            if (ktot > 0 && (tail0 >> 7) == t) nbadd[(tail0 >> 5) & 3] |= 1u << (tail0 & 31);
+#pragma unroll
+            for (int k = 0; k < 4; ++k)
+                if (nbadd[k]) bnd[w0 + k] |= nbadd[k];
+            if (extc) {  // the newly reached vertices: one class after the tail, tie order
+                int idx = xe;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    uint32_t e2 = ext[k];
+                    while (e2) {
+                        const int b = __ffs(e2) - 1;
+                        e2 &= e2 - 1;
+                        const int dst = (MODE == CHORDAL_TIE_DESCENDING) ? tail0 + (ktot - 1 - idx) : tail0 + idx;
+                        ++idx;
+                        A[dst] = (uint16_t)(32 * (w0 + k) + b);
+                        P[32 * (w0 + k) + b] = (uint16_t)dst;
+                    }
+                }
+            }
+        }
+        if (ktot > 0) {
+            tail = tail0 + ktot;
+            ++nclasses;
+        }
+        __syncthreads();  // B4
+        SEG_T(full ? 7 : 3);
+        // ---- early exit: everything reached, every class a singleton ----------
+        if (tail == n && nclasses == tail - hpos) {
+            for (int p = hpos + t; p < n; p += NT) {
+                const int v = A[p];
+                order[p] = v;
+                pos_out[v] = p;
+                // the skipped steps would still have refreshed this vertex's
+                // parent: leave it to the PEO check (unknown = -2)
+                if (parent) parent[v] = -2;
+            }
+            break;
+        }
+    }
+#ifdef SEG_PROFILE
+    if (t == 0)
+        for (int k = 0; k < 9; ++k) seg_prof[k] = seg_acc[k];
+#endif
+}
+
+size_t seg_smem_bytes(int64_t n) { return SegLayout((int)((n + 31) >> 5)).total; }
+
+int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int32_t tie_rule, uint64_t seed, uint64_t cell,
+                      int32_t *order, int32_t *pos, int32_t *parent, cudaStream_t stream) {
+    if (n <= 0) return CHORDAL_OK;
+    if (n > CHORDAL_DENSE_LEXBFS_MAX_N) return CHORDAL_ETOOLARGE;
+    const int W = (int)((n + 31) >> 5);
+    const int T = max(32, ((W + 3) / 4 + 31) / 32 * 32);  // one thread per four row words
+    const size_t smem = seg_smem_bytes(n);
+    cudaError_t e;
+#define SEG_LAUNCH(M)                                                                                          \
+    e = cudaFuncSetAttribute(lexbfs_seg_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+    if (e != cudaSuccess) return CHORDAL_ECUDA;                                                                 \
+    lexbfs_seg_kernel<M><<<1, T, smem, stream>>>(adj, (int)n, stride, seed, cell, order, pos, parent);
+    switch (tie_rule) {
+        case CHORDAL_TIE_ASCENDING: SEG_LAUNCH(CHORDAL_TIE_ASCENDING); break;
+        case CHORDAL_TIE_DESCENDING: SEG_LAUNCH(CHORDAL_TIE_DESCENDING); break;
+        case CHORDAL_TIE_SEEDED_ARB: SEG_LAUNCH(CHORDAL_TIE_SEEDED_ARB); break;
+        default: return CHORDAL_EINVAL;
+    }
+#undef SEG_LAUNCH
+    CH_LAUNCH_CHECK();
+    return CHORDAL_OK;
+}
+
+}  // namespace chordal

@@ -35,7 +35,7 @@ def lexbfs(rows: DeviceRows, tie_rule: int = _native.TIE_ASCENDING, seed: int = 
     n, dev = rows.n, rows.data.device
     order, pos, parent = _i32(torch, n, dev), _i32(torch, n, dev), _i32(torch, n, dev)
     if n:
-        mm = m if m >= 0 else (rows.m if rows.m >= 0 else count_edges(rows, stream))
+        mm = _edge_count(rows, m, stream)
         ws = _ws(torch, lib.chordal_dense_workspace_bytes(n, mm), dev)
         check(
             lib.chordal_lexbfs_dense(rows.ptr, n, rows.stride, mm, tie_rule, seed & U64_MAX, ptr(order), ptr(pos),
@@ -45,6 +45,19 @@ def lexbfs(rows: DeviceRows, tie_rule: int = _native.TIE_ASCENDING, seed: int = 
     if want_parent:
         return order[:n], pos[:n], parent[:n]
     return order[:n], pos[:n]
+
+
+def _edge_count(rows: DeviceRows, m: int, stream=None) -> int:
+    """The edge count the dense entry points need: only graphs above the
+    shared-memory engine's limit (n > 32768, CSR route) need it; the others
+    pass 0 and skip the counting pass and its host synchronisation."""
+    if m >= 0:
+        return m
+    if rows.m >= 0:
+        return rows.m
+    if rows.n <= _native.DENSE_LEXBFS_MAX_N:
+        return 0
+    return count_edges(rows, stream)
 
 
 def count_edges(rows: DeviceRows, stream=None) -> int:
@@ -123,7 +136,7 @@ def is_chordal(rows: DeviceRows, tie_rule: int = _native.TIE_ASCENDING, seed: in
     n, dev = rows.n, rows.data.device
     order, pos = _i32(torch, n, dev), _i32(torch, n, dev)
     wit = torch.empty(4, dtype=torch.int32, device=dev)
-    mm = m if m >= 0 else (rows.m if rows.m >= 0 or n == 0 else count_edges(rows, stream))
+    mm = _edge_count(rows, m, stream)
     if ws is None:
         ws = _ws(torch, lib.chordal_dense_workspace_bytes(n, max(mm, 0)), dev)
     check(

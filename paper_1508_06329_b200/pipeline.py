@@ -1,8 +1,8 @@
 """Engine dispatch shared by the reference-shaped entry points.
 
 Dense inputs (``_packed`` rows) go through chordal_lexbfs_dense /
-chordal_is_chordal_dense (which pick the arrangement or slot engine by
-density); CSR inputs through the CSR kernels.  Everything returns host
+chordal_is_chordal_dense (the shared-memory touched-segment engine for
+n <= 32768, the CSR slot engine above); CSR inputs through the CSR kernels.  Everything returns host
 numpy arrays (0-based) at the end -- the only device->host copies of a call.
 """
 

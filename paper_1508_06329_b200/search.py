@@ -2,7 +2,8 @@
 
 ``lexbfs_labels`` (search.py:262-310) and ``lexbfs_partition``
 (search.py:500-532) keep their signatures and return types; both run the
-persistent single-CTA kernel of ``csrc/lexbfs_dense.cu``.  Under the default
+persistent single-CTA kernel of ``csrc/lexbfs_seg.cu`` (n <= 32768; larger
+graphs the CSR slot engine).  Under the default
 ``LOWEST_INDEX`` tie-break every reference method ("linked", "array",
 "auto") yields the same order (the reference's own equality tests,
 test_search.py:98-112), and so does this one.

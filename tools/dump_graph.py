@@ -1,0 +1,28 @@
+"""Write a chordal config graph as (int64 n, int64 stride, packed rows) for tools/seg_profile.
+
+    python tools/dump_graph.py N K out.bin
+"""
+import os
+import sys
+
+import numpy as np
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+from paper_1508_06329_b200.generate import chordal_random_edges  # noqa: E402
+from paper_1508_06329_b200.graph import device_stride  # noqa: E402
+
+
+def main(n, k, out):
+    u, v = chordal_random_edges(n, k, 0)
+    stride = device_stride(n)
+    rows = np.zeros((n, stride), np.uint8)
+    for a, b in ((u, v), (v, u)):
+        np.bitwise_or.at(rows, (a, b >> 3), (1 << (b & 7)).astype(np.uint8))
+    with open(out, "wb") as f:
+        np.array([n, stride], np.int64).tofile(f)
+        rows.tofile(f)
+
+
+if __name__ == "__main__":
+    main(int(sys.argv[1]), int(sys.argv[2]), sys.argv[3])

@@ -34,16 +34,20 @@ def main():
         rows = DeviceRows(n, device_stride(n), ops.edges_to_dense(u, v, n, device_stride(n)))
         cases.append((f"chordal n={n} k={k}", rows))
     cases.append(("dense n=8192 p=.5", DeviceRows(8192, 1024, gen_dense_random_device(8192, 0.5, 0)[0])))
+    cases.append(("dense n=32768 p=.5", DeviceRows(32768, 4096, gen_dense_random_device(32768, 0.5, 0)[0])))
     for name, rows in cases:
         m = ops.count_edges(rows)
         ip, ix = ops.dense_to_csr(rows)
         slot = t(lambda: ops.lexbfs_csr(ip, ix, rows.n))
-        arr = t(lambda: ops.lexbfs(DeviceRows(rows.n, rows.stride, rows.data, 10**12)))  # force arrangement
-        o1 = ops.lexbfs_csr(ip, ix, rows.n)[0]
-        o2 = ops.lexbfs(DeviceRows(rows.n, rows.stride, rows.data, 10**12))[0]
+        seg = t(lambda: ops.lexbfs(rows))  # n <= 32768: touched-segment arrangement engine
+        o1, _, p1 = ops.lexbfs_csr(ip, ix, rows.n)
+        o2, _, p2 = ops.lexbfs(rows, want_parent=True)
         same = bool(torch.equal(o1, o2))
-        print(f"{name:24s} m={m:9d} avgdeg={2 * m / rows.n:7.1f}  slot(smem/L2) {slot:9.3f} ms "
-              f"({slot * 1e6 / rows.n:8.1f} ns/step)  arrangement {arr:9.3f} ms  same={same}", flush=True)
+        known = p2 != -2
+        same_par = bool(torch.equal(p1[known], p2[known]))
+        print(f"{name:24s} m={m:9d} avgdeg={2 * m / rows.n:7.1f}  slot(CSR) {slot:9.3f} ms "
+              f"({slot * 1e6 / rows.n:8.1f} ns/step)  seg {seg:9.3f} ms ({seg * 1e6 / rows.n:8.1f} ns/step) "
+              f"same_order={same} same_parent={same_par}", flush=True)
 
 
 if __name__ == "__main__":
