@@ -39,6 +39,7 @@
 // the start of step i -- right whenever the head class is not split), so the
 // row fetch of step i+1 overlaps step i.
 #include "common.cuh"
+#include "warp_seg.cuh"
 
 namespace chordal {
 
@@ -251,7 +252,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
     const uint32_t *rows = reinterpret_cast<const uint32_t *>(adj);
     const long long sw = stride >> 2;  // row pitch in words (a multiple of 4)
 #ifdef SEG_PROFILE
-    unsigned long long seg_acc[9] = {0, 0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long seg_acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
     int tail = 1, nclasses = 1;
     int guess = -1;
@@ -557,7 +558,14 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
             __syncthreads();  // B2.5
             SEG_T(5);
             const int ntouch = fl[4];
+#ifdef SEG_PROFILE
+            seg_acc[9] += ntouch;
+            seg_acc[10] += cntA;
+#endif
             // ---- phase 3b: stable partition of split classes into An --------------
+#ifdef SEG_DOUBLE3B
+            for (int rep3 = 0; rep3 < 2; ++rep3)
+#endif
             for (int j0 = 4 * warp; j0 < ntouch; j0 += 4 * NW) {  // four words per round: loads overlap
                 int q[4], v[4], dst[4];
                 bool ok[4];
@@ -583,7 +591,11 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                         const uint32_t fq = F[q[u]];
                         const int fb = (int)Pc[q[u]] + __popc(fq & mask_below(lane)) - cs;
                         dst[u] = ((fq >> lane) & 1u) ? s + fb : s + T + (p - s - fb);
-                        if (p == s) {
+                        if (p == s
+#ifdef SEG_DOUBLE3B
+                            && rep3 == 0
+#endif
+                        ) {
                             atomicOr(&NB[(s + T) >> 5], 1u << ((s + T) & 31));
                             atomicAdd(fl + 5, 1);
                         }
@@ -596,6 +608,9 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
             __syncthreads();  // B3
             SEG_T(6);
             nclasses += fl[5];
+#ifdef SEG_PROFILE
+            seg_acc[11] += fl[5];
+#endif
             // ---- phase 3c: copy back and positions --------------------------------
             for (int j0 = 4 * warp; j0 < ntouch; j0 += 4 * NW) {
                 int p[4], v[4];
@@ -664,16 +679,50 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
     }
 #ifdef SEG_PROFILE
     if (t == 0)
-        for (int k = 0; k < 9; ++k) seg_prof[k] = seg_acc[k];
+        for (int k = 0; k < 12; ++k) seg_prof[k] = seg_acc[k];
 #endif
 }
 
 size_t seg_smem_bytes(int64_t n) { return SegLayout((int)((n + 31) >> 5)).total; }
 
+// n <= 1024, LOWEST_INDEX / descending ties: the one-warp engine (warp_seg.cuh),
+// bitsets in registers; the arrays are copied out at the end.
+template <int MODE>
+__global__ void __launch_bounds__(32, 1)
+lexbfs_warp_kernel(const uint8_t *__restrict__ adj, int n, long long stride, int32_t *__restrict__ order,
+                   int32_t *__restrict__ pos_out, int32_t *__restrict__ parent) {
+    extern __shared__ __align__(16) uint8_t smem[];
+    const size_t np = size_t((n + 31) >> 5) * 32;
+    WarpSegMem M;
+    M.A = (uint16_t *)smem;
+    M.An = M.A + np;
+    M.P = M.An + np;
+    M.par = M.P + np;
+    M.F = (uint32_t *)(M.par + np);
+    M.NB = M.F + 32;
+    warp_seg_lexbfs<MODE>(reinterpret_cast<const uint32_t *>(adj), (int)(stride >> 2), n, M);
+    for (int k = threadIdx.x; k < n; k += 32) {
+        order[k] = M.A[k];
+        pos_out[k] = M.P[k];
+        if (parent) parent[k] = (int)(int16_t)M.par[k];
+    }
+}
+
 int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int32_t tie_rule, uint64_t seed, uint64_t cell,
                       int32_t *order, int32_t *pos, int32_t *parent, cudaStream_t stream) {
     if (n <= 0) return CHORDAL_OK;
     if (n > CHORDAL_DENSE_LEXBFS_MAX_N) return CHORDAL_ETOOLARGE;
+    if (n <= 1024 && tie_rule != CHORDAL_TIE_SEEDED_ARB) {
+        const size_t wsmem = size_t((n + 31) >> 5) * 32 * 2 * 4 + 256;
+        if (tie_rule == CHORDAL_TIE_DESCENDING)
+            lexbfs_warp_kernel<CHORDAL_TIE_DESCENDING><<<1, 32, wsmem, stream>>>(adj, (int)n, stride, order, pos,
+                                                                                parent);
+        else
+            lexbfs_warp_kernel<CHORDAL_TIE_ASCENDING><<<1, 32, wsmem, stream>>>(adj, (int)n, stride, order, pos,
+                                                                               parent);
+        CH_LAUNCH_CHECK();
+        return CHORDAL_OK;
+    }
     const int W = (int)((n + 31) >> 5);
     const int T = max(32, ((W + 3) / 4 + 31) / 32 * 32);  // one thread per four row words
     const size_t smem = seg_smem_bytes(n);

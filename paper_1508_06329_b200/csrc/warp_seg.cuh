@@ -1,0 +1,326 @@
+// warp_seg.cuh -- one-warp LexBFS for graphs with n <= 1024 (the batch
+// kernel's engine and the single-graph path for small n).
+//
+// The touched-segment arrangement algorithm of lexbfs_seg.cu (search.py:328-532
+// / _arraylex.py:17-65 semantics, LOWEST_INDEX or fixed-descending ties) with
+// lane l owning 32-bit word l of every bitset, so that the per-step scans are
+// warp shuffles and the bitsets live in registers:
+//   registers  U (unreached), RA (reached unvisited), B (class starts over
+//              positions), the row word of the pivot and the speculative next
+//              row word;
+//   shared     A / An (arrangement and its scatter buffer), P (positions),
+//              par (PEO parents), F / NB (32-word mover and new-start bitsets
+//              written with shared atomics) -- 8 * 32W + 256 bytes per graph.
+// A step with no split class costs a few dozen instructions; a split step adds
+// three shuffle scans and one pass per touched word.  At the end A is the
+// order and P the positions.
+#pragma once
+#include "common.cuh"
+
+namespace chordal {
+
+#ifdef WSEG_PROFILE
+// [0] steps [1] row-guess hits [2] cycles waiting for the row [3] total cycles
+// [4] split steps (tools/warp_profile.cu only)
+__device__ unsigned long long wseg_prof[8];
+#endif
+
+struct WarpSegMem {
+    uint16_t *A, *An, *P;  // [32 W]
+    uint16_t *par;         // [n] or nullptr; 0xFFFF = no parent, 0xFFFE = left to the PEO check
+    uint32_t *F, *NB;      // [32]
+};
+
+namespace wseg {
+
+constexpr int kBig = 0x7FFFFFFF;
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t m;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+    return m;
+}
+
+// A load that is issued where it stands (the speculative next-row load must
+// not be sunk to its use one step later).
+__device__ __forceinline__ uint32_t ld_issue(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+
+}  // namespace wseg
+
+// rows: the graph's packed rows (global), sw: row pitch in 32-bit words.
+template <int MODE>
+__device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n, const WarpSegMem &M) {
+    using namespace wseg;
+    const int l = threadIdx.x & 31;
+    const int W = (n + 31) >> 5;
+    uint32_t Ul = l < W ? ((l < W - 1 || !(n & 31)) ? CH_FULL : mask_below(n & 31)) : 0u;
+    uint32_t RAl = 0, Bl = 0;
+    M.F[l] = 0;
+    M.NB[l] = 0;
+    if (M.par)
+        for (int v = l; v < n; v += 32) M.par[v] = 0xFFFF;
+    // every rule starts at vertex 0 (parallel/lexbfs.py:173)
+    if (l == 0) {
+        M.A[0] = 0;
+        M.P[0] = 0;
+        Ul &= ~1u;
+        Bl = 1u;
+    }
+    __syncwarp();
+    int tail = 1, nclasses = 1, guess = -1;
+    uint32_t nxt = 0;
+#ifdef WSEG_PROFILE
+    unsigned long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    const long long pstart = clock64();
+#endif
+    for (int i = 0; i < n; ++i) {
+        if (i == tail) {  // reached region empty: a new component from the unreached class
+            const uint32_t any = __ballot_sync(CH_FULL, Ul != 0);
+            int v;
+            if (MODE == CHORDAL_TIE_DESCENDING) {
+                const int src = highest_bit(any);
+                v = 32 * src + highest_bit(__shfl_sync(CH_FULL, Ul, src));
+            } else {
+                const int src = __ffs(any) - 1;
+                v = 32 * src + __ffs(__shfl_sync(CH_FULL, Ul, src)) - 1;
+            }
+            if (l == 0) {
+                M.A[i] = (uint16_t)v;
+                M.P[v] = (uint16_t)i;
+            }
+            if (l == (v >> 5)) Ul &= ~(1u << (v & 31));
+            if (l == (i >> 5)) Bl |= 1u << (i & 31);
+            tail = i + 1;
+            nclasses = 1;
+            __syncwarp();
+        }
+        const int x = M.A[i];
+        const int tail0 = tail, hpos = i + 1;
+        const uint32_t bh = __shfl_sync(CH_FULL, Bl, (hpos >> 5) & 31);
+        if (hpos >= tail0 || ((bh >> (hpos & 31)) & 1u)) --nclasses;  // x's class was {x}
+        // ---- row of x (speculatively loaded one step ahead) -------------------
+        uint32_t r = 0;
+#ifdef WSEG_PROFILE
+        pacc[0]++;
+        if (x == guess) pacc[1]++;
+        const long long pw0 = clock64();
+#endif
+        if (l < W) r = (x == guess) ? nxt : __ldg(rows + (long long)x * sw + l);
+#ifdef WSEG_PROFILE
+        {
+            const uint32_t any_r = __reduce_or_sync(CH_FULL, r);
+            if (any_r == 0xDEADBEEFu) pacc[7]++;  // forces the wait here
+            pacc[2] += clock64() - pw0;
+        }
+#endif
+        guess = hpos < tail0 ? (int)M.A[hpos] : -1;
+        if (guess >= 0 && l < W) nxt = ld_issue(rows + (long long)guess * sw + l);
+        if (l == (x >> 5)) RAl &= ~(1u << (x & 31));
+        uint32_t mv = r & RAl;
+        const uint32_t ext = r & Ul;
+        // ---- movers: flag their positions, record x as their parent ------------
+        const int cnt = __popc(mv);
+        int pmn = kBig, pmx = -1;
+        while (mv) {
+            int y[4], pp[4], c = 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                y[u] = 32 * l + __ffs(mv) - 1;
+                if (mv) ++c;
+                mv &= mv - 1;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) pp[u] = u < c ? (int)M.P[y[u]] : 0;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                if (u < c) {
+                    atomicOr(&M.F[pp[u] >> 5], 1u << (pp[u] & 31));
+                    if (M.par) M.par[y[u]] = (uint16_t)x;
+                    pmn = min(pmn, pp[u]);
+                    pmx = max(pmx, pp[u]);
+                }
+            }
+        }
+        if (ext) {
+            if (M.par) {
+                uint32_t m3 = ext;
+                while (m3) {
+                    M.par[32 * l + __ffs(m3) - 1] = (uint16_t)x;
+                    m3 &= m3 - 1;
+                }
+            }
+            Ul &= ~ext;
+            RAl |= ext;
+        }
+        const int cntA = __reduce_add_sync(CH_FULL, cnt);
+        // newly reached vertices: exclusive prefix over lanes (= id order)
+        const int ec = __popc(ext);
+        int incl = ec;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+            const int o = __shfl_up_sync(CH_FULL, incl, d);
+            if (l >= d) incl += o;
+        }
+        const int xe = incl - ec;
+        const int ktot = __shfl_sync(CH_FULL, incl, 31);
+
+        if (cntA) {
+            __syncwarp();  // the mover flags are in F
+            const uint32_t Fl = M.F[l];
+            M.F[l] = 0;
+            const int gmn = (int)__reduce_min_sync(CH_FULL, (unsigned)pmn);
+            const int gmx = __reduce_max_sync(CH_FULL, pmx);
+            const uint32_t bmn = __shfl_sync(CH_FULL, Bl, (gmn >> 5) & 31);
+            const uint32_t bmx = __shfl_sync(CH_FULL, Bl, ((gmx + 1) >> 5) & 31);
+            // movers that fill a run of whole classes change nothing (search.py:448-453)
+            const bool whole = cntA == gmx - gmn + 1 && (gmn == hpos || ((bmn >> (gmn & 31)) & 1u)) &&
+                               (gmx + 1 >= tail0 || ((bmx >> ((gmx + 1) & 31)) & 1u));
+            if (!whole && gmn > hpos) {
+                // A split of the head class [hpos, ...) brings its first mover (the
+                // smallest mover position gmn, if no class starts in (hpos, gmn])
+                // to hpos: re-aim the speculative row load at it.
+                uint32_t sb = Bl;
+                const int lo2 = hpos + 1 - 32 * l, hi2 = gmn + 1 - 32 * l;
+                sb &= lo2 <= 0 ? CH_FULL : (lo2 >= 32 ? 0u : ~mask_below(lo2));
+                sb &= hi2 <= 0 ? 0u : mask_below(min(hi2, 32));
+                if (!__any_sync(CH_FULL, sb != 0)) {
+                    guess = M.A[gmn];
+                    if (l < W) nxt = ld_issue(rows + (long long)guess * sw + l);
+                }
+            }
+#ifdef WSEG_PROFILE
+            if (!whole) pacc[4]++;
+#endif
+            if (!whole) {
+                // region class starts of word l: [hpos, tail0) with hpos forced
+                uint32_t b = Bl;
+                {
+                    const int lo = hpos - 32 * l;
+                    if (lo > 0) b = lo >= 32 ? 0u : (b & ~mask_below(lo));
+                    if (lo >= 0 && lo < 32) b |= 1u << lo;
+                }
+                const int fc = __popc(Fl);
+                const int hb = b ? 32 * l + highest_bit(b) : 0;
+                const int lb = b ? 32 * l + __ffs(b) - 1 : kBig;
+                int ia = fc, ih = hb, il = lb;
+#pragma unroll
+                for (int d = 1; d < 32; d <<= 1) {
+                    const int oa = __shfl_up_sync(CH_FULL, ia, d), oh = __shfl_up_sync(CH_FULL, ih, d);
+                    const int ol = __shfl_down_sync(CH_FULL, il, d);
+                    if (l >= d) { ia += oa; ih = max(ih, oh); }
+                    if (l + d < 32) il = min(il, ol);
+                }
+                const int Pc = ia - fc;  // movers before word l
+                int LBr = __shfl_up_sync(CH_FULL, ih, 1);  // last class start before word l
+                int NBr = __shfl_down_sync(CH_FULL, il, 1);  // first class start after word l
+                if (l == 0) LBr = 0;
+                if (l == 31) NBr = kBig;
+                NBr = min(NBr, tail0);
+                // movers at positions < pp (all lanes must call: shuffles)
+                auto cntb = [&](int pp) -> int {
+                    const int q = pp >> 5;
+                    const int pcq = __shfl_sync(CH_FULL, Pc, q & 31);
+                    const uint32_t fq = __shfl_sync(CH_FULL, Fl, q & 31);
+                    return q >= W ? cntA : pcq + __popc(fq & mask_below(pp & 31));
+                };
+                // ---- words of split classes ---------------------------------------
+                const int lo = max(32 * l, hpos), hi = min(32 * l + 32, tail0);
+                const bool inr = lo < hi;
+                const int lob = inr ? lo - 32 * l : 0, hib = inr ? hi - 32 * l : 0;
+                const uint32_t vm = inr ? (mask_below(hib) & ~mask_below(lob)) : 0u;
+                bool touched = (((Fl ^ (Fl >> 1)) & ~(b >> 1)) & vm & (vm >> 1)) != 0;
+                // a class entering from the previous word / leaving into the next one
+                const int s_in = LBr, e_in = b ? 32 * l + __ffs(b) - 1 : NBr;
+                const int s_out = b ? 32 * l + highest_bit(b) : 0, e_out = NBr;
+                const int c1 = cntb(s_in), c2 = cntb(e_in), c3 = cntb(s_out), c4 = cntb(e_out);
+                if (inr && !touched && !((b >> lob) & 1u)) {
+                    const int T = c2 - c1;
+                    touched = T > 0 && T < e_in - s_in;
+                }
+                if (inr && !touched && hib == 32 && NBr > 32 * l + 32 && b) {
+                    const int T = c4 - c3;
+                    touched = T > 0 && T < e_out - s_out;
+                }
+                const uint32_t tmask = __ballot_sync(CH_FULL, touched);
+                // ---- stable partition of every split class: movers first -----------
+                int nsp = 0;
+                for (uint32_t tm = tmask; tm; tm &= tm - 1) {
+                    const int q = __ffs(tm) - 1;
+                    const uint32_t bq = __shfl_sync(CH_FULL, b, q), fq = __shfl_sync(CH_FULL, Fl, q);
+                    const int lbq = __shfl_sync(CH_FULL, LBr, q), nbq = __shfl_sync(CH_FULL, NBr, q);
+                    const int pcq = __shfl_sync(CH_FULL, Pc, q);
+                    const int p = 32 * q + l;
+                    const bool ok = p >= hpos && p < tail0;
+                    const uint32_t bl = bq & mask_below(l + 1), ab = bq & ~mask_below(l + 1);
+                    const int s = bl ? 32 * q + highest_bit(bl) : lbq;
+                    const int e = ab ? 32 * q + __ffs(ab) - 1 : nbq;
+                    const int cs = cntb(s), T = cntb(e) - cs;
+                    const int v = M.A[p];
+                    if (ok) {
+                        int dst = p;
+                        if (T > 0 && T < e - s) {
+                            const int fb = pcq + __popc(fq & mask_below(l)) - cs;
+                            dst = ((fq >> l) & 1u) ? s + fb : s + T + (p - s - fb);
+                            if (p == s) {
+                                atomicOr(&M.NB[(s + T) >> 5], 1u << ((s + T) & 31));
+                                ++nsp;
+                            }
+                        }
+                        M.An[dst] = (uint16_t)v;
+                    }
+                }
+                __syncwarp();
+                for (uint32_t tm = tmask; tm; tm &= tm - 1) {
+                    const int p = 32 * (__ffs(tm) - 1) + l;
+                    if (p >= hpos && p < tail0) {
+                        const int v = M.An[p];
+                        M.A[p] = (uint16_t)v;
+                        M.P[v] = (uint16_t)p;
+                    }
+                }
+                nclasses += __reduce_add_sync(CH_FULL, nsp);
+                __syncwarp();
+                Bl |= M.NB[l];
+                M.NB[l] = 0;
+            }
+        }
+        // ---- append the newly reached vertices as one class (tie order) ---------
+        if (ext) {
+            int idx = xe;
+            uint32_t e2 = ext;
+            while (e2) {
+                const int y = 32 * l + __ffs(e2) - 1;
+                e2 &= e2 - 1;
+                const int dst = (MODE == CHORDAL_TIE_DESCENDING) ? tail0 + (ktot - 1 - idx) : tail0 + idx;
+                ++idx;
+                M.A[dst] = (uint16_t)y;
+                M.P[y] = (uint16_t)dst;
+            }
+        }
+        if (hpos < tail0 && l == (hpos >> 5)) Bl |= 1u << (hpos & 31);
+        if (ktot > 0 && l == (tail0 >> 5)) Bl |= 1u << (tail0 & 31);
+        if (ktot > 0) {
+            tail = tail0 + ktot;
+            ++nclasses;
+        }
+        __syncwarp();
+        // ---- early exit: everything reached, every class a singleton ---------------
+        if (tail == n && nclasses == tail - hpos) {
+            if (M.par)
+                for (int p = hpos + l; p < n; p += 32) M.par[M.A[p]] = 0xFFFE;
+            break;
+        }
+    }
+    __syncwarp();
+#ifdef WSEG_PROFILE
+    pacc[3] = clock64() - pstart;
+    if (l == 0)
+        for (int k = 0; k < 8; ++k) atomicAdd(&wseg_prof[k], pacc[k]);
+#endif
+}
+
+}  // namespace chordal
