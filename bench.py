@@ -430,12 +430,16 @@ def run_ours(args, rank, world, local):
                                                        wit_h.data_ptr(), 8192)
         _native.check(rc, "chordal_is_chordal_batch_host")
 
-    e2e_step()
+    for _ in range(max(3, args.warmup)):  # first calls map the staging buffers
+        e2e_step()
     e2e_steps = max(2, min(args.steps, 5))
     barrier(world)
     t0 = time.perf_counter()
+    call_ms = []
     for _ in range(e2e_steps):
+        tc = time.perf_counter()
         e2e_step()
+        call_ms.append(round(1e3 * (time.perf_counter() - tc), 2))
     e2e_s = reduce_max(time.perf_counter() - t0, world)
     assert torch.equal(wit_h, wit.cpu()) and torch.equal(orders_h, orders.cpu()), "e2e result differs"
     e2e_value = args.graphs * e2e_steps / e2e_s
@@ -462,7 +466,8 @@ def run_ours(args, rank, world, local):
                      "kernel": "batch_chordal_kernel", "peak_kind": peak_kind,
                      "algorithmic_bytes_per_graph": BYTES_PER_GRAPH},
         "e2e": {"value": e2e_value, "unit": "graphs/s", "h2d_bytes_per_step": B * N512 * STRIDE512,
-                "d2h_bytes_per_step": B * (4 * N512 + 12), "api": "chordal_is_chordal_batch_host"},
+                "d2h_bytes_per_step": B * (4 * N512 + 12), "api": "chordal_is_chordal_batch_host",
+                "calls_ms": call_ms},
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
         "chordal_fraction": float((wit[:, 0] < 0).float().mean().item()),

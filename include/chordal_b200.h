@@ -20,7 +20,10 @@
  *  - "_dev" arguments are device pointers; every call is asynchronous on
  *    `stream` (a cudaStream_t; NULL = legacy default stream) unless the name
  *    ends in _host.  The library keeps no global mutable state, holds no
- *    caller pointer after return and is reentrant per stream.
+ *    caller pointer after return and is reentrant per stream.  The _host
+ *    entry points allocate stream-ordered from the device's default memory
+ *    pool and raise that pool's release threshold to one call's footprint so
+ *    the buffers stay mapped between calls (the only process-wide effect).
  *  - Witness triples are int32[3] = (v, p, z) -- WitnessTriple (peo.py:26-45),
  *    0-based -- or (-1, -1, -1) when the ordering is a PEO.
  *  - Every function returns a chordal status code (CHORDAL_OK == 0).

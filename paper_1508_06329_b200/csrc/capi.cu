@@ -54,6 +54,21 @@ uint32_t crc32_str(const char *s) {
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// The host-buffer entry points allocate their device buffers stream-ordered
+// from the device's default pool.  With the pool's default release threshold
+// (0) every call would hand the memory back to the driver and map it again on
+// the next call (tens of ms for the batch staging buffers); raising the
+// threshold to the bytes one call needs keeps them cached.  Only ever raised.
+void keep_pool_bytes(size_t bytes) {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+    uint64_t cur = 0;
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &cur) != cudaSuccess) return;
+    uint64_t want = bytes;
+    if (cur < want) cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &want);
+}
+
 int check_dense(const void *adj, int64_t n, int64_t stride) {
     if (n < 0) return CHORDAL_EINVAL;
     if (n == 0) return CHORDAL_OK;
@@ -257,6 +272,7 @@ int chordal_is_chordal_dense_host(const uint8_t *adj_host, int64_t n, int64_t ro
             if (rc) break;
         }
         const size_t wsb = DenseWs(n, m).total;
+        keep_pool_bytes(adj_bytes + sizeof(int32_t) * (2 * n + 4) + wsb + 16);
         if (cudaMallocAsync((void **)&ws, wsb + 16, s) != cudaSuccess) { rc = CHORDAL_ENOMEM; break; }
         int32_t *wit = reinterpret_cast<int32_t *>(ws + wsb);
         rc = chordal_is_chordal_dense(adj, n, stride, m, tie_rule, seed, order, order + n, ws, wsb, wit, s);
@@ -370,6 +386,7 @@ int chordal_is_chordal_batch_host(const uint8_t *adj_host, int64_t batch, int64_
     const int64_t stride = (((n + 7) / 8) + 15) / 16 * 16;
     const size_t gbytes = (size_t)n * stride;
     constexpr int NB = 3;  // H2D of chunk c+1 and D2H of c-1 overlap the search of c
+    keep_pool_bytes(NB * (gbytes * chunk + sizeof(int32_t) * (n + 3) * chunk));
     cudaStream_t st[NB] = {};
     uint8_t *buf[NB] = {};
     int32_t *ord[NB] = {};

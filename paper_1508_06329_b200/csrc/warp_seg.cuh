@@ -119,6 +119,8 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
 #endif
         guess = hpos < tail0 ? (int)M.A[hpos] : -1;
         if (guess >= 0 && l < W) nxt = ld_issue(rows + (long long)guess * sw + l);
+        if (hpos + 1 < tail0 && l == 0)  // two steps ahead: warm L2
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(rows + (long long)M.A[hpos + 1] * sw));
         if (l == (x >> 5)) RAl &= ~(1u << (x & 31));
         uint32_t mv = r & RAl;
         const uint32_t ext = r & Ul;
