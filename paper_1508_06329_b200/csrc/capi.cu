@@ -7,7 +7,7 @@
 #include "common.cuh"
 
 namespace chordal {
-int launch_lexbfs_seg(const uint8_t *, int64_t, int64_t, int32_t, uint64_t, uint64_t, int32_t *, int32_t *,
+int launch_lexbfs_seg(const uint8_t *, int64_t, int64_t, int64_t, int32_t, uint64_t, uint64_t, int32_t *, int32_t *,
                       int32_t *, cudaStream_t);
 int launch_positions(const int32_t *, int64_t, int32_t *, cudaStream_t);
 int launch_fill_i32(int32_t *, int64_t, int32_t, cudaStream_t);
@@ -149,7 +149,7 @@ int chordal_lexbfs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int6
     cudaStream_t s = as_stream(stream);
     const uint64_t cell = current_cell(crc32_str("current"));
     if (use_seg(n))
-        return launch_lexbfs_seg(adj_dev, n, stride, tie_rule, seed, cell, order_dev, pos_dev, parent_dev, s);
+        return launch_lexbfs_seg(adj_dev, n, stride, m, tie_rule, seed, cell, order_dev, pos_dev, parent_dev, s);
     if (m < 0) {
         rc = count_edges_sync(adj_dev, n, stride, s, &m);
         if (rc) return rc;
@@ -267,7 +267,7 @@ int chordal_is_chordal_dense_host(const uint8_t *adj_host, int64_t n, int64_t ro
         if (stride != row_bytes && cudaMemsetAsync(adj, 0, adj_bytes, s) != cudaSuccess) { rc = CHORDAL_ECUDA; break; }
         if (cudaMemcpy2DAsync(adj, stride, adj_host, row_bytes, (n + 7) / 8, n, cudaMemcpyHostToDevice, s) !=
             cudaSuccess) { rc = CHORDAL_ECUDA; break; }
-        if (!use_seg(n)) {
+        if (n > 1024) {  // the engine choice (CSR route) and its thread count depend on the density
             rc = count_edges_sync(adj, n, stride, s, &m);
             if (rc) break;
         }

@@ -63,6 +63,7 @@ __device__ unsigned long long seg_prof[16];
 namespace {
 
 constexpr int kSegBig = 0x7FFFFFFF;
+constexpr int kSegDenseDeg = 64;  // average degree from which the kernel runs 512 threads
 
 struct SegLayout {
     size_t A, An, P, U, RA, F, NB, bnd, Pc, LB, NBq, TW, wt, misc, total;
@@ -194,7 +195,7 @@ __device__ __forceinline__ int seg_scan1(int e, int *wt, int &te) {
 }  // namespace
 
 template <int MODE>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(512, 1)
 lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint64_t seed, uint64_t cell,
                   int32_t *__restrict__ order, int32_t *__restrict__ pos_out, int32_t *__restrict__ parent) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -708,7 +709,7 @@ lexbfs_warp_kernel(const uint8_t *__restrict__ adj, int n, long long stride, int
     }
 }
 
-int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int32_t tie_rule, uint64_t seed, uint64_t cell,
+int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int64_t m, int32_t tie_rule, uint64_t seed, uint64_t cell,
                       int32_t *order, int32_t *pos, int32_t *parent, cudaStream_t stream) {
     if (n <= 0) return CHORDAL_OK;
     if (n > CHORDAL_DENSE_LEXBFS_MAX_N) return CHORDAL_ETOOLARGE;
@@ -724,7 +725,14 @@ int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int32_t tie
         return CHORDAL_OK;
     }
     const int W = (int)((n + 31) >> 5);
-    const int T = max(32, ((W + 3) / 4 + 31) / 32 * 32);  // one thread per four row words
+    // One thread per four row words; graphs with a high average degree (m known,
+    // 2m/n >= kSegDenseDeg) split many classes per step, and their partition
+    // phases (3b / 3c, one warp per four split-class words) run on 512 threads.
+    int T = max(32, ((W + 3) / 4 + 31) / 32 * 32);
+    if (m >= 0 && n > 1024 && 2 * m >= kSegDenseDeg * n) T = max(T, 512);
+#ifdef SEG_THREADS_ENV
+    if (const char *ev = getenv("SEG_THREADS")) T = max(T, atoi(ev));
+#endif
     const size_t smem = seg_smem_bytes(n);
     cudaError_t e;
 #define SEG_LAUNCH(M)                                                                                          \

@@ -1,6 +1,6 @@
 """Small driver for ncu captures: runs each hot kernel a few times on config inputs.
 
-    python tools/profile_driver.py {batch|lexbfs32k|peo32k|lexbfs1k|all}
+    python tools/profile_driver.py {batch|batch_chordal|batch_dense|lexbfs32k|peo32k|lexbfs1k|all}
 """
 import os
 import sys
@@ -23,8 +23,12 @@ def rows_chordal(n, k, seed):
 
 
 def main(what):
-    if what in ("batch", "all"):
+    if what in ("batch", "all", "batch_chordal", "batch_dense"):
         adj = bench.build_batch(0, int(os.environ.get("GRAPHS", "16384")), "cuda")
+        if what == "batch_chordal":
+            adj = adj[1::2].contiguous()
+        elif what == "batch_dense":
+            adj = adj[0::2].contiguous()
         for _ in range(3):
             ops.is_chordal_batch(adj, 512, 64)
     if what in ("lexbfs32k", "peo32k", "all"):

@@ -6,6 +6,7 @@
 //   tools/seg_profile graph.bin      (int64 n, int64 stride, then n*stride bytes)
 #include <cstdio>
 #include <cstdlib>
+#define SEG_THREADS_ENV
 #include <vector>
 
 #include "../paper_1508_06329_b200/csrc/lexbfs_seg.cu"
@@ -32,7 +33,7 @@ int main(int argc, char **argv) {
         cudaEventCreate(&a);
         cudaEventCreate(&b);
         cudaEventRecord(a);
-        int rc = chordal::launch_lexbfs_seg(adj, n, stride, CHORDAL_TIE_ASCENDING, 0, cell, ord, ord + n, ord + 2 * n,
+        int rc = chordal::launch_lexbfs_seg(adj, n, stride, -1, CHORDAL_TIE_ASCENDING, 0, cell, ord, ord + n, ord + 2 * n,
                                             0);
         cudaEventRecord(b);
         cudaEventSynchronize(b);

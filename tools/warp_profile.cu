@@ -29,7 +29,7 @@ int main(int argc, char **argv) {
         cudaEventCreate(&a);
         cudaEventCreate(&b);
         cudaEventRecord(a);
-        int rc = chordal::launch_lexbfs_seg(adj, n, stride, CHORDAL_TIE_ASCENDING, 0, 0, ord, ord + n, ord + 2 * n, 0);
+        int rc = chordal::launch_lexbfs_seg(adj, n, stride, -1, CHORDAL_TIE_ASCENDING, 0, 0, ord, ord + n, ord + 2 * n, 0);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
         float ms = 0;
