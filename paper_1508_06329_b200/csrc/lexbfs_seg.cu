@@ -253,7 +253,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
     const uint32_t *rows = reinterpret_cast<const uint32_t *>(adj);
     const long long sw = stride >> 2;  // row pitch in words (a multiple of 4)
 #ifdef SEG_PROFILE
-    unsigned long long seg_acc[12] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long seg_acc[16] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
 #endif
     int tail = 1, nclasses = 1;
     int guess = -1;
@@ -607,6 +607,13 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                     if (ok[u]) An[dst[u]] = (uint16_t)v[u];
             }
             __syncthreads();  // B3
+#ifdef SEG_PROFILE
+            {  // 3b cycles of small (<= 64 words) and large split steps
+                const long long c3b = clock64() - seg_t0;
+                seg_acc[ntouch <= 64 ? 12 : 14] += (unsigned long long)c3b;
+                seg_acc[ntouch <= 64 ? 13 : 15] += 1;
+            }
+#endif
             SEG_T(6);
             nclasses += fl[5];
 #ifdef SEG_PROFILE
@@ -680,7 +687,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
     }
 #ifdef SEG_PROFILE
     if (t == 0)
-        for (int k = 0; k < 12; ++k) seg_prof[k] = seg_acc[k];
+        for (int k = 0; k < 16; ++k) seg_prof[k] = seg_acc[k];
 #endif
 }
 
