@@ -43,6 +43,8 @@ extern "C" {
 #define CHORDAL_ETOOLARGE 2  /* n beyond this kernel's capacity (maps to GraphTooLarge) */
 #define CHORDAL_ECUDA 3      /* CUDA launch/runtime failure */
 #define CHORDAL_ENOMEM 4     /* device allocation failed (host-buffer entry points) */
+#define CHORDAL_EPARSE 5     /* text input rejected (maps to ParseError; line + message returned) */
+#define CHORDAL_EUTF8 6      /* text input is not valid UTF-8 (maps to ParseError) */
 
 /* LexBFS tie rules.
  *  ASCENDING  : max label, ties -> smallest vertex id.  = lexbfs_partition /
@@ -222,6 +224,34 @@ int chordal_gen_chordal_random_edges(int64_t n, int64_t k, int64_t seed, int32_t
                                      int64_t *m_dev, void *scratch_dev, size_t scratch_bytes, void *stream);
 int chordal_gen_chordal_random(uint8_t *adj_dev, int64_t batch, int64_t n, int64_t stride, int64_t k, int64_t seed0,
                                int64_t seed_step, void *scratch_dev, size_t scratch_bytes, void *stream);
+
+/* ---- plain-text formats (host side, textio.py) ---------------------------- */
+
+/* parse_graph_text (textio.py:30-86) straight into packed rows.  Two calls:
+ * with rows_out == NULL the text is scanned up to its header and *n_out /
+ * *m_out are returned (errors before or on the header are reported); the
+ * caller then passes zeroed rows_out[n * row_bytes] (row_bytes >= ceil(n/8))
+ * and the whole text is validated while the bits are set.  cap: the vertex cap
+ * of _check_size (graph.py:23-28), < 0 = none.  Errors: CHORDAL_EPARSE with
+ * *err_line (1-based, -1 = no line) and err_msg = the reference's message;
+ * CHORDAL_ETOOLARGE with err_msg = n in decimal (GraphTooLarge);
+ * CHORDAL_EUTF8.  Host memory only; no CUDA. */
+int chordal_parse_graph_text(const char *text, int64_t len, int64_t cap, int64_t *n_out, int64_t *m_out,
+                             uint8_t *rows_out, int64_t row_bytes, int64_t *err_line, char *err_msg,
+                             int64_t err_cap);
+
+/* write_graph_text (textio.py:89-93): "p n m" then "e u v" for u < v
+ * ascending.  Returns the text length; writes it to out when out_cap is large
+ * enough (call with out = NULL to size the buffer); -1 on bad arguments. */
+int64_t chordal_write_graph_text(const uint8_t *rows, int64_t n, int64_t row_bytes, int64_t m, char *out,
+                                 int64_t out_cap);
+
+/* parse_ordering_text's field scan (textio.py:96-106): whitespace-separated
+ * integers; the first n go to order_out (1-based ids as written), *count_out =
+ * the number of fields.  The caller raises InvalidOrdering on a count or
+ * permutation mismatch. */
+int chordal_parse_ordering_text(const char *text, int64_t len, int64_t n, int64_t *order_out, int64_t *count_out,
+                                int64_t *err_line, char *err_msg, int64_t err_cap);
 
 #ifdef __cplusplus
 }

@@ -19,7 +19,7 @@ LIB = os.path.join(LIBDIR, "libchordal_b200.so")
 ROOT = os.path.dirname(HERE)
 INCLUDE = os.path.join(ROOT, "include")
 
-SOURCES = ["capi.cu", "dense_util.cu", "lexbfs_seg.cu", "peo_dense.cu", "batch.cu", "gen.cu", "csr.cu"]
+SOURCES = ["capi.cu", "dense_util.cu", "lexbfs_seg.cu", "peo_dense.cu", "batch.cu", "gen.cu", "csr.cu", "textio.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = [
     "-O3",
@@ -61,7 +61,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
         src = os.path.join(CSRC, s)
         if not os.path.exists(src):
             continue
-        obj = os.path.join(LIBDIR, s.replace(".cu", ".o"))
+        obj = os.path.join(LIBDIR, os.path.splitext(s)[0] + ".o")
         cmd = [_nvcc(), *ARCH, *FLAGS, "-I", INCLUDE, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log.append(r.stdout + r.stderr)

@@ -15,7 +15,7 @@ from .errors import DeviceError, GraphTooLarge, InvalidOrdering
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libchordal_b200.so")
 
-OK, EINVAL, ETOOLARGE, ECUDA, ENOMEM = 0, 1, 2, 3, 4
+OK, EINVAL, ETOOLARGE, ECUDA, ENOMEM, EPARSE, EUTF8 = 0, 1, 2, 3, 4, 5, 6
 TIE_ASCENDING, TIE_DESCENDING, TIE_SEEDED_ARB = 0, 1, 2
 DENSE_LEXBFS_MAX_N = 32768
 BATCH_MAX_N = 1024
@@ -49,12 +49,16 @@ SIGNATURES = {
     "chordal_gen_chordal_random_scratch_bytes": [_I64, _I64, _I64],
     "chordal_gen_chordal_random": [_P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _SZ, _P],
     "chordal_gen_chordal_random_edges": [_I64, _I64, _I64, _P, _P, _P, _P, _SZ, _P],
+    "chordal_parse_graph_text": [_P, _I64, _I64, _P, _P, _P, _I64, _P, _P, _I64],
+    "chordal_write_graph_text": [_P, _I64, _I64, _I64, _P, _I64],
+    "chordal_parse_ordering_text": [_P, _I64, _I64, _P, _P, _P, _P, _I64],
 }
 _RESTYPES = {
     "chordal_strerror": ctypes.c_char_p,
     "chordal_gen_chordal_random_scratch_bytes": _SZ,
     "chordal_dense_workspace_bytes": _SZ,
     "chordal_lexbfs_csr_workspace_bytes": _SZ,
+    "chordal_write_graph_text": _I64,
 }
 
 if not os.path.exists(LIB_PATH):

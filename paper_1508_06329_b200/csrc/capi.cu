@@ -92,6 +92,8 @@ const char *chordal_strerror(int status) {
         case CHORDAL_ETOOLARGE: return "graph too large for this kernel";
         case CHORDAL_ECUDA: return "CUDA error";
         case CHORDAL_ENOMEM: return "device allocation failed";
+        case CHORDAL_EPARSE: return "text input rejected";
+        case CHORDAL_EUTF8: return "text input is not valid UTF-8";
         default: return "unknown status";
     }
 }
