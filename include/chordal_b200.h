@@ -57,10 +57,21 @@ extern "C" {
  *               at iteration i the winner among the max-label set is
  *               argmax_w (splitmix64(prefix_i ^ w), w), w 1-based,
  *               prefix_i = mix64(seed, 4(i-1)+3, mix64(crc32("current"), 0))
- *               (parallel/engine.py:47-53, parallel/lexbfs.py:211-225).      */
+ *               (parallel/engine.py:47-53, parallel/lexbfs.py:211-225).
+ *  SEEDED_PARTITION (CSR entry point only): lexbfs_partition(seeded(seed),
+ *               method="linked") (search.py:515-532): the initial class is
+ *               range(n) shuffled by Generator.shuffle on the stream
+ *               (seed, "lexbfs-partition"); split-off and fully moved classes
+ *               hold their members in adjacency order.
+ *  SEEDED_LABELS (CSR entry point only): lexbfs_labels(seeded(seed),
+ *               method="linked") (search.py:283-290): the pivot is member
+ *               Generator.integers(|C|) of the max-label class C (ascending id
+ *               order) on the stream (seed, "lexbfs-labels").                  */
 #define CHORDAL_TIE_ASCENDING 0
 #define CHORDAL_TIE_DESCENDING 1
 #define CHORDAL_TIE_SEEDED_ARB 2
+#define CHORDAL_TIE_SEEDED_PARTITION 3
+#define CHORDAL_TIE_SEEDED_LABELS 4
 
 /* Largest n the single-CTA dense LexBFS kernel accepts (state lives in SMEM). */
 #define CHORDAL_DENSE_LEXBFS_MAX_N 32768

@@ -46,6 +46,8 @@ def lib():
         L.oracle_lexbfs_partition.argtypes = [P, i64, i64, P, P]
         L.oracle_lexbfs_partition_csr.argtypes = [P, P, i64, P]
         L.oracle_lexbfs_array.argtypes = [P, i64, i64, P, P]
+        L.oracle_lexbfs_partition_seeded.argtypes = [P, i64, i64, ctypes.c_uint64, P]
+        L.oracle_lexbfs_labels_seeded.argtypes = [P, i64, i64, ctypes.c_uint64, P]
         L.oracle_lexbfs_arbitrated.argtypes = [P, i64, i64, ctypes.c_int, ctypes.c_uint64, P]
         L.oracle_is_peo.argtypes = [P, i64, i64, P, P]
         L.oracle_is_peo_csr.argtypes = [P, P, i64, P, P]
@@ -111,6 +113,17 @@ def is_peo(packed: np.ndarray, n: int, order0: np.ndarray) -> tuple[bool, tuple[
     if rc < 0:
         raise MemoryError("oracle_is_peo")
     return (True, None) if rc == 1 else (False, (int(w[0]), int(w[1]), int(w[2])))
+
+
+def lexbfs_linked_seeded(packed: np.ndarray, n: int, seed: int, variant: str) -> np.ndarray:
+    """Seeded linked LexBFS: variant "partition" (search.py:515-532) or
+    "labels" (search.py:283-310); 0-based order."""
+    rows = np.ascontiguousarray(packed, dtype=np.uint8)
+    order = np.empty(max(n, 1), dtype=np.int32)
+    fn = lib().oracle_lexbfs_partition_seeded if variant == "partition" else lib().oracle_lexbfs_labels_seeded
+    if fn(_ptr(rows), n, rows.shape[1] if n else 0, int(seed) & 0xFFFFFFFFFFFFFFFF, _ptr(order)):
+        raise MemoryError("oracle seeded linked LexBFS")
+    return order[:n]
 
 
 def lexbfs_partition_csr(indptr: np.ndarray, indices: np.ndarray, n: int) -> np.ndarray:

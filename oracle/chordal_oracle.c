@@ -265,6 +265,148 @@ int oracle_lexbfs_partition_csr(const int64_t *indptr, const int32_t *indices, i
 }
 
 /* ---------------------------------------------------------------------------
+ * numpy's Philox4x64-10 bit generator and the two Generator draws the seeded
+ * linked LexBFS variants use (rng.py:18-21: key = mix64(seed, crc32(label)),
+ * 256-bit counter starting at 0, incremented before each 4-word block;
+ * next_uint32 hands out the low then the high half of a 64-bit output and
+ * keeps the other half buffered across calls).
+ *   random_interval(max)   masked rejection (Generator.shuffle's Fisher-Yates)
+ *   bounded(rng)           Lemire 32-bit rejection (Generator.integers)
+ */
+typedef struct {
+    uint64_t key, ctr, blk[4];
+    int pos, has32;
+    uint32_t u32;
+} philox_t;
+
+static void philox_init(philox_t *r, uint64_t key) {
+    memset(r, 0, sizeof *r);
+    r->key = key;
+    r->pos = 4;
+}
+
+static uint64_t philox_next64(philox_t *r) {
+    if (r->pos >= 4) {
+        uint64_t c[4] = {++r->ctr, 0, 0, 0}, k0 = r->key, k1 = 0;
+        for (int i = 0; i < 10; ++i) {
+            __uint128_t p0 = (__uint128_t)0xD2E7470EE14C6C93ULL * c[0];
+            __uint128_t p1 = (__uint128_t)0xCA5A826395121157ULL * c[2];
+            uint64_t hi0 = (uint64_t)(p0 >> 64), lo0 = (uint64_t)p0;
+            uint64_t hi1 = (uint64_t)(p1 >> 64), lo1 = (uint64_t)p1;
+            uint64_t n0 = hi1 ^ c[1] ^ k0, n1 = lo1, n2 = hi0 ^ c[3] ^ k1, n3 = lo0;
+            c[0] = n0; c[1] = n1; c[2] = n2; c[3] = n3;
+            k0 += 0x9E3779B97F4A7C15ULL;
+            k1 += 0xBB67AE8584CAA73BULL;
+        }
+        memcpy(r->blk, c, sizeof c);
+        r->pos = 0;
+    }
+    return r->blk[r->pos++];
+}
+
+static uint32_t philox_next32(philox_t *r) {
+    if (r->has32) { r->has32 = 0; return r->u32; }
+    uint64_t x = philox_next64(r);
+    r->has32 = 1;
+    r->u32 = (uint32_t)(x >> 32);
+    return (uint32_t)x;
+}
+
+static uint32_t philox_interval(philox_t *r, uint32_t max) {
+    if (max == 0) return 0;
+    uint32_t mask = max, v;
+    mask |= mask >> 1; mask |= mask >> 2; mask |= mask >> 4; mask |= mask >> 8; mask |= mask >> 16;
+    while ((v = philox_next32(r) & mask) > max) {
+    }
+    return v;
+}
+
+static uint32_t philox_bounded(philox_t *r, uint32_t rng) { /* [0, rng], rng < 2^32 - 1 */
+    if (rng == 0) return 0;
+    const uint32_t excl = rng + 1u;
+    uint64_t m = (uint64_t)philox_next32(r) * excl;
+    uint32_t left = (uint32_t)m;
+    if (left < excl) {
+        const uint32_t th = (0xFFFFFFFFu - rng) % excl;
+        while (left < th) {
+            m = (uint64_t)philox_next32(r) * excl;
+            left = (uint32_t)m;
+        }
+    }
+    return (uint32_t)(m >> 32);
+}
+
+static uint64_t stream_key(uint64_t seed, const char *label) {
+    return oracle_splitmix64(oracle_splitmix64(seed) ^ (uint64_t)crc32_str(label));
+}
+
+/* lexbfs_partition(g, seeded(seed), method="linked"), search.py:515-532: the
+ * members are range(n) after Generator.shuffle (Fisher-Yates, i = n-1..1,
+ * j = random_interval(i)) on the stream (seed, "lexbfs-partition"). */
+int oracle_lexbfs_partition_seeded(const uint8_t *adj, int64_t n, int64_t stride, uint64_t seed,
+                                   int32_t *order) {
+    if (n <= 0) return ORACLE_OK;
+    int32_t *members = malloc(sizeof(int32_t) * (size_t)n);
+    if (!members) return ORACLE_ENOMEM;
+    for (int64_t k = 0; k < n; ++k) members[k] = (int32_t)k;
+    philox_t r;
+    philox_init(&r, stream_key(seed, "lexbfs-partition"));
+    for (int64_t i = n - 1; i >= 1; --i) {
+        uint32_t j = philox_interval(&r, (uint32_t)i);
+        int32_t t = members[i];
+        members[i] = members[j];
+        members[j] = t;
+    }
+    int rc = oracle_lexbfs_partition(adj, n, stride, members, order);
+    free(members);
+    return rc;
+}
+
+/* lexbfs_labels(g, seeded(seed), method="linked"), search.py:283-310: the
+ * pivot is member Generator.integers(|C|) of the max-label class C in chain
+ * order.  The chain starts as range(n) and receives movers in adjacency
+ * order, so every class lists its members by ascending id -- the order of a
+ * PartitionList started from range(n), whose first class is the chain tail. */
+int oracle_lexbfs_labels_seeded(const uint8_t *adj, int64_t n, int64_t stride, uint64_t seed, int32_t *order) {
+    if (n <= 0) return ORACLE_OK;
+    plist_t P;
+    if (plist_init(&P, n, NULL) != ORACLE_OK) { plist_free(&P); return ORACLE_ENOMEM; }
+    uint8_t *visited = calloc((size_t)n, 1);
+    if (!visited) { plist_free(&P); return ORACLE_ENOMEM; }
+    philox_t r;
+    philox_init(&r, stream_key(seed, "lexbfs-labels"));
+    int64_t rowbytes = (n + 7) >> 3;
+    for (int64_t i = 1; i <= n; ++i) {
+        int32_t c = P.chead, size = 0;
+        for (int32_t v = P.cfirst[c];; v = P.vnext[v]) {
+            ++size;
+            if (v == P.clast[c]) break;
+        }
+        uint32_t k = philox_bounded(&r, (uint32_t)(size - 1));
+        int32_t x = P.cfirst[c];
+        while (k--) x = P.vnext[x];
+        plist_detach(&P, x);  /* detach_vertex, search.py:215-227 */
+        if (P.cfirst[c] == -1) plist_unlink_class(&P, c);
+        P.class_of[x] = -1;
+        visited[x] = 1;
+        order[i - 1] = x;
+        const uint8_t *row = adj + (int64_t)x * stride;
+        for (int64_t b = 0; b < rowbytes; ++b) {
+            uint8_t byte = row[b];
+            while (byte) {
+                int kk = __builtin_ctz(byte);
+                byte &= (uint8_t)(byte - 1);
+                int64_t y = (b << 3) + kk;
+                if (y < n && !visited[y]) plist_move_to_splitter(&P, (int32_t)y, (int32_t)i);
+            }
+        }
+    }
+    free(visited);
+    plist_free(&P);
+    return ORACLE_OK;
+}
+
+/* ---------------------------------------------------------------------------
  * Array partition refinement -- lexbfs_array, _arraylex.py:22-65.  Ties are
  * broken by position in `initial` (identity => LOWEST_INDEX; a Philox
  * permutation => the seeded array path, search.py:535-541).

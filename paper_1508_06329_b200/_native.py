@@ -16,7 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libchordal_b200.so")
 
 OK, EINVAL, ETOOLARGE, ECUDA, ENOMEM, EPARSE, EUTF8 = 0, 1, 2, 3, 4, 5, 6
-TIE_ASCENDING, TIE_DESCENDING, TIE_SEEDED_ARB = 0, 1, 2
+TIE_ASCENDING, TIE_DESCENDING, TIE_SEEDED_ARB, TIE_SEEDED_PARTITION, TIE_SEEDED_LABELS = 0, 1, 2, 3, 4
 DENSE_LEXBFS_MAX_N = 32768
 BATCH_MAX_N = 1024
 

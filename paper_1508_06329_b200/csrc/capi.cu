@@ -307,7 +307,12 @@ int chordal_lexbfs_csr(const int64_t *indptr_dev, const int32_t *indices_dev, in
     if (n > 0x7FFFFFF0LL / 2) return CHORDAL_ETOOLARGE;
     if (!indptr_dev || !indices_dev || !order_dev || !pos_dev || !ws) return CHORDAL_EINVAL;
     if (ws_bytes < csr_workspace_bytes(n, m)) return CHORDAL_EINVAL;
-    if (tie_rule < 0 || tie_rule > 2) return CHORDAL_EINVAL;
+    if (tie_rule < 0 || tie_rule > 4) return CHORDAL_EINVAL;
+    // the seeded linked variants draw from the Philox stream (seed, label) (rng.py:18-21)
+    if (tie_rule == CHORDAL_TIE_SEEDED_PARTITION)
+        seed = splitmix64(splitmix64(seed) ^ (uint64_t)crc32_str("lexbfs-partition"));
+    else if (tie_rule == CHORDAL_TIE_SEEDED_LABELS)
+        seed = splitmix64(splitmix64(seed) ^ (uint64_t)crc32_str("lexbfs-labels"));
     return launch_lexbfs_csr(indptr_dev, indices_dev, n, m, tie_rule, seed, current_cell(crc32_str("current")),
                              order_dev, pos_dev, parent_dev, ws, as_stream(stream));
 }

@@ -318,6 +318,12 @@ int launch_lexbfs_csr(const int64_t *indptr, const int32_t *indices, int64_t n, 
         case CHORDAL_TIE_SEEDED_ARB:
             return launch_csr_mode<CHORDAL_TIE_SEEDED_ARB>(indptr, indices, n, m, seed, cell, order, pos, parent, ws,
                                                            stream);
+        case CHORDAL_TIE_SEEDED_PARTITION:  // seed: the Philox key of (seed, "lexbfs-partition")
+            return launch_csr_mode<CHORDAL_TIE_SEEDED_PARTITION>(indptr, indices, n, m, seed, cell, order, pos, parent,
+                                                                 ws, stream);
+        case CHORDAL_TIE_SEEDED_LABELS:  // seed: the Philox key of (seed, "lexbfs-labels")
+            return launch_csr_mode<CHORDAL_TIE_SEEDED_LABELS>(indptr, indices, n, m, seed, cell, order, pos, parent,
+                                                              ws, stream);
         default:
             return CHORDAL_EINVAL;
     }

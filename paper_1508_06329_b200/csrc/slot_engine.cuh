@@ -40,6 +40,7 @@
 // S the slot index type.
 #pragma once
 #include "common.cuh"
+#include "philox.cuh"
 
 namespace chordal {
 
@@ -288,6 +289,30 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
         M.c_next[0] = C::NIL;
     }
     __syncwarp();
+    if (MODE == CHORDAL_TIE_SEEDED_PARTITION) {
+        // lexbfs_partition(seeded, method="linked") (search.py:515-518): the one
+        // initial class holds range(n) shuffled by Generator.shuffle -- Fisher-
+        // Yates with random_interval (masked rejection on next_uint32), i = n-1..1,
+        // on the stream keyed by `seed` (= mix64(seed, crc32("lexbfs-partition"))).
+        if (lane == 0) {
+            PhiloxStream rs(seed);
+            for (int i2 = n - 1; i2 >= 1; --i2) {
+                uint32_t mask = (uint32_t)i2;
+                mask |= mask >> 1; mask |= mask >> 2; mask |= mask >> 4; mask |= mask >> 8; mask |= mask >> 16;
+                uint32_t j;
+                while ((j = rs.next32() & mask) > (uint32_t)i2) {
+                }
+                const I t = M.slot_v[i2];
+                M.slot_v[i2] = M.slot_v[j];
+                M.slot_v[j] = t;
+            }
+        }
+        __syncwarp();
+    }
+    // lexbfs_labels(seeded, method="linked") (search.py:285-290): the pivot is
+    // member Generator.integers(|C|) of the max-label class C, members in chain
+    // order (= ascending id here); every lane keeps the same stream.
+    PhiloxStream lab(seed);
     int chead = 0, nfree = n, nclasses = 1, nunv = n;
     long long top = n;
 
@@ -320,6 +345,19 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
                 if (s2 >= 0 && (bs < 0 || b2 > best || (b2 == best && v2 > bv))) { best = b2; bs = s2; bv = v2; }
             }
             xs = bs;
+        } else if (MODE == CHORDAL_TIE_SEEDED_LABELS) {
+            int rem = (int)lab.bounded(0, (uint64_t)((int)M.c_live[c0] - 1));
+            for (long long s0 = h;; s0 += 32) {
+                const long long s = s0 + lane;
+                const bool live = s < e0 && (int)M.cls[(int)M.slot_v[s]] == c0;
+                const uint32_t bm = __ballot_sync(CH_FULL, live);
+                const int c = __popc(bm);
+                if (rem < c) {
+                    xs = s0 + (long long)__fns(bm, 0, rem + 1);
+                    break;
+                }
+                rem -= c;
+            }
         } else {
             xs = slot_detail::first_live<I, S>(M, c0, h, e0);
         }
@@ -327,7 +365,8 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
         if (xs + 1 < e0) src.prefetch((int)M.slot_v[xs + 1]);  // the head class's next member
         __syncwarp();
         if (lane == 0) {
-            if (MODE != CHORDAL_TIE_SEEDED_ARB || xs == (long long)M.c_head[c0]) M.c_head[c0] = (S)(xs + 1);
+            if ((MODE != CHORDAL_TIE_SEEDED_ARB && MODE != CHORDAL_TIE_SEEDED_LABELS) || xs == (long long)M.c_head[c0])
+                M.c_head[c0] = (S)(xs + 1);
             M.cls[x] = C::VISITED;
             order[i] = (O)x;
             if (pos) pos[x] = (O)i;
@@ -395,7 +434,7 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
                 if (t < ntouch) {
                     const int c = (int)M.touched[t];
                     k = (int)M.c_cnt[c];
-                    if (k == (int)M.c_live[c]) k = 0;  // whole class moves: stays in place
+                    if (k == (int)M.c_live[c] && MODE != CHORDAL_TIE_SEEDED_PARTITION) k = 0;  // whole class moves: stays in place
                 }
                 need += __reduce_add_sync(CH_FULL, k);
             }
@@ -405,16 +444,20 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
         for (int t0 = 0; t0 < ntouch; t0 += 32) {
             const int t = t0 + lane;
             int c = 0, k = 0;
-            bool split = false;
+            bool split = false, resort = false;
             if (t < ntouch) {
                 c = (int)M.touched[t];
                 k = (int)M.c_cnt[c];
                 split = k != (int)M.c_live[c];
+                // PartitionList moves every member, so a class whose members all
+                // move is re-ordered by adjacency (search.py:440-463); with the
+                // seeded initial shuffle that order differs from the slot order
+                resort = !split && MODE == CHORDAL_TIE_SEEDED_PARTITION;
             }
             const uint32_t sm = __ballot_sync(CH_FULL, split);
             const int rank = __popc(sm & lt);
-            // segment offsets: inclusive prefix of k over the splitting lanes
-            const int kk = split ? k : 0;
+            // segment offsets: inclusive prefix of k over the splitting (and re-sorted) lanes
+            const int kk = (split || resort) ? k : 0;
             int incl = kk;
 #pragma unroll
             for (int d = 1; d < 32; d <<= 1) {
@@ -433,6 +476,12 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
                 M.c_tgt[c] = (I)d;
                 M.c_cnt[c] = (I)(start - top0);  // pass 2: next free slot of the new segment
                 pold = (int)M.c_prev[c];
+            } else if (resort) {
+                const long long start = top + incl - kk;
+                M.c_head[c] = (S)start;
+                M.c_end[c] = (S)(start + k);
+                M.c_tgt[c] = (I)c;
+                M.c_cnt[c] = (I)(start - top0);
             } else if (t < ntouch) {
                 M.c_tgt[c] = (I)c;
             }
@@ -463,7 +512,7 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
             int c = ok ? (int)M.cls[y] : (int)C::VISITED;
             ok = ok && c != (int)C::VISITED;
             const int d = ok ? (int)M.c_tgt[c] : 0;
-            ok = ok && d != c;  // whole-class moves need no slot change
+            if (MODE != CHORDAL_TIE_SEEDED_PARTITION) ok = ok && d != c;  // whole-class moves need no slot change
             const uint32_t vm = __ballot_sync(CH_FULL, ok);
             const uint32_t peers = __match_any_sync(CH_FULL, ok ? c : -1) & vm;
             if (ok) {

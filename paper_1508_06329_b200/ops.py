@@ -60,6 +60,21 @@ def _edge_count(rows: DeviceRows, m: int, stream=None) -> int:
     return count_edges(rows, stream)
 
 
+def csr_from_rows(rows: DeviceRows, stream=None):
+    """Device CSR (indptr int64[n+1], indices int32[2m], ascending rows) of device rows."""
+    torch = _native.require_cuda()
+    dev = rows.data.device
+    indptr = torch.empty(rows.n + 1, dtype=torch.int64, device=dev)
+    check(lib.chordal_dense_to_csr(rows.ptr, rows.n, rows.stride, ptr(indptr), None, stream_ptr(stream)),
+          "chordal_dense_to_csr")
+    nnz = int(indptr[rows.n].item())
+    rows.m = nnz // 2
+    indices = torch.empty(max(nnz, 1), dtype=torch.int32, device=dev)
+    check(lib.chordal_dense_to_csr(rows.ptr, rows.n, rows.stride, ptr(indptr), ptr(indices), stream_ptr(stream)),
+          "chordal_dense_to_csr")
+    return indptr, indices[:nnz]
+
+
 def count_edges(rows: DeviceRows, stream=None) -> int:
     """Edge count of device rows (one popcount pass + a 8-byte read-back)."""
     torch = _native.require_cuda()
@@ -165,6 +180,8 @@ def lexbfs_csr(indptr, indices, n: int, tie_rule: int = _native.TIE_ASCENDING, s
         if m is None:
             m = int(indices.numel()) // 2
         ws = _ws(torch, lib.chordal_lexbfs_csr_workspace_bytes(n, m), dev)
+        if indices.numel() == 0:  # edgeless: the ABI wants a real pointer
+            indices = torch.zeros(1, dtype=torch.int32, device=dev)
         check(
             lib.chordal_lexbfs_csr(ptr(indptr), ptr(indices), n, m, tie_rule, seed & U64_MAX, ptr(order), ptr(pos),
                                    ptr(parent), ptr(ws), ws.numel(), stream_ptr(stream)),

@@ -28,6 +28,20 @@ def lexbfs(g, tie_rule: int, seed: int = 0) -> VertexOrdering:
     return VertexOrdering._trusted(order.cpu().numpy(), pos.cpu().numpy())
 
 
+def lexbfs_linked_seeded(g, tie_rule: int, seed: int) -> VertexOrdering:
+    """The seeded *linked* LexBFS variants (TIE_SEEDED_PARTITION / _LABELS) run on
+    the CSR slot engine (dense inputs are converted to CSR on the device)."""
+    n = int(g.n)
+    if n == 0:
+        return VertexOrdering(())
+    if is_csr(g):
+        ip, ix = device_csr(g)
+    else:
+        ip, ix = ops.csr_from_rows(device_rows(g))
+    order, pos, _ = ops.lexbfs_csr(ip, ix, n, tie_rule, seed, m=int(ix.numel()) // 2)
+    return VertexOrdering._trusted(order.cpu().numpy(), pos.cpu().numpy())
+
+
 def peo_witness(g, o: VertexOrdering):
     """0-based witness of the PEO test of ordering ``o`` (None when a PEO)."""
     torch = _native.require_cuda()

@@ -12,8 +12,12 @@ Seeded tie-breaks are method-dependent in the reference:
 ``method="array"`` (and "auto" for n >= 1024) breaks ties by a Philox
 permutation of the vertices (search.py:535-541); that is replayed here by
 relabelling the graph on the device with the same permutation and running the
-ascending kernel.  The linked seeded variants (n < 1024 under "auto") draw
-per-step or per-split random choices and are not offered yet.
+ascending kernel.  The linked seeded variants (n < 1024 under "auto") run
+the CSR slot engine with the reference's random choices replayed from the
+same Philox streams: ``lexbfs_partition`` shuffles the initial class
+(Generator.shuffle) and keeps split-off classes in adjacency order,
+``lexbfs_labels`` draws the pivot's index in the max-label class
+(Generator.integers) at every step.
 """
 
 from __future__ import annotations
@@ -76,11 +80,13 @@ def _run_lexbfs(g, tie_break: TieBreak, label: str, method: str) -> VertexOrderi
     n = int(g.n)
     if tie_break.seed is None:
         return pipeline.lexbfs(g, _native.TIE_ASCENDING)
-    if method != "array" or is_csr(g):
-        raise NotImplementedError(
-            "seeded tie-breaks of the linked reference methods (n < 1024 under method='auto') "
-            "are not replayed on the GPU yet; pass method='array' with a dense graph"
-        )
+    if method == "linked":
+        # per-split / per-step random choices of the linked structures
+        # (search.py:285-290 labels, 515-518 partition), replayed by the slot engine
+        rule = _native.TIE_SEEDED_LABELS if label == "lexbfs-labels" else _native.TIE_SEEDED_PARTITION
+        return pipeline.lexbfs_linked_seeded(g, rule, int(tie_break.seed))
+    if is_csr(g):
+        raise NotImplementedError("the seeded array method needs the dense rows (it relabels the matrix)")
     if n == 0:
         return VertexOrdering(())
     initial = np.asarray(tie_break.generator(label).permutation(n), dtype=np.int64)

@@ -459,3 +459,43 @@ def test_device_csr_generator_matches_host():
         ref = CSRGraph.from_edges0(n, u, v)
         assert ip.cpu().numpy().tolist() == ref.indptr.tolist()
         assert ix.cpu().numpy().tolist() == ref.indices.tolist()
+
+
+# ------------------------------------------------- seeded linked variants ----
+
+
+def test_seeded_linked_goldens():
+    """lexbfs_partition / lexbfs_labels with seeded(s), method="linked" (and
+    "auto" below 1024 vertices): the reference's frozen orders, and is_chordal
+    with method="reference" (tests/golden/seeded_linked.npz)."""
+    z = load_npz("seeded_linked.npz")
+    for i in range(len(z["n"])):
+        n, s = int(z["n"][i]), int(z["seed"][i])
+        g = G(z["packed"][i, :n, : (n + 7) // 8], n)
+        assert o0(P.lexbfs_partition(g, P.seeded(s), method="linked")) == z["part"][i, :n].tolist(), i
+        assert o0(P.lexbfs_labels(g, P.seeded(s), method="linked")) == z["labels"][i, :n].tolist(), i
+        if n < 1024:
+            assert o0(P.lexbfs_partition(g, P.seeded(s))) == z["part"][i, :n].tolist(), i
+        v = P.is_chordal(g, "partition", P.seeded(s), method="reference")
+        assert bool(v.chordal) == bool(z["chordal"][i]), i
+        assert (w0(v.witness) or [-1, -1, -1]) == z["witness"][i].tolist(), i
+
+
+def test_seeded_linked_against_oracle_larger():
+    from paper_1508_06329_b200.csr import CSRGraph
+
+    cases = [gen_chordal_random(3000, 12, 5), gen_dense_random(2500, 0.01, 6), gen_dense_random(1200, 0.6, 7),
+             gen_chordal_random(40000, 6, 8, cap=40000)]
+    for k, g in enumerate(cases):
+        for s in (0, 77 + k, -3):
+            for variant, fn in (("partition", P.lexbfs_partition), ("labels", P.lexbfs_labels)):
+                want = oracle.lexbfs_linked_seeded(g._packed, g.n, s, variant).tolist()
+                assert o0(fn(g, P.seeded(s), method="linked")) == want, (k, s, variant)
+    # CSR input (the N > 32768 global-memory slot engine)
+    from paper_1508_06329_b200.generate import chordal_random_edges
+
+    g = cases[-1]
+    u, v = chordal_random_edges(40000, 6, 8)
+    c = CSRGraph.from_edges0(g.n, u, v)
+    want = oracle.lexbfs_linked_seeded(g._packed, g.n, 9, "labels").tolist()
+    assert o0(P.lexbfs_labels(c, P.seeded(9), method="linked")) == want

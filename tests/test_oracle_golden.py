@@ -152,3 +152,14 @@ def test_oracle_batch_matches_single(small_corpus):
         ok, order, w = oracle.is_chordal(g._packed, 96)
         assert verdict[b] == ok and orders[b].tolist() == order.tolist()
         assert (list(w) if w else [-1, -1, -1]) == wit[b].tolist()
+
+
+def test_oracle_seeded_linked_goldens():
+    """Seeded linked LexBFS (search.py:283-310, 515-532) with the C Philox port:
+    the orders the reference produced (tests/golden/seeded_linked.npz)."""
+    z = load_npz("seeded_linked.npz")
+    for i in range(len(z["n"])):
+        n, s = int(z["n"][i]), int(z["seed"][i])
+        rows = z["packed"][i, :n, : (n + 7) // 8]
+        assert oracle.lexbfs_linked_seeded(rows, n, s, "partition").tolist() == z["part"][i, :n].tolist(), i
+        assert oracle.lexbfs_linked_seeded(rows, n, s, "labels").tolist() == z["labels"][i, :n].tolist(), i
