@@ -236,6 +236,24 @@ int chordal_gen_chordal_random_edges(int64_t n, int64_t k, int64_t seed, int32_t
 int chordal_gen_chordal_random(uint8_t *adj_dev, int64_t batch, int64_t n, int64_t stride, int64_t k, int64_t seed0,
                                int64_t seed_step, void *scratch_dev, size_t scratch_bytes, void *stream);
 
+/* ---- other vertex orderings (search.py:79-145) ----------------------------- */
+
+/* mcs_order (search.py:113-145) on dense rows, n <= 65535: maximum cardinality
+ * search, ties to the smallest id; seeded != 0 replays TieBreak(seed): the
+ * winner is ties[Generator.integers(len(ties))] on the stream (seed, "mcs"),
+ * ties ascending.  One persistent CTA, weights in shared memory. */
+int chordal_mcs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int32_t seeded, uint64_t seed,
+                      int32_t *order_dev, int32_t *pos_dev, void *stream);
+
+/* bfs_order (search.py:79-110) on CSR rows: FIFO order with restarts at the
+ * smallest unqueued vertex; seeded != 0 replays TieBreak(seed) (restart at
+ * pool[integers(len(pool))], fresh neighbours Generator.shuffle'd) on the
+ * stream (seed, "bfs").  ws: chordal_bfs_csr_workspace_bytes(n) bytes (0
+ * unless n exceeds the shared-memory bitset). */
+size_t chordal_bfs_csr_workspace_bytes(int64_t n);
+int chordal_bfs_csr(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, int32_t seeded, uint64_t seed,
+                    int32_t *order_dev, int32_t *pos_dev, void *ws, size_t ws_bytes, void *stream);
+
 /* ---- plain-text formats (host side, textio.py) ---------------------------- */
 
 /* parse_graph_text (textio.py:30-86) straight into packed rows.  Two calls:

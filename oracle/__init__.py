@@ -48,6 +48,8 @@ def lib():
         L.oracle_lexbfs_array.argtypes = [P, i64, i64, P, P]
         L.oracle_lexbfs_partition_seeded.argtypes = [P, i64, i64, ctypes.c_uint64, P]
         L.oracle_lexbfs_labels_seeded.argtypes = [P, i64, i64, ctypes.c_uint64, P]
+        L.oracle_mcs_order.argtypes = [P, i64, i64, ctypes.c_int, ctypes.c_uint64, P]
+        L.oracle_bfs_order.argtypes = [P, i64, i64, ctypes.c_int, ctypes.c_uint64, P]
         L.oracle_lexbfs_arbitrated.argtypes = [P, i64, i64, ctypes.c_int, ctypes.c_uint64, P]
         L.oracle_is_peo.argtypes = [P, i64, i64, P, P]
         L.oracle_is_peo_csr.argtypes = [P, P, i64, P, P]
@@ -123,6 +125,17 @@ def lexbfs_linked_seeded(packed: np.ndarray, n: int, seed: int, variant: str) ->
     fn = lib().oracle_lexbfs_partition_seeded if variant == "partition" else lib().oracle_lexbfs_labels_seeded
     if fn(_ptr(rows), n, rows.shape[1] if n else 0, int(seed) & 0xFFFFFFFFFFFFFFFF, _ptr(order)):
         raise MemoryError("oracle seeded linked LexBFS")
+    return order[:n]
+
+
+def other_order(packed: np.ndarray, n: int, which: str, seed: int | None = None) -> np.ndarray:
+    """mcs_order (search.py:113-145) or bfs_order (search.py:79-110); 0-based."""
+    rows = np.ascontiguousarray(packed, dtype=np.uint8)
+    order = np.empty(max(n, 1), dtype=np.int32)
+    fn = lib().oracle_mcs_order if which == "mcs" else lib().oracle_bfs_order
+    if fn(_ptr(rows), n, rows.shape[1] if n else 0, int(seed is not None), int(seed or 0) & 0xFFFFFFFFFFFFFFFF,
+          _ptr(order)):
+        raise MemoryError("oracle " + which)
     return order[:n]
 
 

@@ -406,6 +406,77 @@ int oracle_lexbfs_labels_seeded(const uint8_t *adj, int64_t n, int64_t stride, u
     return ORACLE_OK;
 }
 
+/* mcs_order, search.py:113-145: scan for the unvisited vertex of largest
+ * weight (first = smallest id); seeded: ties[integers(len(ties))] on the
+ * stream (seed, "mcs").  O(n^2 / 8 + n^2) like the reference. */
+int oracle_mcs_order(const uint8_t *adj, int64_t n, int64_t stride, int seeded, uint64_t seed, int32_t *order) {
+    if (n <= 0) return ORACLE_OK;
+    int32_t *weight = calloc((size_t)n, sizeof(int32_t)), *ties = malloc(sizeof(int32_t) * (size_t)n);
+    uint8_t *done = calloc((size_t)n, 1);
+    if (!weight || !ties || !done) { free(weight); free(ties); free(done); return ORACLE_ENOMEM; }
+    philox_t r;
+    philox_init(&r, stream_key(seed, "mcs"));
+    for (int64_t i = 0; i < n; ++i) {
+        int32_t best = -1, x = -1, nt = 0;
+        for (int32_t v = 0; v < n; ++v) {
+            if (done[v]) continue;
+            if (weight[v] > best) { best = weight[v]; x = v; nt = 0; ties[nt++] = v; }
+            else if (weight[v] == best) ties[nt++] = v;
+        }
+        if (seeded) x = ties[philox_bounded(&r, (uint32_t)(nt - 1))];
+        done[x] = 1;
+        order[i] = x;
+        const uint8_t *row = adj + (int64_t)x * stride;
+        for (int32_t y = 0; y < n; ++y)
+            if (dbit(row, y) && !done[y]) ++weight[y];
+    }
+    free(weight); free(ties); free(done);
+    return ORACLE_OK;
+}
+
+/* bfs_order, search.py:79-110: FIFO queue, restarts at the smallest unqueued
+ * vertex; seeded: restart at pool[integers(len(pool))], fresh neighbours
+ * shuffled (Fisher-Yates, random_interval) on the stream (seed, "bfs"). */
+int oracle_bfs_order(const uint8_t *adj, int64_t n, int64_t stride, int seeded, uint64_t seed, int32_t *order) {
+    if (n <= 0) return ORACLE_OK;
+    uint8_t *queued = calloc((size_t)n, 1);
+    if (!queued) return ORACLE_ENOMEM;
+    philox_t r;
+    philox_init(&r, stream_key(seed, "bfs"));
+    int64_t head = 0, tail = 0, next_start = 0, nq = 0;
+    while (head < n) {
+        if (head == tail) {
+            int64_t s;
+            if (!seeded) {
+                while (queued[next_start]) ++next_start;
+                s = next_start;
+            } else {
+                uint32_t k = philox_bounded(&r, (uint32_t)(n - nq - 1));
+                for (s = 0;; ++s)
+                    if (!queued[s] && k-- == 0) break;
+            }
+            queued[s] = 1;
+            order[tail++] = (int32_t)s;
+            ++nq;
+        }
+        int32_t x = order[head++];
+        int64_t t0 = tail;
+        const uint8_t *row = adj + (int64_t)x * stride;
+        for (int32_t y = 0; y < n; ++y)
+            if (dbit(row, y) && !queued[y]) { queued[y] = 1; order[tail++] = y; }
+        if (seeded && tail - t0 > 1)
+            for (int64_t i = tail - t0 - 1; i >= 1; --i) {
+                uint32_t j = philox_interval(&r, (uint32_t)i);
+                int32_t tmp = order[t0 + i];
+                order[t0 + i] = order[t0 + j];
+                order[t0 + j] = tmp;
+            }
+        nq += tail - t0;
+    }
+    free(queued);
+    return ORACLE_OK;
+}
+
 /* ---------------------------------------------------------------------------
  * Array partition refinement -- lexbfs_array, _arraylex.py:22-65.  Ties are
  * broken by position in `initial` (identity => LOWEST_INDEX; a Philox

@@ -49,6 +49,9 @@ SIGNATURES = {
     "chordal_gen_chordal_random_scratch_bytes": [_I64, _I64, _I64],
     "chordal_gen_chordal_random": [_P, _I64, _I64, _I64, _I64, _I64, _I64, _P, _SZ, _P],
     "chordal_gen_chordal_random_edges": [_I64, _I64, _I64, _P, _P, _P, _P, _SZ, _P],
+    "chordal_mcs_dense": [_P, _I64, _I64, _I32, _U64, _P, _P, _P],
+    "chordal_bfs_csr_workspace_bytes": [_I64],
+    "chordal_bfs_csr": [_P, _P, _I64, _I32, _U64, _P, _P, _P, _SZ, _P],
     "chordal_parse_graph_text": [_P, _I64, _I64, _P, _P, _P, _I64, _P, _P, _I64],
     "chordal_write_graph_text": [_P, _I64, _I64, _I64, _P, _I64],
     "chordal_parse_ordering_text": [_P, _I64, _I64, _P, _P, _P, _P, _I64],
@@ -59,6 +62,7 @@ _RESTYPES = {
     "chordal_dense_workspace_bytes": _SZ,
     "chordal_lexbfs_csr_workspace_bytes": _SZ,
     "chordal_write_graph_text": _I64,
+    "chordal_bfs_csr_workspace_bytes": _SZ,
 }
 
 if not os.path.exists(LIB_PATH):

@@ -28,6 +28,10 @@ int launch_peo_dense_witness(const uint8_t *, int64_t, int64_t, const int32_t *,
                              int32_t *, cudaStream_t);
 int launch_permute_dense(const uint8_t *, int64_t, int64_t, const int32_t *, uint8_t *, cudaStream_t);
 int launch_batch(const uint8_t *, int64_t, int64_t, int64_t, int32_t *, int32_t *, cudaStream_t);
+int launch_mcs_dense(const uint8_t *, int64_t, int64_t, bool, uint64_t, int32_t *, int32_t *, cudaStream_t);
+size_t bfs_csr_workspace_bytes(int64_t);
+int launch_bfs_csr(const int64_t *, const int32_t *, int64_t, bool, uint64_t, uint32_t *, int32_t *, int32_t *,
+                   cudaStream_t);
 int launch_gen_dense_random(uint8_t *, int64_t, int64_t, int64_t, double, int64_t, int64_t, uint32_t,
                             cudaStream_t);
 int launch_edges_to_dense(const int32_t *, const int32_t *, int64_t, uint8_t *, int64_t, int64_t, cudaStream_t);
@@ -315,6 +319,29 @@ int chordal_lexbfs_csr(const int64_t *indptr_dev, const int32_t *indices_dev, in
         seed = splitmix64(splitmix64(seed) ^ (uint64_t)crc32_str("lexbfs-labels"));
     return launch_lexbfs_csr(indptr_dev, indices_dev, n, m, tie_rule, seed, current_cell(crc32_str("current")),
                              order_dev, pos_dev, parent_dev, ws, as_stream(stream));
+}
+
+int chordal_mcs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int32_t seeded, uint64_t seed,
+                      int32_t *order_dev, int32_t *pos_dev, void *stream) {
+    int rc = check_dense(adj_dev, n, stride);
+    if (rc) return rc;
+    if (n == 0) return CHORDAL_OK;
+    if (!order_dev || !pos_dev) return CHORDAL_EINVAL;
+    const uint64_t key = splitmix64(splitmix64(seed) ^ (uint64_t)crc32_str("mcs"));
+    return launch_mcs_dense(adj_dev, n, stride, seeded != 0, key, order_dev, pos_dev, as_stream(stream));
+}
+
+size_t chordal_bfs_csr_workspace_bytes(int64_t n) { return n > 0 ? bfs_csr_workspace_bytes(n) : 0; }
+
+int chordal_bfs_csr(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, int32_t seeded, uint64_t seed,
+                    int32_t *order_dev, int32_t *pos_dev, void *ws, size_t ws_bytes, void *stream) {
+    if (n < 0) return CHORDAL_EINVAL;
+    if (n == 0) return CHORDAL_OK;
+    if (!indptr_dev || !indices_dev || !order_dev || !pos_dev) return CHORDAL_EINVAL;
+    if (ws_bytes < bfs_csr_workspace_bytes(n)) return CHORDAL_EINVAL;
+    const uint64_t key = splitmix64(splitmix64(seed) ^ (uint64_t)crc32_str("bfs"));
+    return launch_bfs_csr(indptr_dev, indices_dev, n, seeded != 0, key, reinterpret_cast<uint32_t *>(ws), order_dev,
+                          pos_dev, as_stream(stream));
 }
 
 int chordal_peo_csr_key(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, const int32_t *pos_dev,

@@ -294,3 +294,33 @@ def witness_tuple(w) -> tuple[int, int, int] | None:
     """Device witness tensor -> 0-based (v, p, z) or None."""
     a = w.cpu().numpy() if hasattr(w, "cpu") else np.asarray(w)
     return None if int(a[0]) < 0 else (int(a[0]), int(a[1]), int(a[2]))
+
+
+# ------------------------------------------------------- other orderings ----
+
+
+def mcs(rows: DeviceRows, seeded: bool = False, seed: int = 0, stream=None):
+    """Maximum cardinality search on device rows -> (order, pos) int32 device tensors."""
+    torch = _native.require_cuda()
+    n, dev = rows.n, rows.data.device
+    order, pos = _i32(torch, n, dev), _i32(torch, n, dev)
+    if n:
+        check(lib.chordal_mcs_dense(rows.ptr, n, rows.stride, int(bool(seeded)), seed & U64_MAX, ptr(order),
+                                    ptr(pos), stream_ptr(stream)), "chordal_mcs_dense")
+    return order[:n], pos[:n]
+
+
+def bfs_csr(indptr, indices, n: int, seeded: bool = False, seed: int = 0, stream=None):
+    """Breadth-first order on device CSR -> (order, pos) int32 device tensors."""
+    torch = _native.require_cuda()
+    dev = indptr.device
+    order, pos = _i32(torch, n, dev), _i32(torch, n, dev)
+    if n:
+        if indices.numel() == 0:
+            indices = torch.zeros(1, dtype=torch.int32, device=dev)
+        wsb = int(lib.chordal_bfs_csr_workspace_bytes(n))
+        ws = _ws(torch, wsb, dev) if wsb else None
+        check(lib.chordal_bfs_csr(ptr(indptr), ptr(indices), n, int(bool(seeded)), seed & U64_MAX, ptr(order),
+                                  ptr(pos), ptr(ws) if ws is not None else None, wsb, stream_ptr(stream)),
+              "chordal_bfs_csr")
+    return order[:n], pos[:n]

@@ -67,3 +67,25 @@ def is_chordal(g, tie_rule: int, seed: int = 0):
         order, pos, wit = ops.is_chordal(device_rows(g), tie_rule, seed)
     w0 = ops.witness_tuple(wit)
     return VertexOrdering._trusted(order.cpu().numpy(), pos.cpu().numpy()), w0
+
+
+def mcs_order(g, seeded: bool, seed: int) -> VertexOrdering:
+    n = int(g.n)
+    if n == 0:
+        return VertexOrdering(())
+    if is_csr(g):
+        raise NotImplementedError("mcs_order runs on dense rows (n <= 65535); pass a Graph")
+    order, pos = ops.mcs(device_rows(g), seeded, seed)
+    return VertexOrdering._trusted(order.cpu().numpy(), pos.cpu().numpy())
+
+
+def bfs_order(g, seeded: bool, seed: int) -> VertexOrdering:
+    n = int(g.n)
+    if n == 0:
+        return VertexOrdering(())
+    if is_csr(g):
+        ip, ix = device_csr(g)
+    else:
+        ip, ix = ops.csr_from_rows(device_rows(g))
+    order, pos = ops.bfs_csr(ip, ix, n, seeded, seed)
+    return VertexOrdering._trusted(order.cpu().numpy(), pos.cpu().numpy())

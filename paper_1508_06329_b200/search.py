@@ -115,3 +115,14 @@ def lexbfs_partition(g, tie_break: TieBreak = LOWEST_INDEX, *, method: str = "au
     if method == "auto":
         method = "array" if g.n >= _ARRAY_MIN_N else "linked"
     return _run_lexbfs(g, tie_break, "lexbfs-partition", method)
+
+
+def bfs_order(g, tie_break: TieBreak = LOWEST_INDEX) -> VertexOrdering:
+    """A breadth-first visit order (FIFO queue, component restarts; search.py:79-110) on the GPU."""
+    return pipeline.bfs_order(g, tie_break.seed is not None, int(tie_break.seed or 0))
+
+
+def mcs_order(g, tie_break: TieBreak = LOWEST_INDEX) -> VertexOrdering:
+    """Maximum cardinality search (search.py:113-145) on the GPU: repeatedly visit an
+    unvisited vertex with the most visited neighbours."""
+    return pipeline.mcs_order(g, tie_break.seed is not None, int(tie_break.seed or 0))

@@ -7,6 +7,8 @@ For every graph i (packed rows in the npz) and its seed s_i:
   part[i]   lexbfs_partition(g, seeded(s_i), method="linked")  (search.py:500-532)
   labels[i] lexbfs_labels(g, seeded(s_i), method="linked")     (search.py:262-310)
   chordal[i], witness[i]  is_chordal(g, "partition", seeded(s_i), method="reference")
+  mcs[i], mcs_seeded[i], bfs[i], bfs_seeded[i]   mcs_order / bfs_order (search.py:79-145),
+                          LOWEST_INDEX and seeded(s_i)
 Orders are 0-based, padded with -1.
 """
 import os
@@ -16,7 +18,7 @@ import numpy as np
 from chordalkit.generate import gen_chordal_random, gen_dense_random
 from chordalkit.graph import Graph
 from chordalkit.peo import is_chordal
-from chordalkit.search import lexbfs_labels, lexbfs_partition, seeded
+from chordalkit.search import bfs_order, lexbfs_labels, lexbfs_partition, mcs_order, seeded
 
 OUT = os.path.join(os.path.dirname(os.path.abspath(__file__)), "seeded_linked.npz")
 
@@ -52,19 +54,25 @@ def main():
     labels = -np.ones((B, N), np.int32)
     chordal = np.zeros(B, np.bool_)
     witness = -np.ones((B, 3), np.int32)
+    extra = {k: -np.ones((B, N), np.int32) for k in ("mcs", "mcs_seeded", "bfs", "bfs_seeded")}
     for i, g in enumerate(graphs):
         s = rng.randint(-5, 10**12)
         ns[i], seeds[i] = g.n, s
         packed[i, : g.n, : g._packed.shape[1]] = g._packed
         part[i, : g.n] = np.asarray(lexbfs_partition(g, seeded(s), method="linked").order) - 1
         labels[i, : g.n] = np.asarray(lexbfs_labels(g, seeded(s), method="linked").order) - 1
+        if g.n <= 400:  # the reference's MCS is O(n^2) in Python
+            extra["mcs"][i, : g.n] = np.asarray(mcs_order(g).order) - 1
+            extra["mcs_seeded"][i, : g.n] = np.asarray(mcs_order(g, seeded(s)).order) - 1
+        extra["bfs"][i, : g.n] = np.asarray(bfs_order(g).order) - 1
+        extra["bfs_seeded"][i, : g.n] = np.asarray(bfs_order(g, seeded(s)).order) - 1
         v = is_chordal(g, "partition", seeded(s), method="reference")
         chordal[i] = v.chordal
         if not v.chordal:
             w = v.witness
             witness[i] = (w.v - 1, w.p - 1, w.z - 1)
     np.savez_compressed(OUT, packed=packed, n=ns, seed=seeds, part=part, labels=labels, chordal=chordal,
-                        witness=witness)
+                        witness=witness, **extra)
     print(B, "graphs ->", OUT)
 
 

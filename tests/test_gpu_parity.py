@@ -499,3 +499,45 @@ def test_seeded_linked_against_oracle_larger():
     c = CSRGraph.from_edges0(g.n, u, v)
     want = oracle.lexbfs_linked_seeded(g._packed, g.n, 9, "labels").tolist()
     assert o0(P.lexbfs_labels(c, P.seeded(9), method="linked")) == want
+
+
+# ------------------------------------------------ MCS and BFS orderings ----
+
+
+def test_mcs_bfs_goldens():
+    """mcs_order / bfs_order (search.py:79-145): the reference's frozen orders,
+    LOWEST_INDEX and seeded, plus its named cases (test_search.py:53-66)."""
+    z = load_npz("seeded_linked.npz")
+    for i in range(len(z["n"])):
+        n, s = int(z["n"][i]), int(z["seed"][i])
+        g = G(z["packed"][i, :n, : (n + 7) // 8], n)
+        if z["mcs"][i, 0] >= 0 or n == 0:
+            assert o0(P.mcs_order(g)) == z["mcs"][i, :n].tolist(), i
+            assert o0(P.mcs_order(g, P.seeded(s))) == z["mcs_seeded"][i, :n].tolist(), i
+        assert o0(P.bfs_order(g)) == z["bfs"][i, :n].tolist(), i
+        assert o0(P.bfs_order(g, P.seeded(s))) == z["bfs_seeded"][i, :n].tolist(), i
+    c4 = P.Graph.from_edge_list(4, [(1, 2), (2, 3), (3, 4), (4, 1)])
+    assert list(P.bfs_order(c4)) == [1, 2, 4, 3] and list(P.mcs_order(c4)) == [1, 2, 3, 4]
+    assert list(P.bfs_order(P.Graph.from_edge_list(4, [(1, 2), (3, 4)]))) == [1, 2, 3, 4]
+    star = P.Graph.from_edge_list(5, [(1, k) for k in range(2, 6)])
+    assert list(P.mcs_order(star)) == [1, 2, 3, 4, 5]
+
+
+def test_mcs_bfs_against_oracle_larger():
+    """Larger graphs vs the oracle; MCS + is_peo decides chordality (Tarjan-Yannakakis,
+    the reference's test_peo.py:127-129)."""
+    from paper_1508_06329_b200.csr import CSRGraph
+    from paper_1508_06329_b200.generate import chordal_random_edges
+
+    for k, g in enumerate([gen_chordal_random(3000, 10, 11), gen_dense_random(2000, 0.3, 12),
+                           gen_dense_random(5000, 0.002, 13)]):
+        for s in (None, 5 + k):
+            tb = P.LOWEST_INDEX if s is None else P.seeded(s)
+            assert o0(P.mcs_order(g, tb)) == oracle.other_order(g._packed, g.n, "mcs", s).tolist(), (k, s)
+            assert o0(P.bfs_order(g, tb)) == oracle.other_order(g._packed, g.n, "bfs", s).tolist(), (k, s)
+        ok, _ = P.is_peo(g, P.mcs_order(g))
+        assert ok == P.is_chordal(g).chordal
+    u, v = chordal_random_edges(200000, 6, 3)
+    c = CSRGraph.from_edges0(200000, u, v)
+    got = P.bfs_order(c).order0
+    assert sorted(got.tolist()) == list(range(200000)) and got[0] == 0

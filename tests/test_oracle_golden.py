@@ -163,3 +163,17 @@ def test_oracle_seeded_linked_goldens():
         rows = z["packed"][i, :n, : (n + 7) // 8]
         assert oracle.lexbfs_linked_seeded(rows, n, s, "partition").tolist() == z["part"][i, :n].tolist(), i
         assert oracle.lexbfs_linked_seeded(rows, n, s, "labels").tolist() == z["labels"][i, :n].tolist(), i
+
+
+def test_oracle_mcs_bfs_goldens():
+    """mcs_order / bfs_order (search.py:79-145), LOWEST_INDEX and seeded: the
+    reference's frozen orders (tests/golden/seeded_linked.npz; MCS for n <= 400)."""
+    z = load_npz("seeded_linked.npz")
+    for i in range(len(z["n"])):
+        n, s = int(z["n"][i]), int(z["seed"][i])
+        rows = z["packed"][i, :n, : (n + 7) // 8]
+        if z["mcs"][i, 0] >= 0 or n == 0:
+            assert oracle.other_order(rows, n, "mcs").tolist() == z["mcs"][i, :n].tolist(), i
+            assert oracle.other_order(rows, n, "mcs", s).tolist() == z["mcs_seeded"][i, :n].tolist(), i
+        assert oracle.other_order(rows, n, "bfs").tolist() == z["bfs"][i, :n].tolist(), i
+        assert oracle.other_order(rows, n, "bfs", s).tolist() == z["bfs_seeded"][i, :n].tolist(), i
