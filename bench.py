@@ -162,7 +162,8 @@ def reduce_max(x: float, world: int) -> float:
     import torch
     import torch.distributed as dist
 
-    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor([x], dtype=torch.float64, device=dev)
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -385,12 +386,19 @@ def run_ours(args, rank, world, local):
 
     from paper_1508_06329_b200 import _native, ops
 
+    # one process per GPU; BENCH_DIST_BACKEND=gloo (host collectives, ranks may
+    # share a device) exists only to exercise the multi-rank logic on a 1-GPU box
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     device = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=device)
+        backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=device)
+        else:
+            dist.init_process_group(backend)
     lo, hi = shard(args.graphs, rank, world)
     B = hi - lo
     adj = build_batch(lo, hi, device)

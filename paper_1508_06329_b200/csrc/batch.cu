@@ -1,6 +1,7 @@
 // batch.cu -- is_chordal over many small independent graphs (n <= 1024).
 //
-// One warp per graph, kBatchWarps graphs per CTA, no CTA-level synchronisation.
+// One warp per graph, four graphs per CTA (graph b + w * gridDim.x for warp w of
+// CTA b), no CTA-level synchronisation.
 // The warp runs the register-resident touched-segment LexBFS of warp_seg.cuh
 // (any density; ~4 KB of shared state per graph at n = 512, so ~40 graphs are
 // in flight per SM to hide the per-step latency) and then the PEO check.
@@ -17,7 +18,6 @@ namespace chordal {
 
 namespace {
 
-constexpr int kBatchWarps = 4;
 
 struct BatchLayout {  // shared memory per graph (one warp); the adjacency stays in global memory
     size_t A, An, P, par, F, NB, total;
@@ -37,13 +37,15 @@ struct BatchLayout {  // shared memory per graph (one warp); the adjacency stays
 
 }  // namespace
 
-__global__ void __launch_bounds__(32 * kBatchWarps)
+template <int WPC, int MINB>
+__global__ void __launch_bounds__(32 * WPC, MINB)
 batch_chordal_kernel(const uint8_t *__restrict__ adj_all, long long batch, int n, int stride,
                      int32_t *__restrict__ orders, int32_t *__restrict__ witness) {
     extern __shared__ __align__(16) uint8_t smem[];
     const BatchLayout L(n);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const long long g = (long long)blockIdx.x * kBatchWarps + warp;
+    // warp w of CTA b takes graph b + w * gridDim.x
+    const long long g = (long long)blockIdx.x + (long long)warp * gridDim.x;
     if (g >= batch) return;  // whole warp; the CTA never synchronises
     const int W = (n + 31) >> 5;
     const int sw = stride >> 2;  // row pitch in 32-bit words
@@ -161,20 +163,29 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, long long batch, int n
     }
 }
 
+template <int WPC, int MINB>
+static int launch_batch_cfg(const uint8_t *adj, int64_t batch, int64_t n, int64_t stride, int32_t *orders,
+                            int32_t *witness, cudaStream_t stream) {
+    const BatchLayout L((int)n);
+    const size_t smem = L.total * WPC;
+    cudaError_t e = cudaFuncSetAttribute(batch_chordal_kernel<WPC, MINB>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)smem);
+    if (e != cudaSuccess) return CHORDAL_ECUDA;
+    const long long blocks = (batch + WPC - 1) / WPC;
+    batch_chordal_kernel<WPC, MINB><<<(unsigned)blocks, 32 * WPC, smem, stream>>>(adj, batch, (int)n, (int)stride,
+                                                                                  orders, witness);
+    CH_LAUNCH_CHECK();
+    return CHORDAL_OK;
+}
+
 int launch_batch(const uint8_t *adj, int64_t batch, int64_t n, int64_t stride, int32_t *orders,
                  int32_t *witness, cudaStream_t stream) {
     if (batch <= 0) return CHORDAL_OK;
     if (n > 1024) return CHORDAL_ETOOLARGE;
-    const BatchLayout L((int)n);
-    const size_t smem = L.total * kBatchWarps;
-    cudaError_t e = cudaFuncSetAttribute(batch_chordal_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
-    if (e != cudaSuccess) return CHORDAL_ECUDA;
-    const long long blocks = (batch + kBatchWarps - 1) / kBatchWarps;
-    batch_chordal_kernel<<<(unsigned)blocks, 32 * kBatchWarps, smem, stream>>>(adj, batch, (int)n, (int)stride,
-                                                                               orders, witness);
-    CH_LAUNCH_CHECK();
-    return CHORDAL_OK;
+    // Four warps per CTA, warp w of CTA b on graph b + w * gridDim.x: the
+    // measured best of {1, 2, 4} warps per CTA x register caps (higher
+    // occupancy only spills; tools/batch_split.py, round 1).
+    return launch_batch_cfg<4, 1>(adj, batch, n, stride, orders, witness, stream);
 }
 
 }  // namespace chordal
