@@ -240,13 +240,16 @@ def single_graph_lines(with_cpu: bool) -> dict:
         if rows.m < 0:  # Graph.m, as the public API passes it (picks the engine's thread count)
             ops.count_edges(rows)
         lex = time_events(lambda: ops.lexbfs(rows))
-        order, pos = ops.lexbfs(rows)
-        peo = time_events(lambda: ops.peo(rows, order, pos))
+        order, pos, parent = ops.lexbfs(rows, want_parent=True)
+        # PEO check as the pipeline runs it (parents handed over by LexBFS), and
+        # standalone is_peo on the same order (parents searched by the kernel)
+        peo = time_events(lambda: ops.peo(rows, order, pos, parent))
+        peo_search = time_events(lambda: ops.peo(rows, order, pos))
         full = time_events(lambda: ops.is_chordal(rows))
         _, _, wit = ops.is_chordal(rows)
         w = ops.witness_tuple(wit)
         rec = {"n": n, "ms_per_graph": full, "lexbfs_ms": lex, "lexbfs_ns_per_step": lex * 1e6 / n,
-               "peo_ms": peo, "chordal": w is None,
+               "peo_ms": peo, "peo_parent_search_ms": peo_search, "chordal": w is None,
                "witness": None if w is None else [w[0] + 1, w[1] + 1, w[2] + 1]}
         peo_bytes = 2 * n * rows.stride + 12 * n
         rec["peo_roofline"] = {"bound": "hbm", "achieved_gbs": peo_bytes / (peo * 1e-3) / 1e9,

@@ -29,6 +29,7 @@ namespace chordal {
 namespace {
 
 constexpr int kBackRounds = 4;  // 128 candidate positions before the full pass
+constexpr int kRowU4 = 8;       // uint4 per lane per row chunk: 32 x 8 x 16 B = 4 KB (n = 32768) per round
 
 __device__ __forceinline__ bool row_bit(const uint32_t *row, int v) {
     return (__ldg(row + (v >> 5)) >> (v & 31)) & 1u;
@@ -90,28 +91,58 @@ peo_dense_key_kernel(const uint8_t *__restrict__ adj, int n, long long stride,
         const unsigned long long k64 = ((unsigned long long)parent << 32) | (unsigned)v;
         if (k64 >= *(volatile unsigned long long *)key) continue;
         // ---- stray test: A[v] & ~A[p] & ~{p}, confirmed by pos < pos(p) ---
+        // Rows go in chunks of 32 x kRowU4 uint4 per warp with every load of a
+        // chunk issued before any is used (one memory round trip per 4 KB of
+        // row per warp); p is excluded by setting its bit in the copy of A[p];
+        // candidate positions are looked up eight at a time.
         const int pp = __ldg(pos + parent);
         const uint4 *rv4 = reinterpret_cast<const uint4 *>(rowv);
         const uint4 *rp4 = reinterpret_cast<const uint4 *>(adj + (long long)parent * stride);
         bool viol = false;
-        for (int k0 = 0; k0 < n4; k0 += 32) {
-            int k = k0 + lane;
-            if (k < n4) {
-                uint4 a = __ldg(rv4 + k), b = __ldg(rp4 + k);
-                uint32_t ws[4] = {a.x & ~b.x, a.y & ~b.y, a.z & ~b.z, a.w & ~b.w};
+        for (int k0 = 0; k0 < n4 && !viol; k0 += 32 * kRowU4) {
+            uint4 a[kRowU4], b[kRowU4];
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    uint32_t w = ws[j];
-                    int base = 128 * k + 32 * j;
-                    if (parent >= base && parent < base + 32) w &= ~(1u << (parent - base));
-                    while (w && !viol) {
-                        int b2 = __ffs(w) - 1;
-                        w &= w - 1;
-                        if (__ldg(pos + base + b2) < pp) viol = true;
+            for (int j = 0; j < kRowU4; ++j) {
+                const int k = k0 + 32 * j + lane;
+                a[j] = make_uint4(0, 0, 0, 0);
+                b[j] = make_uint4(0, 0, 0, 0);
+                if (k < n4) {
+                    a[j] = __ldg(rv4 + k);
+                    b[j] = __ldg(rp4 + k);
+                }
+            }
+#pragma unroll
+            for (int j = 0; j < kRowU4; ++j) {
+                const int k = k0 + 32 * j + lane;
+                if ((parent >> 7) == k) {  // exclude p itself
+                    const uint32_t pb = 1u << (parent & 31);
+                    switch ((parent >> 5) & 3) {
+                        case 0: b[j].x |= pb; break;
+                        case 1: b[j].y |= pb; break;
+                        case 2: b[j].z |= pb; break;
+                        default: b[j].w |= pb; break;
+                    }
+                }
+                const uint32_t ws[4] = {a[j].x & ~b[j].x, a[j].y & ~b[j].y, a[j].z & ~b[j].z, a[j].w & ~b[j].w};
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    uint32_t w = ws[q];
+                    const int base = 128 * k + 32 * q;
+                    while (w && !viol) {  // up to eight position lookups in flight
+                        int z[8], pz[8];
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            z[u] = w ? base + __ffs(w) - 1 : -1;
+                            w &= w - 1;
+                        }
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) pz[u] = z[u] >= 0 ? __ldg(pos + z[u]) : 0x7FFFFFFF;
+#pragma unroll
+                        for (int u = 0; u < 8; ++u) viol |= pz[u] < pp;
                     }
                 }
             }
-            if (__any_sync(CH_FULL, viol)) { viol = true; break; }
+            viol = __any_sync(CH_FULL, viol);
         }
         if (viol && lane == 0) atomicMin(key, k64);
     }
