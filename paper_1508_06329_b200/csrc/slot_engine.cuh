@@ -65,22 +65,9 @@ struct SlotConst {
 };
 
 // ---------------------------------------------------------------------------
-// Neighbour sources.  bounds(x) gives the ascending list as entries [b, e);
+// Neighbour source: bounds(x) gives the ascending list as entries [b, e);
 // the engine walks it in blocks of at most capacity() entries, calling the
 // warp-collective stage(lo, hi) before reading entries of [lo, hi) with get().
-
-struct CsrSource {  // CSR rows read in place from global memory
-    const int64_t *indptr;
-    const int32_t *indices;
-    __device__ __forceinline__ void bounds(int x, int64_t &b, int64_t &e) const {
-        b = __ldg(indptr + x);
-        e = __ldg(indptr + x + 1);
-    }
-    __device__ __forceinline__ int capacity() const { return 0x7FFFFFFF; }
-    __device__ __forceinline__ void stage(int64_t, int64_t) const {}
-    __device__ __forceinline__ int get(int64_t e) const { return __ldg(indices + e); }
-    __device__ __forceinline__ void prefetch(int) const {}
-};
 
 // CSR rows staged through a shared-memory buffer: each block of the pivot's
 // list is fetched with one burst of independent loads (one memory round trip
@@ -114,45 +101,37 @@ struct CsrStagedSource {
         __syncwarp();
     }
     __device__ __forceinline__ int get(int64_t e) const { return (int)buf[e - base]; }
-    __device__ __forceinline__ void prefetch(int) const {}
+    // Row bounds of a likely next pivot, issued where they stand (their values
+    // are used a step later), and an L2 prefetch of the row itself once they
+    // have arrived: the next step's row fetch then skips the indptr round trip
+    // and finds the list in L2.
+    __device__ __forceinline__ void bounds_issue(int v, int64_t &b, int64_t &e) const {
+        asm volatile("ld.global.nc.s64 %0, [%1];" : "=l"(b) : "l"(indptr + v));
+        asm volatile("ld.global.nc.s64 %0, [%1];" : "=l"(e) : "l"(indptr + v + 1));
+    }
+    __device__ __forceinline__ void prefetch_row(int64_t b, int64_t e) const {
+        const int lane = threadIdx.x & 31;
+        const int64_t k = b + 32 * (int64_t)lane;
+        if (k < e) asm volatile("prefetch.global.L2 [%0];" ::"l"(indices + k));
+    }
 };
 
-// Packed bitset row of n <= 1024 bits (generic pointer: smem or global); the
-// neighbour ids are compacted into nbuf by bounds().
-template <typename I>
-struct BitsetSource {
-    const uint32_t *rows;
-    int sw;      // row pitch in 32-bit words
-    int words;   // ceil(n/32) <= 32
-    I *nbuf;     // [n]
-    __device__ __forceinline__ void bounds(int x, int64_t &b, int64_t &e) const {
-        const int lane = threadIdx.x & 31;
-        uint32_t w = lane < words ? rows[x * sw + lane] : 0u;
-        int c = __popc(w), incl = c;
-#pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            int o = __shfl_up_sync(CH_FULL, incl, d);
-            if (lane >= d) incl += o;
-        }
-        int at = incl - c;
-        while (w) {
-            int bit = __ffs(w) - 1;
-            w &= w - 1;
-            nbuf[at++] = (I)(32 * lane + bit);
-        }
-        b = 0;
-        e = __shfl_sync(CH_FULL, incl, 31);
-        __syncwarp();
-    }
-    __device__ __forceinline__ int capacity() const { return 0x7FFFFFFF; }
-    __device__ __forceinline__ void stage(int64_t, int64_t) const {}
-    __device__ __forceinline__ int get(int64_t e) const { return (int)nbuf[e]; }
-    // speculative L1 prefetch of a likely next pivot's row
-    __device__ __forceinline__ void prefetch(int v) const {
-        const int lane = threadIdx.x & 31;
-        if (lane < words) asm volatile("prefetch.global.L1 [%0];" ::"l"(rows + v * sw + lane));
-    }
-};
+#ifdef SLOT_PROFILE
+// lane-0 cycle counters (tools/slot_profile.cu only): [0] steps [1] pivot
+// [2] bounds + pass 1 [3] allocate [4] pass 2 + restore [5] touched classes
+// [6] steps with the pivot known ahead [7] steps with its row bounds fetched ahead
+__device__ unsigned long long slot_prof[8];
+#define SLOT_T(k)                                           \
+    do {                                                    \
+        const long long _c = clock64();                     \
+        slot_acc[k] += (unsigned long long)(_c - slot_t0);  \
+        slot_t0 = _c;                                       \
+    } while (0)
+#else
+#define SLOT_T(k) \
+    do {          \
+    } while (0)
+#endif
 
 namespace slot_detail {
 
@@ -168,24 +147,25 @@ template <int MODE, typename Src, typename Fn>
 __device__ __forceinline__ void for_each_chunk(const Src &src, int64_t b, int64_t e, Fn &&fn) {
     const int lane = threadIdx.x & 31;
     const int64_t cap = src.capacity();
+    int chunk = 0;
     if (MODE == CHORDAL_TIE_DESCENDING) {
         for (int64_t hi = e; hi > b; hi -= cap) {
             const int64_t lo = hi - cap > b ? hi - cap : b;
             src.stage(lo, hi);
-            for (int64_t c0 = hi; c0 > lo; c0 -= 32) {
+            for (int64_t c0 = hi; c0 > lo; c0 -= 32, ++chunk) {
                 const int64_t k = c0 - 1 - lane;
                 const bool ok = k >= lo;
-                fn(ok, ok ? src.get(k) : 0);
+                fn(ok, ok ? src.get(k) : 0, chunk);
             }
         }
     } else {
         for (int64_t lo = b; lo < e; lo += cap) {
             const int64_t hi = lo + cap < e ? lo + cap : e;
             src.stage(lo, hi);
-            for (int64_t c0 = lo; c0 < hi; c0 += 32) {
+            for (int64_t c0 = lo; c0 < hi; c0 += 32, ++chunk) {
                 const int64_t k = c0 + lane;
                 const bool ok = k < hi;
-                fn(ok, ok ? src.get(k) : 0);
+                fn(ok, ok ? src.get(k) : 0, chunk);
             }
         }
     }
@@ -197,30 +177,27 @@ __device__ __forceinline__ void for_each_chunk(const Src &src, int64_t b, int64_
 // and 16-byte aligned, so the over-read past e stays inside the allocation.
 constexpr int kSlotPad = 256;  // >= 32 * V for V = 8 (u16) and 4 (int32)
 template <typename I, typename S>
-__device__ __forceinline__ long long first_live(const SlotMem<I, S> &M, int c, long long h, long long e) {
+__device__ __forceinline__ long long first_live(const SlotMem<I, S> &M, int c, long long h, long long e,
+                                               int *vert = nullptr) {
     constexpr int V = 16 / sizeof(I);
     const int lane = threadIdx.x & 31;
-    if (__isShared(M.slot_v)) {  // shared-memory slots: one slot per lane is cheaper
-        for (;; h += 32) {
-            const long long s = h + lane;
-            const bool live = s < e && (int)M.cls[(int)M.slot_v[s]] == c;
-            const uint32_t m = __ballot_sync(CH_FULL, live);
-            if (m) return h + __ffs(m) - 1;
-        }
-    }
     for (long long base = h & ~(long long)(V - 1);; base += 32 * V) {
         const long long s0 = base + (long long)lane * V;
         const uint4 raw = *reinterpret_cast<const uint4 *>(M.slot_v + s0);
         const I *vals = reinterpret_cast<const I *>(&raw);
-        int first = V;
+        int first = V, v1 = -1;
 #pragma unroll
         for (int j = V - 1; j >= 0; --j) {
             const long long s = s0 + j;
-            if (s >= h && s < e && (int)M.cls[(int)vals[j]] == c) first = j;
+            if (s >= h && s < e && (int)M.cls[(int)vals[j]] == c) {
+                first = j;
+                v1 = (int)vals[j];
+            }
         }
         const uint32_t m = __ballot_sync(CH_FULL, first < V);
         if (m) {
             const int src = __ffs(m) - 1;
+            if (vert) *vert = __shfl_sync(CH_FULL, v1, src);
             return base + (long long)src * V + __shfl_sync(CH_FULL, first, src);
         }
     }
@@ -315,14 +292,44 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
     PhiloxStream lab(seed);
     int chead = 0, nfree = n, nclasses = 1, nunv = n;
     long long top = n;
+    int gv = -1;  // vertex whose row bounds (gb0, gb1) were fetched ahead
+    int64_t gb0 = 0, gb1 = 0;
+    // Next-pivot tracking (ascending / descending / seeded-partition ties): the
+    // next pivot is the first live member of the head class after the step,
+    // i.e. the head class's next live slot after x -- unless the step gives the
+    // head class a new segment, when it is the head class's first mover in tie
+    // order.  Both are known by the end of the step, so the next step skips the
+    // first-live scan; -1 = unknown (fall back to the scan).
+    constexpr bool kTrack = MODE == CHORDAL_TIE_ASCENDING || MODE == CHORDAL_TIE_DESCENDING ||
+                            MODE == CHORDAL_TIE_SEEDED_PARTITION;
+    constexpr int V = 16 / sizeof(I);
+    int nx = -1;
+    long long nxs = -1;
 
+#ifdef SLOT_PROFILE
+    unsigned long long slot_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long slot_t0 = clock64();
+#endif
     for (int i = 0; i < n; ++i) {
+#ifdef SLOT_PROFILE
+        slot_acc[0]++;
+        slot_t0 = clock64();
+#endif
         // ---- pivot: first live slot of the head class (or hash election) ----
         const int c0 = chead;
-        long long h = (long long)M.c_head[c0];
         const long long e0 = (long long)M.c_end[c0];
+        const int live_c0 = (int)M.c_live[c0], next_c0 = (int)M.c_next[c0];  // one round trip
         long long xs = -1;
-        if (MODE == CHORDAL_TIE_SEEDED_ARB && i > 0) {
+        int x = -1;
+#ifdef SLOT_PROFILE
+        if (kTrack && nx >= 0) slot_acc[6]++;
+        if (kTrack && nx >= 0 && nx == gv) slot_acc[7]++;
+#endif
+        if (kTrack && nx >= 0) {
+            xs = nxs;
+            x = nx;
+        } else if (MODE == CHORDAL_TIE_SEEDED_ARB && i > 0) {
+            const long long h = (long long)M.c_head[c0];
             const uint64_t prefix = mix64_3(seed, (uint64_t)(4 * (i - 1) + 3), cell);
             uint64_t best = 0;
             long long bs = -1;
@@ -346,6 +353,7 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
             }
             xs = bs;
         } else if (MODE == CHORDAL_TIE_SEEDED_LABELS) {
+            const long long h = (long long)M.c_head[c0];
             int rem = (int)lab.bounded(0, (uint64_t)((int)M.c_live[c0] - 1));
             for (long long s0 = h;; s0 += 32) {
                 const long long s = s0 + lane;
@@ -359,10 +367,14 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
                 rem -= c;
             }
         } else {
-            xs = slot_detail::first_live<I, S>(M, c0, h, e0);
+            xs = slot_detail::first_live<I, S>(M, c0, (long long)M.c_head[c0], e0, &x);
         }
-        const int x = (int)M.slot_v[xs];
-        if (xs + 1 < e0) src.prefetch((int)M.slot_v[xs + 1]);  // the head class's next member
+        if (x < 0) x = (int)M.slot_v[xs];
+        // the slots after x in its class: candidates for the next pivot (their
+        // classes are fetched before pass 1 and tested after it)
+        const long long cand_base = (xs + 1) & ~(long long)(V - 1);
+        uint4 cand_raw = make_uint4(0, 0, 0, 0);
+        if (kTrack) cand_raw = *reinterpret_cast<const uint4 *>(M.slot_v + cand_base + (long long)lane * V);
         __syncwarp();
         if (lane == 0) {
             if ((MODE != CHORDAL_TIE_SEEDED_ARB && MODE != CHORDAL_TIE_SEEDED_LABELS) || xs == (long long)M.c_head[c0])
@@ -372,9 +384,9 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
             if (pos) pos[x] = (O)i;
         }
         --nunv;
-        const int live0 = (int)M.c_live[c0] - 1;
+        const int live0 = live_c0 - 1;
         if (live0 == 0) {  // unlink the emptied head class
-            chead = (int)M.c_next[c0];
+            chead = next_c0;
             if (lane == 0) {
                 if (chead != (int)C::NIL) M.c_prev[chead] = C::NIL;
                 M.freel[nfree] = (I)c0;
@@ -405,13 +417,33 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
             __syncwarp();
             break;
         }
+        SLOT_T(1);
         // ---- pass 1: count movers per class ----------------------------------
         int64_t nb0, nb1;
-        src.bounds(x, nb0, nb1);
+        if (x == gv) {  // bounds fetched a step ago
+            nb0 = gb0;
+            nb1 = gb1;
+        } else {
+            src.bounds(x, nb0, nb1);
+        }
+        const int hc = chead;  // head class before this step's splits
+        int ccl[V];
+        if (kTrack) {
+            const I *cv = reinterpret_cast<const I *>(&cand_raw);
+#pragma unroll
+            for (int j = 0; j < V; ++j) {  // only slots inside x's segment hold valid ids
+                const long long sj = cand_base + (long long)lane * V + j;
+                ccl[j] = (sj > xs && sj < e0) ? (int)M.cls[(int)cv[j]] : -1;
+            }
+        }
         int ntouch = 0;
-        slot_detail::for_each_chunk<MODE>(src, nb0, nb1, [&](bool ok, int y) {
+        int hm = MODE == CHORDAL_TIE_DESCENDING ? -1 : 0x7FFFFFFF;  // first mover of hc in tie order
+        int cls_c0 = (int)C::VISITED;  // the first chunk's classes, reused by pass 2
+        slot_detail::for_each_chunk<MODE>(src, nb0, nb1, [&](bool ok, int y, int chunk) {
             int c = ok ? (int)M.cls[y] : (int)C::VISITED;
+            if (chunk == 0) cls_c0 = c;
             ok = ok && c != (int)C::VISITED;
+            if (kTrack && ok && c == hc) hm = MODE == CHORDAL_TIE_DESCENDING ? max(hm, y) : min(hm, y);
             if (ok && parent) parent[y] = (O)x;
             const uint32_t vm = __ballot_sync(CH_FULL, ok);
             const uint32_t peers = __match_any_sync(CH_FULL, ok ? c : -1) & vm;
@@ -424,7 +456,42 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
             if (leader) M.c_cnt[c] = (I)(old + __popc(peers));
             __syncwarp();
         });
-        if (ntouch == 0) continue;
+        // next pivot if the head class keeps its segment: its next live slot in the window
+        int guess = -1;
+        long long gslot = -1;
+        if (kTrack) {
+            const I *cv = reinterpret_cast<const I *>(&cand_raw);
+            int fj = V, fv = -1;
+#pragma unroll
+            for (int j = V - 1; j >= 0; --j) {
+                const long long sj = cand_base + (long long)lane * V + j;
+                if (hc == c0 && sj > xs && sj < e0 && ccl[j] == c0) {
+                    fj = j;
+                    fv = (int)cv[j];
+                }
+            }
+            const uint32_t gm = __ballot_sync(CH_FULL, fj < V);
+            if (gm) {
+                const int src_l = __ffs(gm) - 1;
+                guess = __shfl_sync(CH_FULL, fv, src_l);
+                gslot = cand_base + (long long)src_l * V + __shfl_sync(CH_FULL, fj, src_l);
+            }
+            hm = MODE == CHORDAL_TIE_DESCENDING ? __reduce_max_sync(CH_FULL, hm)
+                                                : (int)__reduce_min_sync(CH_FULL, (unsigned)hm);
+        }
+        SLOT_T(2);
+#ifdef SLOT_PROFILE
+        slot_acc[5] += ntouch;
+#endif
+        if (ntouch == 0) {
+            nx = guess;
+            nxs = gslot;
+            if (nx >= 0 && nx != gv) {
+                src.bounds_issue(nx, gb0, gb1);
+                gv = nx;
+            }
+            continue;
+        }
         // ---- allocate new classes (lanes over touched classes) -----------------
         if (top + (nb1 - nb0) > M.cap) {  // the movers need at most deg(x) slots
             int need = 0;
@@ -438,9 +505,14 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
                 }
                 need += __reduce_add_sync(CH_FULL, k);
             }
-            if (top + need > M.cap) top = slot_detail::compact<I, S>(M, chead, lane);
+            if (top + need > M.cap) {
+                top = slot_detail::compact<I, S>(M, chead, lane);
+                gslot = -1;  // slots moved: the guess's slot is stale
+                guess = -1;
+            }
         }
         const long long top0 = top;  // pass 2 slots are top0 + c_cnt[c] + rank
+        long long hstart = -1;        // first slot of the segment hc's movers go to, if any
         for (int t0 = 0; t0 < ntouch; t0 += 32) {
             const int t = t0 + lane;
             int c = 0, k = 0;
@@ -485,6 +557,10 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
             } else if (t < ntouch) {
                 M.c_tgt[c] = (I)c;
             }
+            if (kTrack) {  // did hc get a new segment?
+                const uint32_t hb = __ballot_sync(CH_FULL, (split || resort) && c == hc);
+                if (hb) hstart = __shfl_sync(CH_FULL, top + incl - kk, __ffs(hb) - 1);
+            }
             const int nsplit = __popc(sm);
             top += __shfl_sync(CH_FULL, incl, 31);
             nfree -= nsplit;
@@ -507,9 +583,18 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
             if (sm && M.c_prev[chead] != C::NIL) chead = (int)M.c_prev[chead];
         }
         __syncwarp();
+        if (kTrack) {
+            nx = hstart >= 0 ? hm : guess;
+            nxs = hstart >= 0 ? hstart : gslot;
+            if (nx >= 0 && nx != gv) {  // its row bounds arrive during pass 2
+                src.bounds_issue(nx, gb0, gb1);
+                gv = nx;
+            }
+        }
+        SLOT_T(3);
         // ---- pass 2: place the movers in ascending (tie) order -----------------
-        slot_detail::for_each_chunk<MODE>(src, nb0, nb1, [&](bool ok, int y) {
-            int c = ok ? (int)M.cls[y] : (int)C::VISITED;
+        slot_detail::for_each_chunk<MODE>(src, nb0, nb1, [&](bool ok, int y, int chunk) {
+            int c = chunk == 0 ? cls_c0 : (ok ? (int)M.cls[y] : (int)C::VISITED);
             ok = ok && c != (int)C::VISITED;
             const int d = ok ? (int)M.c_tgt[c] : 0;
             if (MODE != CHORDAL_TIE_SEEDED_PARTITION) ok = ok && d != c;  // whole-class moves need no slot change
@@ -525,8 +610,14 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
         });
         // ---- restore c_cnt = 0 on the classes touched in this step -------------
         for (int t = lane; t < ntouch; t += 32) M.c_cnt[(int)M.touched[t]] = (I)0;
+        if (kTrack && nx >= 0) src.prefetch_row(gb0, gb1);  // the next pivot's row into L2
         __syncwarp();
+        SLOT_T(4);
     }
+#ifdef SLOT_PROFILE
+    if (lane == 0)
+        for (int k = 0; k < 8; ++k) atomicAdd(&slot_prof[k], slot_acc[k]);
+#endif
 }
 
 }  // namespace chordal

@@ -1,6 +1,6 @@
 """Small driver for ncu captures: runs each hot kernel a few times on config inputs.
 
-    python tools/profile_driver.py {batch|batch_chordal|batch_dense|lexbfs32k|peo32k|lexbfs1k|all}
+    python tools/profile_driver.py {batch|batch_chordal|batch_dense|lexbfs32k|peo32k|lexbfs1k|csr1m|all}
 """
 import os
 import sys
@@ -36,6 +36,11 @@ def main(what):
         for _ in range(2):
             order, pos = ops.lexbfs(r)
             ops.peo(r, order, pos)
+    if what == "csr1m":
+        from paper_1508_06329_b200.generate import gen_chordal_random_csr_device
+
+        ip, ix = gen_chordal_random_csr_device(1_000_000, 8, 0)
+        ops.lexbfs_csr(ip, ix, 1_000_000)
     if what in ("lexbfs1k", "all"):
         r = rows_chordal(1000, 8, 0)
         for _ in range(3):
