@@ -14,14 +14,15 @@ HEADER = os.path.join(ROOT, "include", "chordal_b200.h")
 
 def declared_functions():
     text = open(HEADER).read()
-    return sorted(set(re.findall(r"^(?:int|const char \*)\s*(chordal_\w+)\s*\(", text, flags=re.M)))
+    return sorted(set(re.findall(r"^(?:int|int64_t|size_t|const char \*)\s*(chordal_\w+)\s*\(", text, flags=re.M)))
 
 
 def test_header_declares_the_boundary():
     names = declared_functions()
     for must in ("chordal_lexbfs_dense", "chordal_peo_dense", "chordal_is_chordal_dense",
                  "chordal_is_chordal_dense_host", "chordal_is_chordal_batch", "chordal_peo_dense_key",
-                 "chordal_peo_dense_witness"):
+                 "chordal_peo_dense_witness", "chordal_parse_graph_text", "chordal_write_graph_text",
+                 "chordal_mcs_dense", "chordal_bfs_csr", "chordal_lexbfs_csr"):
         assert must in names
 
 
