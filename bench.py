@@ -335,6 +335,99 @@ def single_graph_lines(with_cpu: bool) -> dict:
     return out
 
 
+def row_sharded_lines(rank: int, world: int, reps: int = 5) -> dict:
+    """Configurations 5 (CSR N = 10^6) and 3 (dense N = 32768, chord-removed) with the
+    PEO check row-sharded over all ranks: LexBFS on rank 0 (replicas
+    only -- its per-step chain stays on one GPU), order + parents broadcast, each
+    rank tests its contiguous rows, one 8-byte MIN all-reduce of the witness key,
+    z resolved locally.  Timed on the device from the broadcast to the witness, max
+    over ranks; the per-rank PEO kernel time is reported beside it."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_1508_06329_b200 import distributed as D
+    from paper_1508_06329_b200 import ops
+    from paper_1508_06329_b200.device import DeviceRows
+    from paper_1508_06329_b200.generate import chordal_random_edges, gen_chordal_random_csr_device
+    from paper_1508_06329_b200.graph import device_stride
+
+    nccl = world > 1 and dist.get_backend() == "nccl"
+    dev = torch.device("cuda", torch.cuda.current_device())
+    out = {}
+
+    def bcast(t):
+        if world > 1:
+            if nccl:
+                dist.broadcast(t, src=0)
+            else:
+                h = t.cpu()
+                dist.broadcast(h, src=0)
+                t.copy_(h)
+
+    def allmin(k):
+        if world > 1:
+            if nccl:
+                dist.all_reduce(k, op=dist.ReduceOp.MIN)
+            else:
+                h = k.cpu()
+                dist.all_reduce(h, op=dist.ReduceOp.MIN)
+                k.copy_(h)
+
+    def run(name, n, lexbfs, peo_key, witness):
+        if rank == 0:
+            order, _, parent = lexbfs()
+        else:
+            order = torch.empty(n, dtype=torch.int32, device=dev)
+            parent = torch.empty(n, dtype=torch.int32, device=dev)
+        lo, hi = D.shard_bounds(n, rank, world)
+        times, kern = [], []
+        w0 = None
+        for r in range(reps + 1):
+            barrier(world)
+            torch.cuda.synchronize()
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ka, kb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            bcast(order)
+            bcast(parent)
+            pos = ops.positions(order)
+            key = torch.empty(1, dtype=torch.int64, device=dev)
+            ops.key_init(key)
+            ka.record()
+            peo_key(order, pos, parent, lo, hi, key)
+            kb.record()
+            k = D._to_reducible(key, torch)
+            allmin(k)
+            w0 = witness(pos, D._from_reducible(k, torch))
+            b.record()
+            torch.cuda.synchronize()
+            if r:  # the first pass warms up
+                times.append(a.elapsed_time(b))
+                kern.append(ka.elapsed_time(kb))
+        out[name] = {"n": n, "ranks": world, "rows_per_rank": hi - lo,
+                     "peo_step_ms": reduce_max(sum(times) / len(times), world),
+                     "peo_kernel_ms_max_rank": reduce_max(sum(kern) / len(kern), world),
+                     "chordal": w0 is None, "witness": None if w0 is None else [w0[0] + 1, w0[1] + 1, w0[2] + 1],
+                     "timed": "broadcast(order, parent) + positions + row-shard PEO key + MIN all-reduce + z"}
+
+    # configuration 5: CSR, chordal
+    n5 = 1_000_000
+    ip5, ix5 = gen_chordal_random_csr_device(n5, 8, 0)
+    run("c5_csr_chordal_k8_n1e6", n5, lambda: ops.lexbfs_csr(ip5, ix5, n5),
+        lambda o, p, par, lo, hi, key: ops.peo_csr_key(ip5, ix5, n5, p, lo, hi, key, par),
+        lambda p, key: ops.witness_tuple(ops.peo_csr_witness(ip5, ix5, n5, p, key)))
+    del ip5, ix5
+    # configuration 3: dense rows, chord-removed copy (witness (2, 3600, 3))
+    n3 = 32768
+    u, v = chordal_random_edges(n3, 1024, 0)
+    keep = ~((u == 1) & (v == 0)) & ~((u == 0) & (v == 1))  # remove_first_chord drops edge (1, 2)
+    rows = DeviceRows(n3, device_stride(n3), ops.edges_to_dense(u[keep], v[keep], n3, device_stride(n3)))
+    run("c3_nonchordal", n3, lambda: ops.lexbfs(rows, want_parent=True),
+        lambda o, p, par, lo, hi, key: ops.peo_key(rows, o, p, lo, hi, key, par),
+        lambda p, key: ops.witness_tuple(ops.peo_witness(rows, p, key)))
+    return out
+
+
 # -------------------------------------------------------------------- main --
 
 
@@ -503,6 +596,8 @@ def run_ours(args, rank, world, local):
     }
     if rank == 0 and world == 1 and not args.no_cpu:
         line["cpu_baseline"] = cpu_batch_baseline(host[: min(B, 8192)].numpy())
+    if not args.no_secondary:
+        line["row_sharded_peo"] = row_sharded_lines(rank, world)
     if rank == 0 and world == 1 and not args.no_secondary:
         line["single_graph"] = single_graph_lines(with_cpu=not args.no_cpu)
         line["dense32k"] = {k: v["ms_per_graph"] for k, v in line["single_graph"].items() if k.startswith("c3")}

@@ -44,6 +44,15 @@ struct CsrWs {
 // u16 vertex/class ids (NIL = 0xFFFF) for n <= 32768; the per-neighbour arrays
 // (cls, c_cnt, c_tgt) then fit in shared memory next to the staging buffer.
 constexpr long long kSmemMaxN = 32768;
+constexpr int kPeoHeavy = 4096;     // rows longer than this are checked by the whole grid
+constexpr int kPeoHeavyMax = 4096;  // capacity of the heavy-row list
+
+// rows with more neighbours than this are "heavy"; at least kPeoHeavy, raised
+// with the edge count so that at most nnz / threshold < kPeoHeavyMax rows qualify
+__device__ __forceinline__ int64_t heavy_threshold(const int64_t *__restrict__ indptr, int n) {
+    const int64_t t = __ldg(indptr + n) / kPeoHeavyMax + 1;
+    return t > kPeoHeavy ? t : (int64_t)kPeoHeavy;
+}
 constexpr int kNbrBuf = 4096;  // neighbour-list staging entries
 inline size_t smem16_bytes(long long n) { return (size_t)(3 * n + 24 + kNbrBuf) * sizeof(uint16_t) + 64; }
 
@@ -125,9 +134,11 @@ peo_csr_key_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict
     const int lane = threadIdx.x & 31;
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
+    const int64_t heavy = heavy_threshold(indptr, n);
     for (int v = v_begin + gw; v < v_end; v += nw) {
         const int pv = __ldg(pos + v);
         const int64_t b = __ldg(indptr + v), e = __ldg(indptr + v + 1);
+        if (e - b > heavy) continue;  // heavy rows: split over the grid (peo_csr_heavy_*)
         int p = parent_in ? __ldg(parent_in + v) : -2;
         if (p == -2) {  // unknown: max position among the neighbours preceding v
             int best = -1;
@@ -164,6 +175,118 @@ peo_csr_key_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict
         }
         if (viol && lane == 0) atomicMin(key, k64);
     }
+}
+
+// ---- rows with more than kPeoHeavy neighbours (config 5: vertex 0 has 419,309)
+// One warp per row would serialise the whole check behind them, so their
+// neighbour lists are split into 1024-entry slices spread over the grid:
+//   collect  list the heavy rows of [v_begin, v_end)
+//   parent   (only where the search left it unknown) max position before
+//            pos(v) over the slices (atomicMax), then the neighbour holding it
+//   stray    every slice tests its candidates (z != p, pos(z) < pos(p),
+//            z not in N(p)) and lowers the key on a hit.
+struct PeoHeavy {
+    int count;
+    int pad;
+    int v[kPeoHeavyMax];
+    int best[kPeoHeavyMax];    // max position before pos(v) (parent search)
+    int parent[kPeoHeavyMax];  // resolved parent, -1 none
+};
+
+__global__ void peo_csr_heavy_collect(const int64_t *__restrict__ indptr, int n, const int32_t *__restrict__ parent_in,
+                                      int v_begin, int v_end, PeoHeavy *H) {
+    const int64_t heavy = heavy_threshold(indptr, n);
+    for (int v = v_begin + blockIdx.x * blockDim.x + threadIdx.x; v < v_end; v += gridDim.x * blockDim.x) {
+        if (__ldg(indptr + v + 1) - __ldg(indptr + v) > heavy) {
+            const int k = atomicAdd(&H->count, 1);
+            if (k < kPeoHeavyMax) {
+                H->v[k] = v;
+                H->best[k] = -1;
+                H->parent[k] = parent_in ? __ldg(parent_in + v) : -2;
+            }
+        }
+    }
+}
+
+constexpr int kSlice = 1024;  // neighbours per warp work item
+
+// every warp of the grid walks the (heavy row, slice) items
+template <typename Fn>
+__device__ __forceinline__ void for_each_heavy_slice(const int64_t *__restrict__ indptr, const PeoHeavy *H, Fn &&fn) {
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int nw = (gridDim.x * blockDim.x) >> 5;
+    const int cnt = min(H->count, kPeoHeavyMax);
+    long long item = 0;
+    for (int j = 0; j < cnt; ++j) {
+        const int v = H->v[j];
+        const int64_t b = __ldg(indptr + v), e = __ldg(indptr + v + 1);
+        const long long ns = (e - b + kSlice - 1) / kSlice;
+        for (long long sidx = ((gw - item) % nw + nw) % nw; sidx < ns; sidx += nw) {
+            const int64_t lo = b + sidx * kSlice, hi = min(e, lo + kSlice);
+            fn(j, v, lo, hi);
+        }
+        item += ns;
+    }
+}
+
+__global__ void __launch_bounds__(256) peo_csr_heavy_parent_max(const int64_t *__restrict__ indptr,
+                                                                const int32_t *__restrict__ indices,
+                                                                const int32_t *__restrict__ pos, PeoHeavy *H) {
+    const int lane = threadIdx.x & 31;
+    for_each_heavy_slice(indptr, H, [&](int j, int v, int64_t lo, int64_t hi) {
+        if (H->parent[j] != -2) return;  // given by the search
+        const int pv = __ldg(pos + v);
+        int best = -1;
+        for (int64_t k = lo + lane; k < hi; k += 32) {
+            const int pu = __ldg(pos + __ldg(indices + k));
+            if (pu < pv && pu > best) best = pu;
+        }
+        best = __reduce_max_sync(CH_FULL, best);
+        if (lane == 0 && best >= 0) atomicMax(&H->best[j], best);
+    });
+}
+
+__global__ void __launch_bounds__(256) peo_csr_heavy_parent_pick(const int64_t *__restrict__ indptr,
+                                                                 const int32_t *__restrict__ indices,
+                                                                 const int32_t *__restrict__ pos, PeoHeavy *H) {
+    const int lane = threadIdx.x & 31;
+    for_each_heavy_slice(indptr, H, [&](int j, int v, int64_t lo, int64_t hi) {
+        if (H->parent[j] != -2) return;
+        const int best = H->best[j];
+        if (best < 0) {
+            if (lo == __ldg(indptr + v) && lane == 0) H->parent[j] = -1;  // no left neighbour
+            return;
+        }
+        for (int64_t k = lo + lane; k < hi; k += 32) {
+            const int u = __ldg(indices + k);
+            if (__ldg(pos + u) == best) H->parent[j] = u;  // unique: positions are distinct
+        }
+    });
+}
+
+__global__ void __launch_bounds__(256) peo_csr_heavy_stray(const int64_t *__restrict__ indptr,
+                                                           const int32_t *__restrict__ indices,
+                                                           const int32_t *__restrict__ pos, const PeoHeavy *H,
+                                                           unsigned long long *__restrict__ key) {
+    const int lane = threadIdx.x & 31;
+    for_each_heavy_slice(indptr, H, [&](int j, int v, int64_t lo, int64_t hi) {
+        const int p = H->parent[j];
+        if (p < 0 || __ldg(pos + v) == 0) return;
+        const unsigned long long k64 = ((unsigned long long)p << 32) | (unsigned)v;
+        if (k64 >= *(volatile unsigned long long *)key) return;
+        const int pp = __ldg(pos + p);
+        const int64_t pb = __ldg(indptr + p), pe = __ldg(indptr + p + 1);
+        bool viol = false;
+        for (int64_t k0 = lo; k0 < hi; k0 += 32) {
+            const int64_t k = k0 + lane;
+            if (k < hi) {
+                const int z = __ldg(indices + k);
+                if (z != p && __ldg(pos + z) < pp && !contains(indices, pb, pe, z)) viol = true;
+            }
+            if (__any_sync(CH_FULL, viol)) { viol = true; break; }
+        }
+        if (viol && lane == 0) atomicMin(key, k64);
+    });
 }
 
 __global__ void peo_csr_witness_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
@@ -339,7 +462,20 @@ int launch_peo_csr_key(const int64_t *indptr, const int32_t *indices, int64_t n,
     peo_csr_key_kernel<<<(int)blocks, 256, 0, stream>>>(indptr, indices, (int)n, pos, parent, (int)v_begin,
                                                         (int)v_end, reinterpret_cast<unsigned long long *>(key));
     CH_LAUNCH_CHECK();
-    return CHORDAL_OK;
+    // heavy rows (stream-ordered scratch for their list)
+    PeoHeavy *H = nullptr;
+    if (cudaMallocAsync(reinterpret_cast<void **>(&H), sizeof(PeoHeavy), stream) != cudaSuccess) return CHORDAL_ENOMEM;
+    cudaMemsetAsync(H, 0, sizeof(int) * 2, stream);
+    long long cb = (v_end - v_begin + 255) / 256;
+    if (cb > 148LL * 8) cb = 148LL * 8;
+    peo_csr_heavy_collect<<<(int)cb, 256, 0, stream>>>(indptr, (int)n, parent, (int)v_begin, (int)v_end, H);
+    const int hb = 148 * 8;
+    peo_csr_heavy_parent_max<<<hb, 256, 0, stream>>>(indptr, indices, pos, H);
+    peo_csr_heavy_parent_pick<<<hb, 256, 0, stream>>>(indptr, indices, pos, H);
+    peo_csr_heavy_stray<<<hb, 256, 0, stream>>>(indptr, indices, pos, H, reinterpret_cast<unsigned long long *>(key));
+    const cudaError_t le = cudaGetLastError();
+    cudaFreeAsync(H, stream);
+    return le == cudaSuccess ? CHORDAL_OK : CHORDAL_ECUDA;
 }
 
 int launch_peo_csr_witness(const int64_t *indptr, const int32_t *indices, const int32_t *pos, const uint64_t *key,

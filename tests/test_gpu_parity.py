@@ -541,3 +541,41 @@ def test_mcs_bfs_against_oracle_larger():
     c = CSRGraph.from_edges0(200000, u, v)
     got = P.bfs_order(c).order0
     assert sorted(got.tolist()) == list(range(200000)) and got[0] == 0
+
+
+def test_csr_peo_heavy_rows():
+    """Rows longer than the heavy threshold (4096) are checked by the whole grid:
+    a hub with 9000 neighbours on a chordless 4-cycle, LexBFS order and random
+    orders (parents searched), against the oracle's list PEO test."""
+    from paper_1508_06329_b200.csr import CSRGraph
+
+    rng = np.random.default_rng(11)
+    n = 12000
+    us, vs = [0, 1, 2, 3], [1, 2, 3, 0]                    # C4: 0-1-2-3-0, no 0-2, no 1-3
+    hub = [w for w in range(4, 9004)]
+    us += [0] * len(hub)
+    vs += hub
+    a = rng.integers(4, n, 20000)
+    b = rng.integers(4, n, 20000)
+    keep = a != b
+    us += a[keep].tolist()
+    vs += b[keep].tolist()
+    g = CSRGraph.from_edges0(n, np.array(us), np.array(vs))
+    ip, ix = g.indptr, g.indices
+    v = P.is_chordal(g)
+    order = oracle.lexbfs_partition_csr(ip, ix, n)
+    ok, w = oracle.is_peo_csr(ip, ix, n, order)
+    assert v.chordal == ok and o0(P.lexbfs_partition(g)) == order.tolist()
+    assert (w0(v.witness) or [-1, -1, -1]) == (list(w) if w is not None else [-1, -1, -1])
+    for s in range(3):
+        perm = rng.permutation(n).astype(np.int32)
+        ok2, w2 = oracle.is_peo_csr(ip, ix, n, perm)
+        okg, wg = P.is_peo(g, P.VertexOrdering.from_zero_based(perm))
+        assert okg == ok2 and (w0(wg) or [-1, -1, -1]) == (list(w2) if w2 is not None else [-1, -1, -1]), s
+    # chordal with a heavy hub: star + random tree edges between leaves' private vertices
+    us2 = [0] * 8000 + list(range(8001, 11000))
+    vs2 = list(range(1, 8001)) + [int(x) for x in rng.integers(1, 8001, 2999)]
+    g2 = CSRGraph.from_edges0(11000, np.array(us2), np.array(vs2))
+    order2 = oracle.lexbfs_partition_csr(g2.indptr, g2.indices, 11000)
+    ok3, _ = oracle.is_peo_csr(g2.indptr, g2.indices, 11000, order2)
+    assert P.is_chordal(g2).chordal == ok3
