@@ -34,8 +34,9 @@ def main(what):
     if what in ("lexbfs32k", "peo32k", "all"):
         r = rows_chordal(32768, 1024, 0)
         for _ in range(2):
-            order, pos = ops.lexbfs(r)
-            ops.peo(r, order, pos)
+            order, pos, parent = ops.lexbfs(r, want_parent=True)
+            ops.peo(r, order, pos, parent)  # the pipeline form (parents from LexBFS)
+            ops.peo(r, order, pos)          # standalone is_peo (parents searched)
     if what == "csr1m":
         from paper_1508_06329_b200.generate import gen_chordal_random_csr_device
 
