@@ -579,3 +579,23 @@ def test_csr_peo_heavy_rows():
     order2 = oracle.lexbfs_partition_csr(g2.indptr, g2.indices, 11000)
     ok3, _ = oracle.is_peo_csr(g2.indptr, g2.indices, 11000, order2)
     assert P.is_chordal(g2).chordal == ok3
+
+
+def test_new_orderings_edge_cases():
+    """n = 0 / 1 / edgeless / complete for MCS, BFS and the seeded linked variants."""
+    from paper_1508_06329_b200.csr import CSRGraph
+
+    for n in (0, 1, 2, 7):
+        e = P.Graph.from_edge_list(n, [])
+        k = P.Graph.from_edge_list(n, [(a, b) for a in range(1, n + 1) for b in range(a + 1, n + 1)])
+        for g in (e, k):
+            want = list(range(1, n + 1))
+            assert list(P.mcs_order(g)) == want and list(P.bfs_order(g)) == want
+            assert list(P.lexbfs_partition(g, P.seeded(3), method="linked")) == \
+                [x + 1 for x in oracle.lexbfs_linked_seeded(g._packed, n, 3, "partition").tolist()]
+            assert list(P.lexbfs_labels(g, P.seeded(3), method="linked")) == \
+                [x + 1 for x in oracle.lexbfs_linked_seeded(g._packed, n, 3, "labels").tolist()]
+            assert list(P.mcs_order(g, P.seeded(5))) == [x + 1 for x in oracle.other_order(g._packed, n, "mcs", 5)]
+            assert list(P.bfs_order(g, P.seeded(5))) == [x + 1 for x in oracle.other_order(g._packed, n, "bfs", 5)]
+    c = CSRGraph.from_edges0(3, np.array([0]), np.array([2]))
+    assert list(P.bfs_order(c)) == [1, 3, 2]
