@@ -37,6 +37,9 @@ def main(what):
             order, pos, parent = ops.lexbfs(r, want_parent=True)
             ops.peo(r, order, pos, parent)  # the pipeline form (parents from LexBFS)
             ops.peo(r, order, pos)          # standalone is_peo (parents searched)
+    if what == "lexbfs8k":
+        r = rows_chordal(8192, 8, 0)
+        ops.lexbfs(r)
     if what == "csr1m":
         from paper_1508_06329_b200.generate import gen_chordal_random_csr_device
 

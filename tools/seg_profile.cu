@@ -33,7 +33,8 @@ int main(int argc, char **argv) {
         cudaEventCreate(&a);
         cudaEventCreate(&b);
         cudaEventRecord(a);
-        int rc = chordal::launch_lexbfs_seg(adj, n, stride, -1, CHORDAL_TIE_ASCENDING, 0, cell, ord, ord + n, ord + 2 * n,
+        int rc = chordal::launch_lexbfs_seg(adj, n, stride, -1, CHORDAL_TIE_ASCENDING, 0, cell, ord, ord + n,
+                                            getenv("NOPARENT") ? nullptr : ord + 2 * n,
                                             0);
         cudaEventRecord(b);
         cudaEventSynchronize(b);
