@@ -708,7 +708,7 @@ lexbfs_warp_kernel(const uint8_t *__restrict__ adj, int n, long long stride, int
     M.par = M.P + np;
     M.F = (uint32_t *)(M.par + np);
     M.NB = M.F + 32;
-    warp_seg_lexbfs<MODE>(reinterpret_cast<const uint32_t *>(adj), (int)(stride >> 2), n, M);
+    warp_seg_lexbfs<MODE, true>(reinterpret_cast<const uint32_t *>(adj), (int)(stride >> 2), n, M);
     for (int k = threadIdx.x; k < n; k += 32) {
         order[k] = M.A[k];
         pos_out[k] = M.P[k];

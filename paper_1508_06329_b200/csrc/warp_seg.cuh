@@ -23,6 +23,19 @@ namespace chordal {
 // [0] steps [1] row-guess hits [2] cycles waiting for the row [3] total cycles
 // [4] split steps (tools/warp_profile.cu only)
 __device__ unsigned long long wseg_prof[8];
+// per-phase cycles: [0] pivot + row [1] movers [2] newly reached + scan
+// [3] split decision [4] split [5] append + tail
+__device__ unsigned long long wseg_ph[8];
+#define WSEG_T(k)                                              \
+    do {                                                       \
+        const long long _c = clock64();                        \
+        ph[k] += (unsigned long long)(_c - ph_t0);             \
+        ph_t0 = _c;                                            \
+    } while (0)
+#else
+#define WSEG_T(k) \
+    do {          \
+    } while (0)
 #endif
 
 struct WarpSegMem {
@@ -41,6 +54,21 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     return m;
 }
 
+// Exclusive prefix sum over the warp of small values c in [0, 63], and their total:
+// six independent ballots of the bit planes instead of a five-round shuffle scan
+// (the per-step chain is latency-bound).
+__device__ __forceinline__ int excl_prefix6(int c, uint32_t lt, int &total) {
+    int pre = 0, tot = 0;
+#pragma unroll
+    for (int bit = 0; bit < 6; ++bit) {
+        const uint32_t bm = __ballot_sync(CH_FULL, (c >> bit) & 1);
+        pre += __popc(bm & lt) << bit;
+        tot += __popc(bm) << bit;
+    }
+    total = tot;
+    return pre;
+}
+
 // A load that is issued where it stands (the speculative next-row load must
 // not be sunk to its use one step later).
 __device__ __forceinline__ uint32_t ld_issue(const uint32_t *p) {
@@ -52,10 +80,11 @@ __device__ __forceinline__ uint32_t ld_issue(const uint32_t *p) {
 }  // namespace wseg
 
 // rows: the graph's packed rows (global), sw: row pitch in 32-bit words.
-template <int MODE>
+template <int MODE, bool LATENCY = false>
 __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n, const WarpSegMem &M) {
     using namespace wseg;
     const int l = threadIdx.x & 31;
+    const uint32_t ltm = lanemask_lt();
     const int W = (n + 31) >> 5;
     uint32_t Ul = l < W ? ((l < W - 1 || !(n & 31)) ? CH_FULL : mask_below(n & 31)) : 0u;
     uint32_t RAl = 0, Bl = 0;
@@ -75,6 +104,8 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
     uint32_t nxt = 0;
 #ifdef WSEG_PROFILE
     unsigned long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    long long ph_t0 = clock64();
     const long long pstart = clock64();
 #endif
     for (int i = 0; i < n; ++i) {
@@ -122,6 +153,7 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
         if (hpos + 1 < tail0 && l == 0)  // two steps ahead: warm L2
             asm volatile("prefetch.global.L2 [%0];" ::"l"(rows + (long long)M.A[hpos + 1] * sw));
         if (l == (x >> 5)) RAl &= ~(1u << (x & 31));
+        WSEG_T(0);
         uint32_t mv = r & RAl;
         const uint32_t ext = r & Ul;
         // ---- movers: flag their positions, record x as their parent ------------
@@ -147,6 +179,7 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
                 }
             }
         }
+        WSEG_T(1);
         if (ext) {
             if (M.par) {
                 uint32_t m3 = ext;
@@ -160,16 +193,25 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
         }
         const int cntA = __reduce_add_sync(CH_FULL, cnt);
         // newly reached vertices: exclusive prefix over lanes (= id order)
-        const int ec = __popc(ext);
-        int incl = ec;
+        // newly reached vertices: exclusive prefix over lanes (= id order); the
+        // single-graph kernel takes the shorter-latency ballot form, the batch
+        // the cheaper shuffle scan (more graphs in flight hide its latency)
+        int ktot, xe;
+        if (LATENCY) {
+            xe = excl_prefix6(__popc(ext), ltm, ktot);
+        } else {
+            const int ec = __popc(ext);
+            int incl = ec;
 #pragma unroll
-        for (int d = 1; d < 32; d <<= 1) {
-            const int o = __shfl_up_sync(CH_FULL, incl, d);
-            if (l >= d) incl += o;
+            for (int d = 1; d < 32; d <<= 1) {
+                const int o = __shfl_up_sync(CH_FULL, incl, d);
+                if (l >= d) incl += o;
+            }
+            xe = incl - ec;
+            ktot = __shfl_sync(CH_FULL, incl, 31);
         }
-        const int xe = incl - ec;
-        const int ktot = __shfl_sync(CH_FULL, incl, 31);
 
+        WSEG_T(2);
         if (cntA) {
             __syncwarp();  // the mover flags are in F
             const uint32_t Fl = M.F[l];
@@ -197,6 +239,7 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
 #ifdef WSEG_PROFILE
             if (!whole) pacc[4]++;
 #endif
+            WSEG_T(3);
             if (!whole) {
                 // region class starts of word l: [hpos, tail0) with hpos forced
                 uint32_t b = Bl;
@@ -208,19 +251,32 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
                 const int fc = __popc(Fl);
                 const int hb = b ? 32 * l + highest_bit(b) : 0;
                 const int lb = b ? 32 * l + __ffs(b) - 1 : kBig;
-                int ia = fc, ih = hb, il = lb;
+                int Pc, LBr, NBr;  // movers before word l; last class start before it, first after it
+                if (LATENCY) {
+                    int fct;
+                    Pc = excl_prefix6(fc, ltm, fct);
+                    // the starts grow with the word: the nearest words with a start
+                    const uint32_t bw = __ballot_sync(CH_FULL, b != 0);
+                    const uint32_t below = bw & ltm, above = bw & ~ltm & ~(1u << l);
+                    LBr = __shfl_sync(CH_FULL, hb, below ? highest_bit(below) : 0);
+                    NBr = __shfl_sync(CH_FULL, lb, above ? __ffs(above) - 1 : 0);
+                    if (!below) LBr = 0;
+                    if (!above) NBr = kBig;
+                } else {
+                    int ia = fc, ih = hb, il = lb;
 #pragma unroll
-                for (int d = 1; d < 32; d <<= 1) {
-                    const int oa = __shfl_up_sync(CH_FULL, ia, d), oh = __shfl_up_sync(CH_FULL, ih, d);
-                    const int ol = __shfl_down_sync(CH_FULL, il, d);
-                    if (l >= d) { ia += oa; ih = max(ih, oh); }
-                    if (l + d < 32) il = min(il, ol);
+                    for (int d = 1; d < 32; d <<= 1) {
+                        const int oa = __shfl_up_sync(CH_FULL, ia, d), oh = __shfl_up_sync(CH_FULL, ih, d);
+                        const int ol = __shfl_down_sync(CH_FULL, il, d);
+                        if (l >= d) { ia += oa; ih = max(ih, oh); }
+                        if (l + d < 32) il = min(il, ol);
+                    }
+                    Pc = ia - fc;
+                    LBr = __shfl_up_sync(CH_FULL, ih, 1);
+                    NBr = __shfl_down_sync(CH_FULL, il, 1);
+                    if (l == 0) LBr = 0;
+                    if (l == 31) NBr = kBig;
                 }
-                const int Pc = ia - fc;  // movers before word l
-                int LBr = __shfl_up_sync(CH_FULL, ih, 1);  // last class start before word l
-                int NBr = __shfl_down_sync(CH_FULL, il, 1);  // first class start after word l
-                if (l == 0) LBr = 0;
-                if (l == 31) NBr = kBig;
                 NBr = min(NBr, tail0);
                 // movers at positions < pp (all lanes must call: shuffles)
                 auto cntb = [&](int pp) -> int {
@@ -290,6 +346,7 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
                 M.NB[l] = 0;
             }
         }
+        WSEG_T(4);
         // ---- append the newly reached vertices as one class (tie order) ---------
         if (ext) {
             int idx = xe;
@@ -310,6 +367,7 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
             ++nclasses;
         }
         __syncwarp();
+        WSEG_T(5);
         // ---- early exit: everything reached, every class a singleton ---------------
         if (tail == n && nclasses == tail - hpos) {
             if (M.par)
@@ -321,7 +379,10 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
 #ifdef WSEG_PROFILE
     pacc[3] = clock64() - pstart;
     if (l == 0)
-        for (int k = 0; k < 8; ++k) atomicAdd(&wseg_prof[k], pacc[k]);
+        for (int k = 0; k < 8; ++k) {
+            atomicAdd(&wseg_prof[k], pacc[k]);
+            atomicAdd(&wseg_ph[k], ph[k]);
+        }
 #endif
 }
 

@@ -25,6 +25,7 @@ int main(int argc, char **argv) {
     for (int rep = 0; rep < 2; ++rep) {
         unsigned long long z[8] = {0};
         cudaMemcpyToSymbol(chordal::wseg_prof, z, sizeof(z));
+        cudaMemcpyToSymbol(chordal::wseg_ph, z, sizeof(z));
         cudaEvent_t a, b;
         cudaEventCreate(&a);
         cudaEventCreate(&b);
@@ -40,6 +41,11 @@ int main(int argc, char **argv) {
         const char *const names[] = {"steps", "guess-hit", "row-wait-cyc", "total-cyc", "split-steps"};
         for (int k = 0; k < 5; ++k)
             printf("  %-13s %12llu  %8.1f per step\n", names[k], p[k], (double)p[k] / (double)(p[0] ? p[0] : 1));
+        unsigned long long q[8];
+        cudaMemcpyFromSymbol(q, chordal::wseg_ph, sizeof(q));
+        const char *const ph[] = {"pivot+row", "movers", "reached+scan", "split-decide", "split", "append+tail"};
+        for (int k = 0; k < 6; ++k)
+            printf("  %-13s %12llu  %8.1f per step\n", ph[k], q[k], (double)q[k] / (double)(p[0] ? p[0] : 1));
     }
     return 0;
 }
