@@ -314,6 +314,37 @@ def single_graph_lines(with_cpu: bool) -> dict:
         "peo_roofline": {"bound": "hbm", "achieved_gbs": peo5_bytes / (peo5 * 1e-3) / 1e9,
                          "frac": peo5_bytes / (peo5 * 1e-3) / 1e9 / peaks["hbm_gbs"], "algorithmic_bytes": peo5_bytes},
     }
+    # the other orderings and the text formats: GPU time beside the
+    # oracle's C port of the reference algorithm (1 core) on the same graph
+    from paper_1508_06329_b200 import textio
+    from paper_1508_06329_b200.generate import gen_dense_random as gen_dense_host
+
+    g2 = gen_dense_host(8192, 0.5, 0, cap=8192)
+    rows2 = DeviceRows(8192, device_stride(8192), torch.from_numpy(
+        np.pad(np.asarray(g2._packed), ((0, 0), (0, device_stride(8192) - g2._packed.shape[1])))).cuda(), m=g2.m)
+    ip2, ix2 = ops.csr_from_rows(rows2)
+    mcs_ms = time_events(lambda: ops.mcs(rows2))
+    bfs_ms = time_events(lambda: ops.bfs_dense(rows2))
+    bfs_csr_ms = time_events(lambda: ops.bfs_csr(ip2, ix2, 8192))
+    txt = textio.write_graph_text(g2)
+    t0 = time.perf_counter()
+    g2b = textio.parse_graph_text(txt, cap=8192)
+    parse_s = time.perf_counter() - t0
+    assert g2b == g2
+    other = {"graph": "gen_dense_random(8192, 0.5, 0)", "m": int(g2.m),
+             "mcs_order_ms": mcs_ms, "bfs_order_ms": bfs_ms, "bfs_order_csr_ms": bfs_csr_ms,
+             "parse_graph_text": {"bytes": len(txt), "s": parse_s, "MBps": len(txt) / parse_s / 1e6, "threads": 1}}
+    if with_cpu:
+        import oracle
+
+        t0 = time.perf_counter()
+        oracle.other_order(g2._packed, 8192, "mcs")
+        t1 = time.perf_counter()
+        oracle.other_order(g2._packed, 8192, "bfs")
+        t2 = time.perf_counter()
+        other["cpu_baseline"] = {"mcs_order_ms": (t1 - t0) * 1e3, "bfs_order_ms": (t2 - t1) * 1e3, "cores": 1,
+                                 "kind": "port"}
+    out["orders_and_text"] = other
     if with_cpu:
         import oracle
 

@@ -251,6 +251,10 @@ int chordal_mcs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int32_t
  * stream (seed, "bfs").  ws: chordal_bfs_csr_workspace_bytes(n) bytes (0
  * unless n exceeds the shared-memory bitset). */
 size_t chordal_bfs_csr_workspace_bytes(int64_t n);
+/* bfs_order on dense rows (n <= 65535): fresh neighbours = row & ~queued, one
+ * warp, word-parallel -- the form for dense-stored graphs. */
+int chordal_bfs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int32_t seeded, uint64_t seed,
+                      int32_t *order_dev, int32_t *pos_dev, void *stream);
 int chordal_bfs_csr(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, int32_t seeded, uint64_t seed,
                     int32_t *order_dev, int32_t *pos_dev, void *ws, size_t ws_bytes, void *stream);
 

@@ -51,6 +51,7 @@ SIGNATURES = {
     "chordal_gen_chordal_random_edges": [_I64, _I64, _I64, _P, _P, _P, _P, _SZ, _P],
     "chordal_mcs_dense": [_P, _I64, _I64, _I32, _U64, _P, _P, _P],
     "chordal_bfs_csr_workspace_bytes": [_I64],
+    "chordal_bfs_dense": [_P, _I64, _I64, _I32, _U64, _P, _P, _P],
     "chordal_bfs_csr": [_P, _P, _I64, _I32, _U64, _P, _P, _P, _SZ, _P],
     "chordal_parse_graph_text": [_P, _I64, _I64, _P, _P, _P, _I64, _P, _P, _I64],
     "chordal_write_graph_text": [_P, _I64, _I64, _I64, _P, _I64],

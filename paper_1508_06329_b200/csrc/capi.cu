@@ -30,6 +30,7 @@ int launch_permute_dense(const uint8_t *, int64_t, int64_t, const int32_t *, uin
 int launch_batch(const uint8_t *, int64_t, int64_t, int64_t, int32_t *, int32_t *, cudaStream_t);
 int launch_mcs_dense(const uint8_t *, int64_t, int64_t, bool, uint64_t, int32_t *, int32_t *, cudaStream_t);
 size_t bfs_csr_workspace_bytes(int64_t);
+int launch_bfs_dense(const uint8_t *, int64_t, int64_t, bool, uint64_t, int32_t *, int32_t *, cudaStream_t);
 int launch_bfs_csr(const int64_t *, const int32_t *, int64_t, bool, uint64_t, uint32_t *, int32_t *, int32_t *,
                    cudaStream_t);
 int launch_gen_dense_random(uint8_t *, int64_t, int64_t, int64_t, double, int64_t, int64_t, uint32_t,
@@ -329,6 +330,16 @@ int chordal_mcs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int32_t
     if (!order_dev || !pos_dev) return CHORDAL_EINVAL;
     const uint64_t key = splitmix64(splitmix64(seed) ^ (uint64_t)crc32_str("mcs"));
     return launch_mcs_dense(adj_dev, n, stride, seeded != 0, key, order_dev, pos_dev, as_stream(stream));
+}
+
+int chordal_bfs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int32_t seeded, uint64_t seed,
+                      int32_t *order_dev, int32_t *pos_dev, void *stream) {
+    int rc = check_dense(adj_dev, n, stride);
+    if (rc) return rc;
+    if (n == 0) return CHORDAL_OK;
+    if (!order_dev || !pos_dev) return CHORDAL_EINVAL;
+    const uint64_t key = splitmix64(splitmix64(seed) ^ (uint64_t)crc32_str("bfs"));
+    return launch_bfs_dense(adj_dev, n, stride, seeded != 0, key, order_dev, pos_dev, as_stream(stream));
 }
 
 size_t chordal_bfs_csr_workspace_bytes(int64_t n) { return n > 0 ? bfs_csr_workspace_bytes(n) : 0; }

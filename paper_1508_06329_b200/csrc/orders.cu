@@ -141,11 +141,77 @@ mcs_dense_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint6
 }
 
 // BFS on CSR rows, one warp.  `queued` is an n-bit bitset (shared or global).
-template <bool SEEDED>
-__device__ void bfs_csr_warp(const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices, int n,
-                             uint64_t key, uint32_t *queued, int32_t *__restrict__ order, int32_t *__restrict__ pos) {
+// Neighbour sources of the BFS: append x's unqueued neighbours, ascending, at
+// order[tail...] and mark them queued; returns the new tail.
+struct BfsCsrRows {
+    const int64_t *indptr;
+    const int32_t *indices;
+    __device__ __forceinline__ int append(int x, uint32_t *queued, int32_t *order, int tail) const {
+        const int lane = threadIdx.x & 31;
+        const uint32_t lt = (1u << lane) - 1u;
+        const int64_t b = __ldg(indptr + x), e = __ldg(indptr + x + 1);
+        for (int64_t c0 = b; c0 < e; c0 += 32) {
+            const int64_t k = c0 + lane;
+            const int y = k < e ? __ldg(indices + k) : 0;
+            const bool fresh = k < e && !((queued[y >> 5] >> (y & 31)) & 1u);
+            const uint32_t fm = __ballot_sync(CH_FULL, fresh);
+            if (fresh) {
+                order[tail + __popc(fm & lt)] = y;
+                atomicOr(&queued[y >> 5], 1u << (y & 31));
+            }
+            tail += __popc(fm);
+            __syncwarp();
+        }
+        return tail;
+    }
+};
+
+// Dense rows: fresh = row & ~queued word by word, lane l owning a contiguous run
+// of words so that one warp prefix sum places the fresh vertices in id order.
+struct BfsDenseRows {
+    const uint32_t *rows;
+    long long sw;  // pitch in words
+    int W;         // words holding vertex bits
+    __device__ __forceinline__ int append(int x, uint32_t *queued, int32_t *order, int tail) const {
+        const int lane = threadIdx.x & 31;
+        const uint32_t *r = rows + (long long)x * sw;
+        for (int base = 0; base < W; base += 32 * 8) {  // 8 words per lane per round
+            const int w0 = base + 8 * lane;
+            uint32_t f[8];
+            int c = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int w = w0 + j;
+                f[j] = w < W ? (__ldg(r + w) & ~queued[w]) : 0u;
+                c += __popc(f[j]);
+            }
+            int incl = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+                const int o = __shfl_up_sync(CH_FULL, incl, d);
+                if (lane >= d) incl += o;
+            }
+            int at = tail + incl - c;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                uint32_t m = f[j];
+                if (m) queued[w0 + j] |= m;
+                while (m) {
+                    order[at++] = 32 * (w0 + j) + __ffs(m) - 1;
+                    m &= m - 1;
+                }
+            }
+            tail += __shfl_sync(CH_FULL, incl, 31);
+            __syncwarp();
+        }
+        return tail;
+    }
+};
+
+template <bool SEEDED, typename Rows>
+__device__ void bfs_warp(const Rows &R, int n, uint64_t key, uint32_t *queued, int32_t *__restrict__ order,
+                         int32_t *__restrict__ pos) {
     const int lane = threadIdx.x & 31;
-    const uint32_t lt = (1u << lane) - 1u;
     const int W = (n + 31) >> 5;
     for (int w = lane; w < W; w += 32) queued[w] = 0;
     __syncwarp();
@@ -199,21 +265,8 @@ __device__ void bfs_csr_warp(const int64_t *__restrict__ indptr, const int32_t *
         }
         const int x = order[head];
         ++head;
-        const int64_t b = __ldg(indptr + x), e = __ldg(indptr + x + 1);
         const int t0 = tail;
-        for (int64_t c0 = b; c0 < e; c0 += 32) {
-            const int64_t k = c0 + lane;
-            const int y = k < e ? __ldg(indices + k) : 0;
-            const bool fresh = k < e && !((queued[y >> 5] >> (y & 31)) & 1u);
-            const uint32_t fm = __ballot_sync(CH_FULL, fresh);
-            if (fresh) {
-                const int at = tail + __popc(fm & lt);
-                order[at] = y;
-                atomicOr(&queued[y >> 5], 1u << (y & 31));
-            }
-            tail += __popc(fm);
-            __syncwarp();
-        }
+        tail = R.append(x, queued, order, tail);
         if (SEEDED && tail - t0 > 1) {  // gen.shuffle(fresh) (search.py:104-105)
             // every lane draws (the stream stays identical across lanes), lane 0 swaps
             for (int i2 = tail - t0 - 1; i2 >= 1; --i2) {
@@ -243,7 +296,29 @@ __global__ void __launch_bounds__(32, 1)
 bfs_csr_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices, int n, uint64_t key,
                uint32_t *gqueued, int32_t *__restrict__ order, int32_t *__restrict__ pos) {
     extern __shared__ uint32_t squeued[];
-    bfs_csr_warp<SEEDED>(indptr, indices, n, key, gqueued ? gqueued : squeued, order, pos);
+    bfs_warp<SEEDED>(BfsCsrRows{indptr, indices}, n, key, gqueued ? gqueued : squeued, order, pos);
+}
+
+template <bool SEEDED>
+__global__ void __launch_bounds__(32, 1)
+bfs_dense_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint64_t key, int32_t *__restrict__ order,
+                 int32_t *__restrict__ pos) {
+    extern __shared__ uint32_t squeued[];
+    bfs_warp<SEEDED>(BfsDenseRows{reinterpret_cast<const uint32_t *>(adj), stride >> 2, (n + 31) >> 5}, n, key,
+                     squeued, order, pos);
+}
+
+int launch_bfs_dense(const uint8_t *adj, int64_t n, int64_t stride, bool seeded, uint64_t key, int32_t *order,
+                     int32_t *pos, cudaStream_t stream) {
+    if (n <= 0) return CHORDAL_OK;
+    if (n > 65535) return CHORDAL_ETOOLARGE;
+    const size_t smem = (size_t)((n + 31) / 32) * sizeof(uint32_t);
+    if (seeded)
+        bfs_dense_kernel<true><<<1, 32, smem, stream>>>(adj, (int)n, stride, key, order, pos);
+    else
+        bfs_dense_kernel<false><<<1, 32, smem, stream>>>(adj, (int)n, stride, key, order, pos);
+    CH_LAUNCH_CHECK();
+    return CHORDAL_OK;
 }
 
 int launch_mcs_dense(const uint8_t *adj, int64_t n, int64_t stride, bool seeded, uint64_t key, int32_t *order,

@@ -324,3 +324,14 @@ def bfs_csr(indptr, indices, n: int, seeded: bool = False, seed: int = 0, stream
                                   ptr(pos), ptr(ws) if ws is not None else None, wsb, stream_ptr(stream)),
               "chordal_bfs_csr")
     return order[:n], pos[:n]
+
+
+def bfs_dense(rows: DeviceRows, seeded: bool = False, seed: int = 0, stream=None):
+    """Breadth-first order on device rows (word-parallel) -> (order, pos) int32 device tensors."""
+    torch = _native.require_cuda()
+    n, dev = rows.n, rows.data.device
+    order, pos = _i32(torch, n, dev), _i32(torch, n, dev)
+    if n:
+        check(lib.chordal_bfs_dense(rows.ptr, n, rows.stride, int(bool(seeded)), seed & U64_MAX, ptr(order),
+                                    ptr(pos), stream_ptr(stream)), "chordal_bfs_dense")
+    return order[:n], pos[:n]

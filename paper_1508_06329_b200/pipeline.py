@@ -85,7 +85,10 @@ def bfs_order(g, seeded: bool, seed: int) -> VertexOrdering:
         return VertexOrdering(())
     if is_csr(g):
         ip, ix = device_csr(g)
+        order, pos = ops.bfs_csr(ip, ix, n, seeded, seed)
+    elif n <= 65535:  # dense rows: word-parallel fresh-neighbour masks
+        order, pos = ops.bfs_dense(device_rows(g), seeded, seed)
     else:
         ip, ix = ops.csr_from_rows(device_rows(g))
-    order, pos = ops.bfs_csr(ip, ix, n, seeded, seed)
+        order, pos = ops.bfs_csr(ip, ix, n, seeded, seed)
     return VertexOrdering._trusted(order.cpu().numpy(), pos.cpu().numpy())
