@@ -178,6 +178,60 @@ def gen_chordal_random(n: int, k: int, seed: int, *, cap: int | None = None) -> 
     return Graph._from_numpy_edges(n, u + 1, v + 1)
 
 
+def gen_sparse_random(n: int, seed: int, *, cap: int | None = None) -> Graph:
+    """20n distinct uniform edges (generate.py:59-81): batches of endpoint pairs
+    drawn from the "sparse-random" stream, self-loops dropped, first occurrences
+    kept in draw order until 20n are collected."""
+    if n < 41:
+        raise InvalidSize(f"need n >= 41 so that 20n edges fit, got {n}")
+    _check_size(n, cap)
+    gen = stream(seed, "sparse-random")
+    need = 20 * n
+    taken: dict[int, None] = {}
+    while len(taken) < need:
+        batch = max(4096, 2 * (need - len(taken)))
+        a = gen.integers(0, n, size=batch, dtype=np.int64)
+        b = gen.integers(0, n, size=batch, dtype=np.int64)
+        keep = a != b
+        codes = np.minimum(a[keep], b[keep]) * n + np.maximum(a[keep], b[keep])
+        for c in codes.tolist():
+            if c not in taken:
+                taken[c] = None
+                if len(taken) == need:
+                    break
+    codes = np.fromiter(taken.keys(), dtype=np.int64, count=need)
+    return Graph._from_numpy_edges(n, codes // n + 1, codes % n + 1)
+
+
+def gen_tree(n: int, seed: int, *, cap: int | None = None) -> Graph:
+    """Uniform labelled tree (generate.py:84-115): the Pruefer code of n-2 draws
+    from the "tree" stream, decoded (the tree of a code is unique)."""
+    import heapq
+
+    if n < 1:
+        raise InvalidSize("tree needs at least one vertex")
+    _check_size(n, cap)
+    if n == 1:
+        return Graph.from_edge_list(1, [])
+    if n == 2:
+        return Graph.from_edge_list(2, [(1, 2)])
+    code = stream(seed, "tree").integers(0, n, size=n - 2, dtype=np.int64)
+    deg = np.ones(n, dtype=np.int64)
+    np.add.at(deg, code, 1)
+    leaves = [v for v in range(n) if deg[v] == 1]
+    heapq.heapify(leaves)
+    u = np.empty(n - 1, dtype=np.int64)
+    v = np.empty(n - 1, dtype=np.int64)
+    for i, c in enumerate(code.tolist()):
+        leaf = heapq.heappop(leaves)
+        u[i], v[i] = leaf, c
+        deg[c] -= 1
+        if deg[c] == 1:
+            heapq.heappush(leaves, c)
+    u[n - 2], v[n - 2] = heapq.heappop(leaves), heapq.heappop(leaves)
+    return Graph._from_numpy_edges(n, u + 1, v + 1)
+
+
 def remove_first_chord(g: Graph) -> tuple[Graph, tuple[int, int] | None]:
     """Drop the first edge u<v (edges() order) whose endpoints share two
     non-adjacent common neighbours; the copy then has a chordless 4-cycle.
