@@ -192,12 +192,16 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
             RAl |= ext;
         }
         const int cntA = __reduce_add_sync(CH_FULL, cnt);
-        // newly reached vertices: exclusive prefix over lanes (= id order)
-        // newly reached vertices: exclusive prefix over lanes (= id order); the
-        // single-graph kernel takes the shorter-latency ballot form, the batch
+        // newly reached vertices: exclusive prefix over lanes (= id order).  Most
+        // steps reach nothing new or only within one word: no scan then; otherwise
+        // the single-graph kernel takes the shorter-latency ballot form, the batch
         // the cheaper shuffle scan (more graphs in flight hide its latency)
         int ktot, xe;
-        if (LATENCY) {
+        const uint32_t extw = __ballot_sync(CH_FULL, ext != 0);
+        if (__popc(extw) <= 1) {
+            xe = 0;
+            ktot = extw ? __popc(__shfl_sync(CH_FULL, ext, __ffs(extw) - 1)) : 0;
+        } else if (LATENCY) {
             xe = excl_prefix6(__popc(ext), ltm, ktot);
         } else {
             const int ec = __popc(ext);
