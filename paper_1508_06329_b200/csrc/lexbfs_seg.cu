@@ -695,7 +695,7 @@ size_t seg_smem_bytes(int64_t n) { return SegLayout((int)((n + 31) >> 5)).total;
 
 // n <= 1024, LOWEST_INDEX / descending ties: the one-warp engine (warp_seg.cuh),
 // bitsets in registers; the arrays are copied out at the end.
-template <int MODE>
+template <int MODE, bool STAGE>
 __global__ void __launch_bounds__(32, 1)
 lexbfs_warp_kernel(const uint8_t *__restrict__ adj, int n, long long stride, int32_t *__restrict__ order,
                    int32_t *__restrict__ pos_out, int32_t *__restrict__ parent) {
@@ -708,7 +708,24 @@ lexbfs_warp_kernel(const uint8_t *__restrict__ adj, int n, long long stride, int
     M.par = M.P + np;
     M.F = (uint32_t *)(M.par + np);
     M.NB = M.F + 32;
-    warp_seg_lexbfs<MODE, true>(reinterpret_cast<const uint32_t *>(adj), (int)(stride >> 2), n, M);
+    const uint32_t *rows = reinterpret_cast<const uint32_t *>(adj);
+    if (STAGE) {  // rows into shared memory after the state (16-byte aligned), eight copies in flight per lane
+        uint4 *dst = reinterpret_cast<uint4 *>(smem + ((np * 8 + 256 + 15) & ~size_t(15)));
+        const uint4 *src = reinterpret_cast<const uint4 *>(adj);
+        const int n16 = n * (int)(stride >> 4), lane = threadIdx.x & 31;
+        int k = lane;
+        for (; k + 7 * 32 < n16; k += 8 * 32) {
+            uint4 t[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) t[j] = __ldg(src + k + 32 * j);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) dst[k + 32 * j] = t[j];
+        }
+        for (; k < n16; k += 32) dst[k] = __ldg(src + k);
+        __syncwarp();
+        rows = reinterpret_cast<const uint32_t *>(dst);
+    }
+    warp_seg_lexbfs<MODE, true, STAGE>(rows, (int)(stride >> 2), n, M);
     for (int k = threadIdx.x; k < n; k += 32) {
         order[k] = M.A[k];
         pos_out[k] = M.P[k];
@@ -721,13 +738,21 @@ int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int64_t m, 
     if (n <= 0) return CHORDAL_OK;
     if (n > CHORDAL_DENSE_LEXBFS_MAX_N) return CHORDAL_ETOOLARGE;
     if (n <= 1024 && tie_rule != CHORDAL_TIE_SEEDED_ARB) {
-        const size_t wsmem = size_t((n + 31) >> 5) * 32 * 2 * 4 + 256;
-        if (tie_rule == CHORDAL_TIE_DESCENDING)
-            lexbfs_warp_kernel<CHORDAL_TIE_DESCENDING><<<1, 32, wsmem, stream>>>(adj, (int)n, stride, order, pos,
-                                                                                parent);
-        else
-            lexbfs_warp_kernel<CHORDAL_TIE_ASCENDING><<<1, 32, wsmem, stream>>>(adj, (int)n, stride, order, pos,
-                                                                               parent);
+        const size_t state = (size_t((n + 31) >> 5) * 32 * 2 * 4 + 256 + 15) & ~size_t(15);
+        const size_t rows = (size_t)n * stride;
+        const bool stage = state + rows <= 200 * 1024;  // rows staged in shared memory when they fit
+        const size_t wsmem = stage ? state + rows : state;
+#define WARP_LAUNCH(M, S)                                                                                    \
+    if (cudaFuncSetAttribute(lexbfs_warp_kernel<M, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,           \
+                             (int)wsmem) != cudaSuccess)                                                      \
+        return CHORDAL_ECUDA;                                                                                 \
+    lexbfs_warp_kernel<M, S><<<1, 32, wsmem, stream>>>(adj, (int)n, stride, order, pos, parent);
+        if (tie_rule == CHORDAL_TIE_DESCENDING) {
+            if (stage) { WARP_LAUNCH(CHORDAL_TIE_DESCENDING, true) } else { WARP_LAUNCH(CHORDAL_TIE_DESCENDING, false) }
+        } else {
+            if (stage) { WARP_LAUNCH(CHORDAL_TIE_ASCENDING, true) } else { WARP_LAUNCH(CHORDAL_TIE_ASCENDING, false) }
+        }
+#undef WARP_LAUNCH
         CH_LAUNCH_CHECK();
         return CHORDAL_OK;
     }

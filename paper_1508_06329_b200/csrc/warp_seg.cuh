@@ -80,7 +80,7 @@ __device__ __forceinline__ uint32_t ld_issue(const uint32_t *p) {
 }  // namespace wseg
 
 // rows: the graph's packed rows (global), sw: row pitch in 32-bit words.
-template <int MODE, bool LATENCY = false>
+template <int MODE, bool LATENCY = false, bool SMEM_ROWS = false>
 __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n, const WarpSegMem &M) {
     using namespace wseg;
     const int l = threadIdx.x & 31;
@@ -140,7 +140,11 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
         if (x == guess) pacc[1]++;
         const long long pw0 = clock64();
 #endif
-        if (l < W) r = (x == guess) ? nxt : __ldg(rows + (long long)x * sw + l);
+        if (SMEM_ROWS) {  // rows staged in shared memory: no speculation needed
+            if (l < W) r = rows[x * sw + l];
+        } else if (l < W) {
+            r = (x == guess) ? nxt : __ldg(rows + (long long)x * sw + l);
+        }
 #ifdef WSEG_PROFILE
         {
             const uint32_t any_r = __reduce_or_sync(CH_FULL, r);
@@ -148,10 +152,12 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
             pacc[2] += clock64() - pw0;
         }
 #endif
-        guess = hpos < tail0 ? (int)M.A[hpos] : -1;
-        if (guess >= 0 && l < W) nxt = ld_issue(rows + (long long)guess * sw + l);
-        if (hpos + 1 < tail0 && l == 0)  // two steps ahead: warm L2
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(rows + (long long)M.A[hpos + 1] * sw));
+        if (!SMEM_ROWS) {
+            guess = hpos < tail0 ? (int)M.A[hpos] : -1;
+            if (guess >= 0 && l < W) nxt = ld_issue(rows + (long long)guess * sw + l);
+            if (hpos + 1 < tail0 && l == 0)  // two steps ahead: warm L2
+                asm volatile("prefetch.global.L2 [%0];" ::"l"(rows + (long long)M.A[hpos + 1] * sw));
+        }
         if (l == (x >> 5)) RAl &= ~(1u << (x & 31));
         WSEG_T(0);
         uint32_t mv = r & RAl;
@@ -227,7 +233,7 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
             // movers that fill a run of whole classes change nothing (search.py:448-453)
             const bool whole = cntA == gmx - gmn + 1 && (gmn == hpos || ((bmn >> (gmn & 31)) & 1u)) &&
                                (gmx + 1 >= tail0 || ((bmx >> ((gmx + 1) & 31)) & 1u));
-            if (!whole && gmn > hpos) {
+            if (!SMEM_ROWS && !whole && gmn > hpos) {
                 // A split of the head class [hpos, ...) brings its first mover (the
                 // smallest mover position gmn, if no class starts in (hpos, gmn])
                 // to hpos: re-aim the speculative row load at it.
