@@ -6,8 +6,9 @@
 // lane l owning 32-bit word l of every bitset, so that the per-step scans are
 // warp shuffles and the bitsets live in registers:
 //   registers  U (unreached), RA (reached unvisited), B (class starts over
-//              positions), the row word of the pivot and the speculative next
-//              row word;
+//              positions) and the row word of the pivot (rows are read from
+//              global memory in the batch, from a shared-memory copy for single
+//              graphs);
 //   shared     A / An (arrangement and its scatter buffer), P (positions),
 //              par (PEO parents), F / NB (32-word mover and new-start bitsets
 //              written with shared atomics) -- 8 * 32W + 256 bytes per graph.
@@ -20,7 +21,7 @@
 namespace chordal {
 
 #ifdef WSEG_PROFILE
-// [0] steps [1] row-guess hits [2] cycles waiting for the row [3] total cycles
+// [0] steps [1] (unused) [2] cycles waiting for the row [3] total cycles
 // [4] split steps (tools/warp_profile.cu only)
 __device__ unsigned long long wseg_prof[8];
 // per-phase cycles: [0] pivot + row [1] movers [2] newly reached + scan
@@ -69,13 +70,6 @@ __device__ __forceinline__ int excl_prefix6(int c, uint32_t lt, int &total) {
     return pre;
 }
 
-// A load that is issued where it stands (the speculative next-row load must
-// not be sunk to its use one step later).
-__device__ __forceinline__ uint32_t ld_issue(const uint32_t *p) {
-    uint32_t v;
-    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v) : "l"(p));
-    return v;
-}
 
 }  // namespace wseg
 
@@ -100,8 +94,7 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
         Bl = 1u;
     }
     __syncwarp();
-    int tail = 1, nclasses = 1, guess = -1;
-    uint32_t nxt = 0;
+    int tail = 1, nclasses = 1;
 #ifdef WSEG_PROFILE
     unsigned long long pacc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
     unsigned long long ph[8] = {0, 0, 0, 0, 0, 0, 0, 0};
@@ -133,18 +126,16 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
         const int tail0 = tail, hpos = i + 1;
         const uint32_t bh = __shfl_sync(CH_FULL, Bl, (hpos >> 5) & 31);
         if (hpos >= tail0 || ((bh >> (hpos & 31)) & 1u)) --nclasses;  // x's class was {x}
-        // ---- row of x (speculatively loaded one step ahead) -------------------
+        // ---- row of x ---------------------------------------------------------
         uint32_t r = 0;
 #ifdef WSEG_PROFILE
         pacc[0]++;
-        if (x == guess) pacc[1]++;
         const long long pw0 = clock64();
 #endif
-        if (SMEM_ROWS) {  // rows staged in shared memory: no speculation needed
-            if (l < W) r = rows[x * sw + l];
-        } else if (l < W) {
-            r = (x == guess) ? nxt : __ldg(rows + (long long)x * sw + l);
-        }
+        // The row of x: shared memory when staged (single graphs), else the
+        // read-only path.  No speculative next-row load: it cost the batch more
+        // issue slots than the latency it hid (36 graphs per SM hide it anyway).
+        if (l < W) r = SMEM_ROWS ? rows[x * sw + l] : __ldg(rows + x * sw + l);
 #ifdef WSEG_PROFILE
         {
             const uint32_t any_r = __reduce_or_sync(CH_FULL, r);
@@ -152,12 +143,6 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
             pacc[2] += clock64() - pw0;
         }
 #endif
-        if (!SMEM_ROWS) {
-            guess = hpos < tail0 ? (int)M.A[hpos] : -1;
-            if (guess >= 0 && l < W) nxt = ld_issue(rows + (long long)guess * sw + l);
-            if (hpos + 1 < tail0 && l == 0)  // two steps ahead: warm L2
-                asm volatile("prefetch.global.L2 [%0];" ::"l"(rows + (long long)M.A[hpos + 1] * sw));
-        }
         if (l == (x >> 5)) RAl &= ~(1u << (x & 31));
         WSEG_T(0);
         uint32_t mv = r & RAl;
@@ -233,19 +218,6 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
             // movers that fill a run of whole classes change nothing (search.py:448-453)
             const bool whole = cntA == gmx - gmn + 1 && (gmn == hpos || ((bmn >> (gmn & 31)) & 1u)) &&
                                (gmx + 1 >= tail0 || ((bmx >> ((gmx + 1) & 31)) & 1u));
-            if (!SMEM_ROWS && !whole && gmn > hpos) {
-                // A split of the head class [hpos, ...) brings its first mover (the
-                // smallest mover position gmn, if no class starts in (hpos, gmn])
-                // to hpos: re-aim the speculative row load at it.
-                uint32_t sb = Bl;
-                const int lo2 = hpos + 1 - 32 * l, hi2 = gmn + 1 - 32 * l;
-                sb &= lo2 <= 0 ? CH_FULL : (lo2 >= 32 ? 0u : ~mask_below(lo2));
-                sb &= hi2 <= 0 ? 0u : mask_below(min(hi2, 32));
-                if (!__any_sync(CH_FULL, sb != 0)) {
-                    guess = M.A[gmn];
-                    if (l < W) nxt = ld_issue(rows + (long long)guess * sw + l);
-                }
-            }
 #ifdef WSEG_PROFILE
             if (!whole) pacc[4]++;
 #endif
