@@ -567,6 +567,9 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
 #ifdef SEG_DOUBLE3B
             for (int rep3 = 0; rep3 < 2; ++rep3)
 #endif
+#ifdef SEG_PROFILE
+            const long long own0 = clock64();
+#endif
             for (int j0 = 4 * warp; j0 < ntouch; j0 += 4 * NW) {  // four words per round: loads overlap
                 int q[4], v[4], dst[4];
                 bool ok[4];
@@ -606,12 +609,14 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                 for (int u = 0; u < 4; ++u)
                     if (ok[u]) An[dst[u]] = (uint16_t)v[u];
             }
+#ifdef SEG_PROFILE
+            const long long own1 = clock64();
+#endif
             __syncthreads();  // B3
 #ifdef SEG_PROFILE
-            {  // 3b cycles of small (<= 64 words) and large split steps
-                const long long c3b = clock64() - seg_t0;
-                seg_acc[ntouch <= 64 ? 12 : 14] += (unsigned long long)c3b;
-                seg_acc[ntouch <= 64 ? 13 : 15] += 1;
+            {  // 3b: [12] thread 0's own loop cycles, [13] cycles waiting at B3 for the others
+                seg_acc[12] += (unsigned long long)(own1 - own0);
+                seg_acc[13] += (unsigned long long)(clock64() - own1);
             }
 #endif
             SEG_T(6);
