@@ -245,7 +245,11 @@ int chordal_is_chordal_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, 
     }
     uint8_t *w = reinterpret_cast<uint8_t *>(ws);
     uint64_t *key = reinterpret_cast<uint64_t *>(w + L.key);
-    int32_t *parent = reinterpret_cast<int32_t *>(w + L.parent);
+    // The shared-memory CTA engine would record parents with one global store per
+    // unvisited neighbour per step (~6 % of its step time at N = 32768, k = 1024);
+    // the PEO kernel finds them in a fraction of a millisecond instead.  The slot
+    // engine (n > 32768) keeps recording them.
+    int32_t *parent = use_seg(n) ? nullptr : reinterpret_cast<int32_t *>(w + L.parent);
     int rc = chordal_lexbfs_dense(adj_dev, n, stride, m, tie_rule, seed, order_dev, pos_dev, parent, ws, ws_bytes,
                                   stream);
     if (rc) return rc;

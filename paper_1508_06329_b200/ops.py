@@ -39,7 +39,7 @@ def lexbfs(rows: DeviceRows, tie_rule: int = _native.TIE_ASCENDING, seed: int = 
         ws = _ws(torch, lib.chordal_dense_workspace_bytes(n, mm), dev)
         check(
             lib.chordal_lexbfs_dense(rows.ptr, n, rows.stride, mm, tie_rule, seed & U64_MAX, ptr(order), ptr(pos),
-                                     ptr(parent), ptr(ws), ws.numel(), stream_ptr(stream)),
+                                     ptr(parent) if want_parent else None, ptr(ws), ws.numel(), stream_ptr(stream)),
             "chordal_lexbfs_dense",
         )
     if want_parent:
