@@ -537,11 +537,25 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                 return T > 0 && T < e - s;
             };
             // ---- phase 3a: list the words of split classes ------------------------
+            // Split classes hold movers, so they lie inside [span_s, span_e): from
+            // the start of the class of the first mover to the end of the class
+            // of the last one; words outside are never rewritten.
+            int span_s, span_e;
+            {
+                const int qn = gmn >> 5, qx = (gmx + 1) >> 5;
+                const uint32_t bn = breg(qn) & mask_below((gmn & 31) + 1);
+                span_s = bn ? 32 * qn + highest_bit(bn) : (int)LB[qn];
+                span_e = tail0;
+                if (gmx + 1 < tail0) {
+                    const uint32_t bx = qx < W ? breg(qx) & ~mask_below((gmx + 1) & 31) : 0u;
+                    span_e = bx ? 32 * qx + __ffs(bx) - 1 : min((int)NBq[qx], tail0);
+                }
+            }
             if (own) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const int q = w0 + k;
-                    const int lo = max(32 * q, hpos), hi = min(32 * q + 32, tail0);
+                    const int lo = max(32 * q, max(hpos, span_s)), hi = min(32 * q + 32, min(tail0, span_e));
                     if (lo >= hi) continue;
                     const int lob = lo - 32 * q, hib = hi - 32 * q;
                     const uint32_t vm = mask_below(hib) & ~mask_below(lob);
@@ -564,9 +578,6 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
             seg_acc[10] += cntA;
 #endif
             // ---- phase 3b: stable partition of split classes into An --------------
-#ifdef SEG_DOUBLE3B
-            for (int rep3 = 0; rep3 < 2; ++rep3)
-#endif
 #ifdef SEG_PROFILE
             const long long own0 = clock64();
 #endif
@@ -595,11 +606,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                         const uint32_t fq = F[q[u]];
                         const int fb = (int)Pc[q[u]] + __popc(fq & mask_below(lane)) - cs;
                         dst[u] = ((fq >> lane) & 1u) ? s + fb : s + T + (p - s - fb);
-                        if (p == s
-#ifdef SEG_DOUBLE3B
-                            && rep3 == 0
-#endif
-                        ) {
+                        if (p == s) {
                             atomicOr(&NB[(s + T) >> 5], 1u << ((s + T) & 31));
                             atomicAdd(fl + 5, 1);
                         }
