@@ -562,14 +562,22 @@ def run_ours(args, rank, world, local):
     orders_h = torch.empty((B, N512), dtype=torch.int32, pin_memory=True)
     wit_h = torch.empty((B, 3), dtype=torch.int32, pin_memory=True)
 
-    def e2e_step():
-        rc = _native.lib.chordal_is_chordal_batch_host(host.data_ptr(), B, N512, STRIDE512, orders_h.data_ptr(),
-                                                       wit_h.data_ptr(), 8192)
-        _native.check(rc, "chordal_is_chordal_batch_host")
+    # the public host-buffer API in its repeated-call form: a device workspace
+    # allocated once (like a cuDNN/cuBLAS workspace), reused by every call
+    wsb = int(_native.lib.chordal_batch_host_workspace_bytes(N512, 8192))
+    e2e_ws = torch.empty(wsb + 256, dtype=torch.uint8, device=device)
+    ws_ptr = (e2e_ws.data_ptr() + 255) & ~255
 
-    for _ in range(max(3, args.warmup)):  # first calls map the staging buffers
+    def e2e_step():
+        rc = _native.lib.chordal_is_chordal_batch_host_ws(host.data_ptr(), B, N512, STRIDE512, orders_h.data_ptr(),
+                                                          wit_h.data_ptr(), 8192, ws_ptr, wsb)
+        _native.check(rc, "chordal_is_chordal_batch_host_ws")
+
+    # first calls map the staging buffers and fault in the pinned pages (the first
+    # few calls on a fresh box can take 10x longer)
+    for _ in range(max(6, args.warmup)):
         e2e_step()
-    e2e_steps = max(2, min(args.steps, 5))
+    e2e_steps = max(3, min(args.steps, 10))
     barrier(world)
     t0 = time.perf_counter()
     call_ms = []
@@ -633,7 +641,7 @@ def run_ours(args, rank, world, local):
                      "algorithmic_bytes_per_graph": BYTES_PER_GRAPH},
         "roofline_issue": issue,
         "e2e": {"value": e2e_value, "unit": "graphs/s", "h2d_bytes_per_step": B * N512 * STRIDE512,
-                "d2h_bytes_per_step": B * (4 * N512 + 12), "api": "chordal_is_chordal_batch_host",
+                "d2h_bytes_per_step": B * (4 * N512 + 12), "api": "chordal_is_chordal_batch_host_ws",
                 "calls_ms": call_ms,
                 "link": {"bound": "pcie_h2d", "achieved_gbs": h2d_gbs, "peak_gbs": link_best,
                          "peak_kind": "measured pinned H2D copy, 512 MiB, best of 3", "frac": h2d_gbs / link_best}},

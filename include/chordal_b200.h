@@ -203,6 +203,15 @@ int chordal_is_chordal_batch(const uint8_t *adj_dev, int64_t batch, int64_t n, i
 int chordal_is_chordal_batch_host(const uint8_t *adj_host, int64_t batch, int64_t n, int64_t row_bytes,
                                   int32_t *orders_host, int32_t *witness_host, int64_t chunk);
 
+/* The same with a caller-provided device workspace of
+ * chordal_batch_host_workspace_bytes(n, chunk) bytes (256-byte aligned), reused
+ * across calls: the form to call repeatedly.  (Each call of the form above
+ * takes and returns a ~1 GB pool block, which costs some calls 10-600 ms.) */
+size_t chordal_batch_host_workspace_bytes(int64_t n, int64_t chunk);
+int chordal_is_chordal_batch_host_ws(const uint8_t *adj_host, int64_t batch, int64_t n, int64_t row_bytes,
+                                     int32_t *orders_host, int32_t *witness_host, int64_t chunk, void *ws_dev,
+                                     size_t ws_bytes);
+
 /* ---- synthetic inputs --------------------------------------------------- */
 
 /* gen_dense_random (generate.py:32-56) bit for bit: Philox4x64-10 keyed by

@@ -44,6 +44,8 @@ SIGNATURES = {
     "chordal_permute_dense": [_P, _I64, _I64, _P, _P, _P],
     "chordal_is_chordal_batch": [_P, _I64, _I64, _I64, _P, _P, _P],
     "chordal_is_chordal_batch_host": [_P, _I64, _I64, _I64, _P, _P, _I64],
+    "chordal_batch_host_workspace_bytes": [_I64, _I64],
+    "chordal_is_chordal_batch_host_ws": [_P, _I64, _I64, _I64, _P, _P, _I64, _P, _SZ],
     "chordal_gen_dense_random": [_P, _I64, _I64, _I64, _D, _I64, _I64, _P],
     "chordal_edges_to_dense": [_P, _P, _I64, _P, _I64, _I64, _P],
     "chordal_gen_chordal_random_scratch_bytes": [_I64, _I64, _I64],
@@ -64,6 +66,7 @@ _RESTYPES = {
     "chordal_lexbfs_csr_workspace_bytes": _SZ,
     "chordal_write_graph_text": _I64,
     "chordal_bfs_csr_workspace_bytes": _SZ,
+    "chordal_batch_host_workspace_bytes": _SZ,
 }
 
 if not os.path.exists(LIB_PATH):

@@ -430,31 +430,45 @@ int chordal_is_chordal_batch(const uint8_t *adj_dev, int64_t batch, int64_t n, i
     return launch_batch(adj_dev, batch, n, stride, orders_dev, witness_dev, as_stream(stream));
 }
 
-int chordal_is_chordal_batch_host(const uint8_t *adj_host, int64_t batch, int64_t n, int64_t row_bytes,
-                                  int32_t *orders_host, int32_t *witness_host, int64_t chunk) {
-    if (batch < 0 || n < 0 || (batch > 0 && n > 0 && (!adj_host || !orders_host || !witness_host)))
-        return CHORDAL_EINVAL;
-    if (batch == 0 || n == 0) return CHORDAL_OK;
-    if (n > CHORDAL_BATCH_MAX_N) return CHORDAL_ETOOLARGE;
-    if (row_bytes < (n + 7) / 8) return CHORDAL_EINVAL;
+static size_t batch_host_set_bytes(int64_t n, int64_t chunk) {
+    const int64_t stride = (((n + 7) / 8) + 15) / 16 * 16;
+    return ((size_t)n * stride * chunk + sizeof(int32_t) * (size_t)(n + 3) * chunk + 1023) & ~size_t(255);
+}
+
+size_t chordal_batch_host_workspace_bytes(int64_t n, int64_t chunk) {
+    if (n <= 0) return 0;
     if (chunk <= 0) chunk = 4096;
-    if (chunk > batch) chunk = batch;
+    return 3 * batch_host_set_bytes(n, chunk);
+}
+
+// The host-buffer batch over a caller-provided device block (three chunk-sized
+// sets: graphs, orders, witnesses) and three per-call streams.
+static int batch_host_run(const uint8_t *adj_host, int64_t batch, int64_t n, int64_t row_bytes, int32_t *orders_host,
+                          int32_t *witness_host, int64_t chunk, uint8_t *block, cudaStream_t home) {
     const int64_t stride = (((n + 7) / 8) + 15) / 16 * 16;
     const size_t gbytes = (size_t)n * stride;
     constexpr int NB = 3;  // H2D of chunk c+1 and D2H of c-1 overlap the search of c
-    keep_pool_bytes(NB * (gbytes * chunk + sizeof(int32_t) * (n + 3) * chunk));
+    const size_t per_set = batch_host_set_bytes(n, chunk);
+    cudaEvent_t ready = nullptr;
     cudaStream_t st[NB] = {};
     uint8_t *buf[NB] = {};
     int32_t *ord[NB] = {};
     int32_t *wit[NB] = {};
     int rc = CHORDAL_OK;
+    if (cudaEventCreateWithFlags(&ready, cudaEventDisableTiming) != cudaSuccess ||
+        cudaEventRecord(ready, home) != cudaSuccess)
+        rc = CHORDAL_ECUDA;
     for (int k = 0; k < NB && rc == CHORDAL_OK; ++k) {
-        if (cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking) != cudaSuccess) { rc = CHORDAL_ECUDA; break; }
-        if (cudaMallocAsync((void **)&buf[k], gbytes * chunk, st[k]) != cudaSuccess ||
-            cudaMallocAsync((void **)&ord[k], sizeof(int32_t) * n * chunk, st[k]) != cudaSuccess ||
-            cudaMallocAsync((void **)&wit[k], sizeof(int32_t) * 3 * chunk, st[k]) != cudaSuccess)
-            rc = CHORDAL_ENOMEM;
-        else if (stride != row_bytes && cudaMemsetAsync(buf[k], 0, gbytes * chunk, st[k]) != cudaSuccess)
+        uint8_t *base = block + k * per_set;
+        buf[k] = base;
+        ord[k] = reinterpret_cast<int32_t *>(base + ((gbytes * chunk + 255) & ~size_t(255)));
+        wit[k] = ord[k] + (size_t)n * chunk;
+        if (cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking) != cudaSuccess ||
+            cudaStreamWaitEvent(st[k], ready, 0) != cudaSuccess) {
+            rc = CHORDAL_ECUDA;
+            break;
+        }
+        if (stride != row_bytes && cudaMemsetAsync(buf[k], 0, gbytes * chunk, st[k]) != cudaSuccess)
             rc = CHORDAL_ECUDA;
     }
     for (int64_t b0 = 0, c = 0; b0 < batch && rc == CHORDAL_OK; b0 += chunk, ++c) {
@@ -476,13 +490,55 @@ int chordal_is_chordal_batch_host(const uint8_t *adj_host, int64_t batch, int64_
     }
     for (int k = 0; k < NB; ++k) {
         if (!st[k]) continue;
-        if (buf[k]) cudaFreeAsync(buf[k], st[k]);
-        if (ord[k]) cudaFreeAsync(ord[k], st[k]);
-        if (wit[k]) cudaFreeAsync(wit[k], st[k]);
         if (cudaStreamSynchronize(st[k]) != cudaSuccess && rc == CHORDAL_OK) rc = CHORDAL_ECUDA;
         cudaStreamDestroy(st[k]);
     }
+    if (ready) cudaEventDestroy(ready);
     return rc;
+}
+
+static int batch_host_check(const uint8_t *adj_host, int64_t batch, int64_t n, int64_t row_bytes,
+                            int32_t *orders_host, int32_t *witness_host) {
+    if (batch < 0 || n < 0 || (batch > 0 && n > 0 && (!adj_host || !orders_host || !witness_host)))
+        return CHORDAL_EINVAL;
+    if (batch == 0 || n == 0) return -1;  // nothing to do
+    if (n > CHORDAL_BATCH_MAX_N) return CHORDAL_ETOOLARGE;
+    if (row_bytes < (n + 7) / 8) return CHORDAL_EINVAL;
+    return CHORDAL_OK;
+}
+
+int chordal_is_chordal_batch_host(const uint8_t *adj_host, int64_t batch, int64_t n, int64_t row_bytes,
+                                  int32_t *orders_host, int32_t *witness_host, int64_t chunk) {
+    int rc = batch_host_check(adj_host, batch, n, row_bytes, orders_host, witness_host);
+    if (rc) return rc < 0 ? CHORDAL_OK : rc;
+    if (chunk <= 0) chunk = 4096;
+    if (chunk > batch) chunk = batch;
+    // one stream-ordered block per call on the calling thread's default stream
+    // (see chordal_is_chordal_batch_host_ws for the jitter-free form)
+    const size_t wsb = chordal_batch_host_workspace_bytes(n, chunk);
+    keep_pool_bytes(wsb);
+    cudaStream_t home = cudaStreamPerThread;
+    uint8_t *block = nullptr;
+    if (cudaMallocAsync((void **)&block, wsb, home) != cudaSuccess) return CHORDAL_ENOMEM;
+    rc = batch_host_run(adj_host, batch, n, row_bytes, orders_host, witness_host, chunk, block, home);
+    cudaFreeAsync(block, home);
+    if (cudaStreamSynchronize(home) != cudaSuccess && rc == CHORDAL_OK) rc = CHORDAL_ECUDA;
+    return rc;
+}
+
+int chordal_is_chordal_batch_host_ws(const uint8_t *adj_host, int64_t batch, int64_t n, int64_t row_bytes,
+                                     int32_t *orders_host, int32_t *witness_host, int64_t chunk, void *ws_dev,
+                                     size_t ws_bytes) {
+    int rc = batch_host_check(adj_host, batch, n, row_bytes, orders_host, witness_host);
+    if (rc) return rc < 0 ? CHORDAL_OK : rc;
+    if (chunk <= 0) chunk = 4096;
+    if (chunk > batch) chunk = batch;
+    if (!ws_dev || ws_bytes < chordal_batch_host_workspace_bytes(n, chunk) ||
+        (reinterpret_cast<uintptr_t>(ws_dev) & 255))
+        return CHORDAL_EINVAL;
+    cudaStream_t home = cudaStreamPerThread;
+    return batch_host_run(adj_host, batch, n, row_bytes, orders_host, witness_host, chunk,
+                          reinterpret_cast<uint8_t *>(ws_dev), home);
 }
 
 int chordal_gen_dense_random(uint8_t *adj_dev, int64_t batch, int64_t n, int64_t stride, double p,

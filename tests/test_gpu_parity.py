@@ -302,6 +302,18 @@ def test_host_buffer_batch_entry_point():
     assert _native.lib.chordal_is_chordal_batch_host(h2.ctypes.data, 5, 100, 13, o2.ctypes.data, w2.ctypes.data, 2) == 0
     v3, o3, w3 = oracle.is_chordal_batch(h2, 100)
     assert (o2 == o3).all() and (w2 == w3).all()
+    # the workspace form (repeated calls): same results, workspace reused
+    wsb = int(_native.lib.chordal_batch_host_workspace_bytes(512, 7))
+    ws = torch.empty(wsb + 256, dtype=torch.uint8, device="cuda")
+    wp = (ws.data_ptr() + 255) & ~255
+    for _ in range(2):
+        o4 = np.empty((40, 512), dtype=np.int32)
+        w4 = np.empty((40, 3), dtype=np.int32)
+        assert _native.lib.chordal_is_chordal_batch_host_ws(host.ctypes.data, 40, 512, 64, o4.ctypes.data,
+                                                            w4.ctypes.data, 7, wp, wsb) == 0
+        assert (o4 == o).all() and (w4 == w).all()
+    assert _native.lib.chordal_is_chordal_batch_host_ws(host.ctypes.data, 40, 512, 64, o4.ctypes.data,
+                                                        w4.ctypes.data, 7, wp, wsb - 1) == _native.EINVAL
     torch.cuda.synchronize()
 
 
