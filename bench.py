@@ -261,9 +261,16 @@ def single_graph_lines(with_cpu: bool) -> dict:
             wit_h = np.empty(3, dtype=np.int32)
             flag = ctypes.c_int32()
 
+            m_ = int(rows.m)
+            wsb = int(_native.lib.chordal_dense_host_workspace_bytes(n, m_))
+            ws_t = torch.empty(wsb + 256, dtype=torch.uint8, device="cuda")
+            wp = (ws_t.data_ptr() + 255) & ~255
+
             def e2e():
-                _native.lib.chordal_is_chordal_dense_host(hp.ctypes.data, n, hp.shape[1], 0, 0, order_h.ctypes.data,
-                                                          wit_h.ctypes.data, ctypes.byref(flag))
+                rc = _native.lib.chordal_is_chordal_dense_host_ws(hp.ctypes.data, n, hp.shape[1], m_, 0, 0,
+                                                                  order_h.ctypes.data, wit_h.ctypes.data,
+                                                                  ctypes.byref(flag), wp, wsb)
+                _native.check(rc, "chordal_is_chordal_dense_host_ws")
 
             e2e()
             t0 = time.perf_counter()

@@ -170,6 +170,14 @@ int chordal_peo_csr_witness(const int64_t *indptr_dev, const int32_t *indices_de
 int chordal_peo_csr(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, const int32_t *pos_dev,
                     const int32_t *parent_dev, uint64_t *key_dev, int32_t *witness_dev, void *stream);
 
+/* The host-buffer pipeline over a caller-provided device workspace of
+ * chordal_dense_host_workspace_bytes(n, m) bytes (256-byte aligned; m = the edge
+ * count, Graph.m), reused across calls, on the calling thread's default stream. */
+size_t chordal_dense_host_workspace_bytes(int64_t n, int64_t m);
+int chordal_is_chordal_dense_host_ws(const uint8_t *adj_host, int64_t n, int64_t row_bytes, int64_t m,
+                                     int32_t tie_rule, uint64_t seed, int32_t *order_host, int32_t *witness_host,
+                                     int32_t *chordal_out, void *ws_dev, size_t ws_bytes);
+
 /* Packed rows -> CSR (ascending rows).  indptr_dev[n+1] is always written;
  * indices_dev (capacity indptr[n]) is filled when not NULL, so a caller can
  * size it from indptr[n] first. */

@@ -35,6 +35,8 @@ SIGNATURES = {
     "chordal_peo_dense": [_P, _I64, _I64, _P, _P, _P, _P, _P, _P],
     "chordal_is_chordal_dense": [_P, _I64, _I64, _I64, _I32, _U64, _P, _P, _P, _SZ, _P, _P],
     "chordal_is_chordal_dense_host": [_P, _I64, _I64, _I32, _U64, _P, _P, _P],
+    "chordal_dense_host_workspace_bytes": [_I64, _I64],
+    "chordal_is_chordal_dense_host_ws": [_P, _I64, _I64, _I64, _I32, _U64, _P, _P, _P, _P, _SZ],
     "chordal_lexbfs_csr_workspace_bytes": [_I64, _I64],
     "chordal_lexbfs_csr": [_P, _P, _I64, _I64, _I32, _U64, _P, _P, _P, _P, _SZ, _P],
     "chordal_peo_csr_key": [_P, _P, _I64, _P, _P, _I64, _I64, _P, _P],
@@ -67,6 +69,7 @@ _RESTYPES = {
     "chordal_write_graph_text": _I64,
     "chordal_bfs_csr_workspace_bytes": _SZ,
     "chordal_batch_host_workspace_bytes": _SZ,
+    "chordal_dense_host_workspace_bytes": _SZ,
 }
 
 if not os.path.exists(LIB_PATH):

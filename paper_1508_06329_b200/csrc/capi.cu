@@ -309,6 +309,53 @@ int chordal_is_chordal_dense_host(const uint8_t *adj_host, int64_t n, int64_t ro
     return rc;
 }
 
+size_t chordal_dense_host_workspace_bytes(int64_t n, int64_t m) {
+    if (n <= 0) return 0;
+    const int64_t stride = (((n + 7) / 8) + 15) / 16 * 16;
+    const size_t adj_bytes = ((size_t)n * stride + 255) & ~size_t(255);
+    const size_t ord_bytes = (sizeof(int32_t) * (size_t)(2 * n + 4) + 255) & ~size_t(255);
+    return adj_bytes + ord_bytes + ((DenseWs(n, m < 0 ? 0 : m).total + 255) & ~size_t(255)) + 256;
+}
+
+int chordal_is_chordal_dense_host_ws(const uint8_t *adj_host, int64_t n, int64_t row_bytes, int64_t m,
+                                     int32_t tie_rule, uint64_t seed, int32_t *order_host, int32_t *witness_host,
+                                     int32_t *chordal_out, void *ws_dev, size_t ws_bytes) {
+    if (n < 0 || m < 0 || !witness_host || !chordal_out || (n > 0 && (!adj_host || !order_host)))
+        return CHORDAL_EINVAL;
+    if (n > 0 && row_bytes < (n + 7) / 8) return CHORDAL_EINVAL;
+    if (n == 0) {
+        witness_host[0] = witness_host[1] = witness_host[2] = -1;
+        *chordal_out = 1;
+        return CHORDAL_OK;
+    }
+    if (!ws_dev || ws_bytes < chordal_dense_host_workspace_bytes(n, m) ||
+        (reinterpret_cast<uintptr_t>(ws_dev) & 255))
+        return CHORDAL_EINVAL;
+    const int64_t stride = (((n + 7) / 8) + 15) / 16 * 16;
+    const size_t adj_bytes = ((size_t)n * stride + 255) & ~size_t(255);
+    const size_t ord_bytes = (sizeof(int32_t) * (size_t)(2 * n + 4) + 255) & ~size_t(255);
+    const size_t wsb = (DenseWs(n, m).total + 255) & ~size_t(255);
+    uint8_t *adj = reinterpret_cast<uint8_t *>(ws_dev);
+    int32_t *order = reinterpret_cast<int32_t *>(adj + adj_bytes);
+    uint8_t *ws = adj + adj_bytes + ord_bytes;
+    int32_t *wit = reinterpret_cast<int32_t *>(ws + wsb);
+    cudaStream_t s = cudaStreamPerThread;
+    int rc = CHORDAL_OK;
+    do {
+        if (stride != row_bytes && cudaMemsetAsync(adj, 0, adj_bytes, s) != cudaSuccess) { rc = CHORDAL_ECUDA; break; }
+        if (cudaMemcpy2DAsync(adj, stride, adj_host, row_bytes, (n + 7) / 8, n, cudaMemcpyHostToDevice, s) !=
+            cudaSuccess) { rc = CHORDAL_ECUDA; break; }
+        rc = chordal_is_chordal_dense(adj, n, stride, m, tie_rule, seed, order, order + n, ws, wsb, wit, s);
+        if (rc) break;
+        if (cudaMemcpyAsync(order_host, order, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+            cudaMemcpyAsync(witness_host, wit, sizeof(int32_t) * 3, cudaMemcpyDeviceToHost, s) != cudaSuccess)
+            rc = CHORDAL_ECUDA;
+    } while (0);
+    if (cudaStreamSynchronize(s) != cudaSuccess && rc == CHORDAL_OK) rc = CHORDAL_ECUDA;
+    if (rc == CHORDAL_OK) *chordal_out = witness_host[0] < 0 ? 1 : 0;
+    return rc;
+}
+
 // ---- CSR -------------------------------------------------------------------
 
 size_t chordal_lexbfs_csr_workspace_bytes(int64_t n, int64_t m) {

@@ -333,6 +333,32 @@ def test_host_buffer_entry_point():
         assert (wit.tolist() if not ok else None) == (None if w is None else list(w))
 
 
+def test_host_buffer_workspace_entry_point():
+    """chordal_is_chordal_dense_host_ws: one workspace reused across graphs of the
+    three engine ranges (warp n <= 1024, CTA n <= 32768, CSR beyond)."""
+    import torch
+
+    graphs = [gen_chordal_random(1000, 8, 0), remove_first_chord(gen_chordal_random(1000, 8, 0))[0],
+              gen_chordal_random(3000, 20, 2), gen_dense_random(2500, 0.4, 3),
+              gen_chordal_random(33000, 3, 4, cap=33000)]
+    big = max(int(_native.lib.chordal_dense_host_workspace_bytes(g.n, g.m)) for g in graphs)
+    ws = torch.empty(big + 256, dtype=torch.uint8, device="cuda")
+    wp = (ws.data_ptr() + 255) & ~255
+    for g in graphs:
+        n = g.n
+        order = np.empty(n, dtype=np.int32)
+        wit = np.empty(3, dtype=np.int32)
+        chordal = ctypes.c_int32(-1)
+        packed = np.ascontiguousarray(g._packed)
+        rc = _native.lib.chordal_is_chordal_dense_host_ws(packed.ctypes.data, n, packed.shape[1], g.m, 0, 0,
+                                                          order.ctypes.data, wit.ctypes.data, ctypes.byref(chordal),
+                                                          wp, big)
+        assert rc == 0
+        ok, o, w = oracle.is_chordal(packed, n)
+        assert bool(chordal.value) == ok and order.tolist() == o.tolist(), n
+        assert (wit.tolist() if not ok else None) == (None if w is None else list(w)), n
+
+
 def test_reference_graph_objects_are_accepted():
     """Any object with n and _packed (e.g. a chordalkit.Graph) is a valid input."""
 
