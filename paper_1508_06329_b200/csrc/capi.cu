@@ -43,6 +43,16 @@ int launch_gen_chordal_edges(int64_t, int64_t, int64_t, uint32_t, int32_t *, int
                              cudaStream_t);
 int launch_gen_chordal_random(uint8_t *, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, uint32_t, int32_t *,
                               cudaStream_t);
+void keep_pool_bytes(size_t bytes) {
+    int dev = 0;
+    cudaMemPool_t pool;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
+    uint64_t cur = 0;
+    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &cur) != cudaSuccess) return;
+    uint64_t want = bytes;
+    if (cur < want) cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &want);
+}
+
 }  // namespace chordal
 
 using namespace chordal;
@@ -66,15 +76,6 @@ inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s
 // (0) every call would hand the memory back to the driver and map it again on
 // the next call (tens of ms for the batch staging buffers); raising the
 // threshold to the bytes one call needs keeps them cached.  Only ever raised.
-void keep_pool_bytes(size_t bytes) {
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
-    uint64_t cur = 0;
-    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &cur) != cudaSuccess) return;
-    uint64_t want = bytes;
-    if (cur < want) cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &want);
-}
 
 int check_dense(const void *adj, int64_t n, int64_t stride) {
     if (n < 0) return CHORDAL_EINVAL;

@@ -11,6 +11,8 @@
 
 namespace chordal {
 
+void keep_pool_bytes(size_t bytes);  // capi.cu
+
 namespace {
 
 // Workspace carve-up (bytes) of the slot engine's global-memory state: isz /
@@ -464,6 +466,7 @@ int launch_peo_csr_key(const int64_t *indptr, const int32_t *indices, int64_t n,
     CH_LAUNCH_CHECK();
     // heavy rows (stream-ordered scratch for their list)
     PeoHeavy *H = nullptr;
+    keep_pool_bytes(sizeof(PeoHeavy));  // keep the block mapped between calls (unmap/remap costs ms)
     if (cudaMallocAsync(reinterpret_cast<void **>(&H), sizeof(PeoHeavy), stream) != cudaSuccess) return CHORDAL_ENOMEM;
     cudaMemsetAsync(H, 0, sizeof(int) * 2, stream);
     long long cb = (v_end - v_begin + 255) / 256;
