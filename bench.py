@@ -199,6 +199,12 @@ def cpu_batch_baseline(adj_host: np.ndarray, budget_s: float = 15.0) -> dict:
 # --------------------------------------------------------------- secondary --
 
 
+# ~10 ms of device spin queued ahead of a timed region, so that a kernel time is
+# not stretched by the host's own call overhead (ctypes, argument checks) or by
+# host scheduling noise on the box; it ends before the start event fires.
+SPIN_CYCLES = 20_000_000
+
+
 def time_events(fn, reps: int = 3, warm: int = 1) -> float:
     import torch
 
@@ -206,6 +212,7 @@ def time_events(fn, reps: int = 3, warm: int = 1) -> float:
         fn()
     torch.cuda.synchronize()
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda._sleep(SPIN_CYCLES)  # device busy while the host enqueues: no launch gaps inside s..e
     s.record()
     for _ in range(reps):
         fn()
@@ -425,6 +432,7 @@ def row_sharded_lines(rank: int, world: int, reps: int = 5) -> dict:
             torch.cuda.synchronize()
             a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ka, kb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda._sleep(SPIN_CYCLES)
             a.record()
             bcast(order)
             bcast(parent)

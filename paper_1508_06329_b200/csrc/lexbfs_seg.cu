@@ -63,7 +63,7 @@ __device__ unsigned long long seg_prof[16];
 namespace {
 
 constexpr int kSegBig = 0x7FFFFFFF;
-constexpr int kSegDenseDeg = 64;  // average degree from which the kernel runs 512 threads
+constexpr int kSegDenseFrac = 8;  // edge density (2m / n^2) from which the kernel runs 512 threads: 1 / 8
 
 struct SegLayout {
     size_t A, An, P, U, RA, F, NB, bnd, Pc, LB, NBq, TW, wt, misc, total;
@@ -364,9 +364,6 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
         const int guess_prev = guess;
 #endif
         guess = hpos < tail0 ? (int)A[hpos] : -1;
-        if (guess >= 0 && own) nxt = ld_nc_v4(rows + (long long)guess * sw + w0);
-        if (hpos + 1 < tail0 && own && (t & 7) == 0)  // one step further ahead: warm L2
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(rows + (long long)A[hpos + 1] * sw + w0));
         if (own) {
             if ((x >> 7) == t) RA[x >> 5] &= ~(1u << (x & 31));
             const uint4 ra4 = *reinterpret_cast<const uint4 *>(RA + w0);
@@ -418,6 +415,14 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                 fl[0] = 1;
             }
         }
+#ifdef SEG_PROFILE
+        if (cnt) atomicMax(fl + 7, cnt);  // [14]: most movers handled by one thread
+#endif
+        // The next pivot's row, issued only now: issued before the mover loop
+        // (into the registers the current row just left) it stalled that loop
+        // (c3 chordal 90.5 -> 86.5 ms); an extra L2 prefetch of the row after
+        // it no longer pays once the load sits here.
+        if (guess >= 0 && own) nxt = ld_nc_v4(rows + (long long)guess * sw + w0);
         {  // mover count and position range: one shared atomic per warp
             const int wc = __reduce_add_sync(CH_FULL, cnt);
             if (wc) {
@@ -435,6 +440,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
         SEG_T(2);
 #ifdef SEG_PROFILE
         if (x == guess_prev) seg_acc[8]++;
+        seg_acc[14] += fl[7];
 #endif
         const bool anyE = fl[0] != 0;
         const int cntA = fl[1];
@@ -526,16 +532,6 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                     if (own) nxt = ld_nc_v4(rows + (long long)g * sw + w0);
                 }
             }
-            // movers at positions < pp
-            auto cntb = [&](int pp) -> int {
-                const int q = pp >> 5;
-                if (q >= W) return ta;
-                return (int)Pc[q] + __popc(F[q] & mask_below(pp & 31));
-            };
-            auto is_split = [&](int s, int e) -> bool {
-                const int T = cntb(e) - cntb(s);
-                return T > 0 && T < e - s;
-            };
             // ---- phase 3a: list the words of split classes ------------------------
             // Split classes hold movers, so they lie inside [span_s, span_e): from
             // the start of the class of the first mover to the end of the class
@@ -551,6 +547,16 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                     span_e = bx ? 32 * qx + __ffs(bx) - 1 : min((int)NBq[qx], tail0);
                 }
             }
+            // movers at positions < pp
+            auto cntb = [&](int pp) -> int {
+                const int q = pp >> 5;
+                if (q >= W) return ta;
+                return (int)Pc[q] + __popc(F[q] & mask_below(pp & 31));
+            };
+            auto is_split = [&](int s, int e) -> bool {
+                const int T = cntb(e) - cntb(s);
+                return T > 0 && T < e - s;
+            };
             if (own) {
 #pragma unroll
                 for (int k = 0; k < 4; ++k) {
@@ -581,35 +587,60 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
 #ifdef SEG_PROFILE
             const long long own0 = clock64();
 #endif
-            for (int j0 = 4 * warp; j0 < ntouch; j0 += 4 * NW) {  // four words per round: loads overlap
-                int q[4], v[4], dst[4];
+            // Branch-free and staged: every round issues its shared-memory loads in
+            // three waves (word data; class bounds; mover counts at the bounds)
+            // for all four words at once -- written with data-dependent branches
+            // the compiler serialised the words, ~2000 cycles per round.
+            for (int j0 = 4 * warp; j0 < ntouch; j0 += 4 * NW) {
+#ifdef SEG_PROFILE
+                seg_acc[15]++;  // 3b rounds of this warp
+#endif
+                int q[4], p[4], v[4], lbw[4], nbw[4], pcw[4];
+                uint32_t bw[4], fw[4];
                 bool ok[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    q[u] = j0 + u < ntouch ? (int)TW[j0 + u] : 0;
-                    const int p = 32 * q[u] + lane;
-                    ok[u] = j0 + u < ntouch && p >= hpos && p < tail0;
-                    v[u] = A[p];
-                    dst[u] = p;
-                }
+                for (int u = 0; u < 4; ++u) q[u] = (int)TW[j0 + u < ntouch ? j0 + u : j0];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                    const int p = 32 * q[u] + lane;
-                    const uint32_t bq = breg(q[u]);
-                    const uint32_t bl = bq & mask_below(lane + 1);
-                    const int s = bl ? 32 * q[u] + highest_bit(bl) : (int)LB[q[u]];
-                    const uint32_t above = bq & ~mask_below(lane + 1);
-                    const int e = above ? 32 * q[u] + __ffs(above) - 1 : (int)NBq[q[u]];
-                    const int cs = cntb(s);
-                    const int T = cntb(e) - cs;
-                    if (ok[u] && T > 0 && T < e - s) {
-                        const uint32_t fq = F[q[u]];
-                        const int fb = (int)Pc[q[u]] + __popc(fq & mask_below(lane)) - cs;
-                        dst[u] = ((fq >> lane) & 1u) ? s + fb : s + T + (p - s - fb);
-                        if (p == s) {
-                            atomicOr(&NB[(s + T) >> 5], 1u << ((s + T) & 31));
-                            atomicAdd(fl + 5, 1);
-                        }
+                    p[u] = 32 * q[u] + lane;
+                    ok[u] = j0 + u < ntouch && p[u] >= hpos && p[u] < tail0;
+                    v[u] = A[p[u]];
+                    bw[u] = bnd[q[u]];
+                    lbw[u] = LB[q[u]];
+                    nbw[u] = NBq[q[u]];
+                    fw[u] = F[q[u]];
+                    pcw[u] = Pc[q[u]];
+                }
+                int s[4], e[4], ps[4], pe[4];
+                uint32_t fs[4], fe[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    uint32_t b = bw[u];
+                    const int lo = hpos - 32 * q[u];
+                    b = lo <= 0 ? b : (lo >= 32 ? 0u : (b & ~mask_below(lo)));
+                    b = (lo >= 0 && lo < 32) ? (b | (1u << lo)) : b;
+                    const uint32_t bl = b & mask_below(lane + 1), above = b & ~mask_below(lane + 1);
+                    s[u] = bl ? 32 * q[u] + highest_bit(bl) : lbw[u];
+                    e[u] = above ? 32 * q[u] + __ffs(above) - 1 : nbw[u];
+                    const int qs = min(s[u] >> 5, W - 1), qe = min(e[u] >> 5, W - 1);
+                    ps[u] = Pc[qs];
+                    fs[u] = F[qs];
+                    pe[u] = Pc[qe];
+                    fe[u] = F[qe];
+                }
+                int dst[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int cs = (s[u] >> 5) >= W ? ta : ps[u] + __popc(fs[u] & mask_below(s[u] & 31));
+                    const int ce = (e[u] >> 5) >= W ? ta : pe[u] + __popc(fe[u] & mask_below(e[u] & 31));
+                    const int T = ce - cs;
+                    const bool split = ok[u] && T > 0 && T < e[u] - s[u];
+                    const int fb = pcw[u] + __popc(fw[u] & mask_below(lane)) - cs;
+                    const int to = ((fw[u] >> lane) & 1u) ? s[u] + fb : s[u] + T + (p[u] - s[u] - fb);
+                    dst[u] = split ? to : p[u];
+                    if (split && p[u] == s[u]) {
+                        atomicOr(&NB[(s[u] + T) >> 5], 1u << ((s[u] + T) & 31));
+                        atomicAdd(fl + 5, 1);
                     }
                 }
 #pragma unroll
@@ -769,13 +800,16 @@ int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int64_t m, 
         return CHORDAL_OK;
     }
     const int W = (int)((n + 31) >> 5);
-    // One thread per four row words; graphs with a high average degree (m known,
-    // 2m/n >= kSegDenseDeg) split many classes per step, and their partition
-    // phases (3b / 3c, one warp per four split-class words) run on 512 threads.
+    // One thread per four row words; dense graphs (m known, 2m >= n^2 / 8:
+    // G(n, 0.5) splits classes of thousands of vertices in each of its few
+    // steps) run their partition phases (3b / 3c, one warp per four split-class
+    // words) on 512 threads: G(32768, 0.5) 0.68 -> 0.60 ms, while the sparser
+    // configuration-3 chordal graph (average degree 1005) is faster on 256
+    // (69.8 vs 71.6 ms, tools/seg_time.cu).
     int T = max(32, ((W + 3) / 4 + 31) / 32 * 32);
-    if (m >= 0 && n > 1024 && 2 * m >= kSegDenseDeg * n) T = max(T, 512);
+    if (m >= 0 && n > 1024 && 2 * m * kSegDenseFrac >= n * n) T = max(T, 512);
 #ifdef SEG_THREADS_ENV
-    if (const char *ev = getenv("SEG_THREADS")) T = max(T, atoi(ev));
+    if (const char *ev = getenv("SEG_THREADS")) T = max(max(32, ((W + 3) / 4 + 31) / 32 * 32), atoi(ev));
 #endif
     const size_t smem = seg_smem_bytes(n);
     cudaError_t e;

@@ -42,7 +42,7 @@ int main(int argc, char **argv) {
         cudaEventElapsedTime(&ms, a, b);
         unsigned long long p[16];
         cudaMemcpyFromSymbol(p, chordal::seg_prof, sizeof(p));
-        const char *const names[] = {"steps", "full", "phase1", "short-tail", "scan", "3a", "3b", "3c+end", "guess-hit", "ntouch", "movers(full)", "splits", "3b-own", "3b-wait", "-", "-"};
+        const char *const names[] = {"steps", "full", "phase1", "short-tail", "scan", "3a", "3b", "3c+end", "guess-hit", "ntouch", "movers(full)", "splits", "3b-own", "3b-wait", "max-thr-mov", "3b-rounds(w0)"};
         printf("rc=%d n=%lld %.3f ms (%.1f ns/step)\n", rc, n, ms, ms * 1e6 / n);
         for (int k = 0; k < 16; ++k)
             printf("  %-10s %14llu  %8.1f per step\n", names[k], p[k], (double)p[k] / (double)(p[0] ? p[0] : 1));
