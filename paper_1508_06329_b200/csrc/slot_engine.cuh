@@ -25,7 +25,9 @@
 //               moved count is linked before c -- all splits of a step at
 //               once (each insertion touches only its own cells);
 //             pass 2 places each mover at d's next free slot -- chunk order is
-//               ascending id, the reference's insertion order.
+//               ascending id, the reference's insertion order;
+//             a pivot with <= 32 neighbours (one chunk) takes a fast step that
+//               does both passes in registers (no per-class counters in memory).
 //   early exit once #classes == #unvisited (every class a singleton): the
 //             rest of the order is the class list.
 // parent[y] = x is recorded for every unvisited neighbour y of x, so after
@@ -101,6 +103,8 @@ struct CsrStagedSource {
         __syncwarp();
     }
     __device__ __forceinline__ int get(int64_t e) const { return (int)buf[e - base]; }
+    // one list entry straight from global memory (the <= 32-neighbour fast step)
+    __device__ __forceinline__ int fetch(int64_t k) const { return __ldg(indices + k); }
     // Row bounds of a likely next pivot, issued where they stand (their values
     // are used a step later), and an L2 prefetch of the row itself once they
     // have arrived: the next step's row fetch then skips the indptr round trip
@@ -120,7 +124,8 @@ struct CsrStagedSource {
 // lane-0 cycle counters (tools/slot_profile.cu only): [0] steps [1] pivot
 // [2] bounds + pass 1 [3] allocate [4] pass 2 + restore [5] touched classes
 // [6] steps with the pivot known ahead [7] steps with its row bounds fetched ahead
-__device__ unsigned long long slot_prof[8];
+// [8] fast steps (<= 32 neighbours) [9] (unused)
+__device__ unsigned long long slot_prof[10];
 #define SLOT_T(k)                                           \
     do {                                                    \
         const long long _c = clock64();                     \
@@ -307,7 +312,7 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
     long long nxs = -1;
 
 #ifdef SLOT_PROFILE
-    unsigned long long slot_acc[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long slot_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
     long long slot_t0 = clock64();
 #endif
     for (int i = 0; i < n; ++i) {
@@ -434,6 +439,136 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
             for (int j = 0; j < V; ++j) {  // only slots inside x's segment hold valid ids
                 const long long sj = cand_base + (long long)lane * V + j;
                 ccl[j] = (sj > xs && sj < e0) ? (int)M.cls[(int)cv[j]] : -1;
+            }
+        }
+        // ---- fast step: at most 32 neighbours (97 % of the configuration-5 steps) --
+        // One chunk holds every mover of the step, so a class's group in the
+        // chunk is its whole move set: counts come from __match_any_sync, each
+        // leader reads its class's fields once, the new segments are laid out
+        // in registers -- no c_cnt / touched round trips and no restore pass.
+        // When x's class emptied, the new head class's first live slot is
+        // fetched too, so the next pivot stays known.
+        if constexpr (MODE == CHORDAL_TIE_ASCENDING || MODE == CHORDAL_TIE_DESCENDING) {
+            if (nb1 - nb0 <= 32 && top + 32 <= M.cap) {
+#ifdef SLOT_PROFILE
+                slot_acc[8]++;
+#endif
+                const int deg = (int)(nb1 - nb0);
+                const int y = lane < deg ? src.fetch(MODE == CHORDAL_TIE_DESCENDING ? nb1 - 1 - lane : nb0 + lane) : 0;
+                const bool alt = hc != c0 && hc != (int)C::NIL;  // head class after x: not x's class
+                long long hh = 0, he = 0;
+                if (alt) {
+                    hh = (long long)M.c_head[hc];
+                    he = (long long)M.c_end[hc];
+                }
+                const int frl = nfree - 1 - lane >= 0 ? (int)M.freel[nfree - 1 - lane] : 0;
+                const int c = lane < deg ? (int)M.cls[y] : (int)C::VISITED;
+                const long long abase = hh & ~(long long)(V - 1);
+                uint4 araw = make_uint4(0, 0, 0, 0);
+                if (alt) araw = *reinterpret_cast<const uint4 *>(M.slot_v + abase + (long long)lane * V);
+                const bool ok = c != (int)C::VISITED;
+                if (ok && parent) parent[y] = (O)x;
+                const uint32_t vm = __ballot_sync(CH_FULL, ok);
+                const uint32_t peers = __match_any_sync(CH_FULL, ok ? c : -1) & vm;
+                const bool leader = ok && (peers & lt) == 0;
+                const int cnt = __popc(peers);
+                int live_c = 0, pold = 0;
+                if (leader) {
+                    live_c = (int)M.c_live[c];
+                    pold = (int)M.c_prev[c];
+                }
+                int acl[V];
+                {
+                    const I *av = reinterpret_cast<const I *>(&araw);
+#pragma unroll
+                    for (int j = 0; j < V; ++j) {
+                        const long long sj = abase + (long long)lane * V + j;
+                        acl[j] = (alt && sj >= hh && sj < he) ? (int)M.cls[(int)av[j]] : -1;
+                    }
+                }
+                int hmv = ok && c == hc ? y : (MODE == CHORDAL_TIE_DESCENDING ? -1 : 0x7FFFFFFF);
+                const int hmf = MODE == CHORDAL_TIE_DESCENDING ? __reduce_max_sync(CH_FULL, hmv)
+                                                               : (int)__reduce_min_sync(CH_FULL, (unsigned)hmv);
+                // next pivot if the head class keeps its segment: its first live
+                // slot after x (x's class) or its first live slot (the next class)
+                auto first_in_window = [&](const uint4 &raw, long long wb, const int *cl, int want, long long lo,
+                                           long long hi, int &gv_out, long long &gs_out) {
+                    const I *cv = reinterpret_cast<const I *>(&raw);
+                    int fj = V, fv = -1;
+#pragma unroll
+                    for (int j = V - 1; j >= 0; --j) {
+                        const long long sj = wb + (long long)lane * V + j;
+                        if (sj >= lo && sj < hi && cl[j] == want) {
+                            fj = j;
+                            fv = (int)cv[j];
+                        }
+                    }
+                    const uint32_t gm = __ballot_sync(CH_FULL, fj < V);
+                    gv_out = -1;
+                    gs_out = -1;
+                    if (gm) {
+                        const int src_l = __ffs(gm) - 1;
+                        gv_out = __shfl_sync(CH_FULL, fv, src_l);
+                        gs_out = wb + (long long)src_l * V + __shfl_sync(CH_FULL, fj, src_l);
+                    }
+                };
+                int guess = -1;
+                long long gslot = -1;
+                if (alt)
+                    first_in_window(araw, abase, acl, hc, hh, he, guess, gslot);
+                else
+                    first_in_window(cand_raw, cand_base, ccl, c0, xs + 1, e0, guess, gslot);
+                // new classes: one per split group, segments laid out in lane order
+                const bool split = leader && cnt != live_c;
+                const uint32_t sm = __ballot_sync(CH_FULL, split);
+                const int d = __shfl_sync(CH_FULL, frl, __popc(sm & lt));
+                const int kk = split ? cnt : 0;
+                int incl = kk;
+#pragma unroll
+                for (int dd = 1; dd < 32; dd <<= 1) {
+                    const int o = __shfl_up_sync(CH_FULL, incl, dd);
+                    if (lane >= dd) incl += o;
+                }
+                const long long start = top + incl - kk;
+                if (split) {
+                    M.c_head[d] = (S)start;
+                    M.c_end[d] = (S)(start + cnt);
+                    M.c_live[d] = (I)cnt;
+                    M.c_cnt[d] = (I)0;
+                    M.c_live[c] = (I)(live_c - cnt);
+                    // link d before c (pold read above, before any link write)
+                    M.c_prev[d] = (I)pold;
+                    M.c_next[d] = (I)c;
+                    M.c_prev[c] = (I)d;
+                    if (pold != (int)C::NIL) M.c_next[pold] = (I)d;
+                }
+                long long hstart = -1;
+                const uint32_t hb = __ballot_sync(CH_FULL, split && c == hc);
+                if (hb) {  // the head class split: its movers' class is the new head
+                    const int src_l = __ffs(hb) - 1;
+                    chead = __shfl_sync(CH_FULL, d, src_l);
+                    hstart = __shfl_sync(CH_FULL, start, src_l);
+                }
+                top += __shfl_sync(CH_FULL, incl, 31);
+                nfree -= __popc(sm);
+                nclasses += __popc(sm);
+                // movers of split classes into their new segment, in lane (tie) order
+                const int ls = ok ? __ffs(peers) - 1 : 0;
+                const int dl = __shfl_sync(CH_FULL, d, ls);
+                const long long stl = __shfl_sync(CH_FULL, start, ls);
+                if (ok && ((sm >> ls) & 1u)) {
+                    M.slot_v[stl + __popc(peers & lt)] = (I)y;
+                    M.cls[y] = (I)dl;
+                }
+                nx = hstart >= 0 ? hmf : guess;
+                nxs = hstart >= 0 ? hstart : gslot;
+                if (nx >= 0 && nx != gv) {  // issuing these earlier (on the window guess) or adding an
+                    src.bounds_issue(nx, gb0, gb1);  // L2 prefetch of the row measured slower
+                    gv = nx;
+                }
+                __syncwarp();
+                SLOT_T(2);
+                continue;
             }
         }
         int ntouch = 0;
@@ -616,7 +751,7 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
     }
 #ifdef SLOT_PROFILE
     if (lane == 0)
-        for (int k = 0; k < 8; ++k) atomicAdd(&slot_prof[k], slot_acc[k]);
+        for (int k = 0; k < 10; ++k) atomicAdd(&slot_prof[k], slot_acc[k]);
 #endif
 }
 
