@@ -320,6 +320,14 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
         slot_acc[0]++;
         slot_t0 = clock64();
 #endif
+        // The pivot known with its row bounds and <= 32 neighbours: its list is
+        // fetched first, so that round trip overlaps the head-class reads below
+        // (config 5: 1.98 -> 1.94 s).
+        constexpr bool kFast = MODE == CHORDAL_TIE_ASCENDING || MODE == CHORDAL_TIE_DESCENDING;
+        const bool pre = kFast && nx >= 0 && nx == gv && gb1 - gb0 <= 32;
+        int ypre = 0;
+        if (pre && lane < (int)(gb1 - gb0))
+            ypre = src.fetch(MODE == CHORDAL_TIE_DESCENDING ? gb1 - 1 - lane : gb0 + lane);
         // ---- pivot: first live slot of the head class (or hash election) ----
         const int c0 = chead;
         const long long e0 = (long long)M.c_end[c0];
@@ -448,13 +456,14 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
         // in registers -- no c_cnt / touched round trips and no restore pass.
         // When x's class emptied, the new head class's first live slot is
         // fetched too, so the next pivot stays known.
-        if constexpr (MODE == CHORDAL_TIE_ASCENDING || MODE == CHORDAL_TIE_DESCENDING) {
+        if constexpr (kFast) {
             if (nb1 - nb0 <= 32 && top + 32 <= M.cap) {
 #ifdef SLOT_PROFILE
                 slot_acc[8]++;
 #endif
                 const int deg = (int)(nb1 - nb0);
-                const int y = lane < deg ? src.fetch(MODE == CHORDAL_TIE_DESCENDING ? nb1 - 1 - lane : nb0 + lane) : 0;
+                const int y = pre ? ypre
+                                  : (lane < deg ? src.fetch(MODE == CHORDAL_TIE_DESCENDING ? nb1 - 1 - lane : nb0 + lane) : 0);
                 const bool alt = hc != c0 && hc != (int)C::NIL;  // head class after x: not x's class
                 long long hh = 0, he = 0;
                 if (alt) {
