@@ -6,12 +6,12 @@
 // (search.py:500-532) and _is_peo_lists (peo.py:100-149) -- the pair the
 // reference runs on graphs that only expose n, m and adjacency_lists0()
 // (the N = 10^6 configuration).
+#include <mutex>
+
 #include "common.cuh"
 #include "slot_engine.cuh"
 
 namespace chordal {
-
-void keep_pool_bytes(size_t bytes);  // capi.cu
 
 namespace {
 
@@ -137,7 +137,13 @@ peo_csr_key_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int nw = (gridDim.x * blockDim.x) >> 5;
     const int64_t heavy = heavy_threshold(indptr, n);
-    for (int v = v_begin + gw; v < v_end; v += nw) {
+    // The current minimum key, refreshed every 16 vertices of this warp: read per
+    // vertex, a million warps' loads of one address queued at one L2 slice and
+    // made the check's time swing 0.8-1.8 ms between runs on configuration 5.
+    unsigned long long kmin = ~0ULL;
+    int it = 0;
+    for (int v = v_begin + gw; v < v_end; v += nw, ++it) {
+        if ((it & 15) == 0) kmin = *(volatile unsigned long long *)key;
         const int pv = __ldg(pos + v);
         const int64_t b = __ldg(indptr + v), e = __ldg(indptr + v + 1);
         if (e - b > heavy) continue;  // heavy rows: split over the grid (peo_csr_heavy_*)
@@ -163,7 +169,7 @@ peo_csr_key_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict
         }
         if (p < 0) continue;
         const unsigned long long k64 = ((unsigned long long)p << 32) | (unsigned)v;
-        if (k64 >= *(volatile unsigned long long *)key) continue;
+        if (k64 >= kmin) continue;
         const int pp = __ldg(pos + p);
         const int64_t pb = __ldg(indptr + p), pe = __ldg(indptr + p + 1);
         bool viol = false;
@@ -175,7 +181,10 @@ peo_csr_key_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict
             }
             if (__any_sync(CH_FULL, viol)) { viol = true; break; }
         }
-        if (viol && lane == 0) atomicMin(key, k64);
+        if (viol) {
+            if (lane == 0) atomicMin(key, k64);
+            kmin = min(kmin, k64);
+        }
     }
 }
 
@@ -194,6 +203,24 @@ struct PeoHeavy {
     int best[kPeoHeavyMax];    // max position before pos(v) (parent search)
     int parent[kPeoHeavyMax];  // resolved parent, -1 none
 };
+
+constexpr int kHeavySlots = 4;
+__device__ PeoHeavy g_peo_heavy[kHeavySlots];  // 4 x 48 KB per device
+
+struct HeavySlots {
+    std::mutex mu;
+    PeoHeavy *base = nullptr;
+    cudaEvent_t ev[kHeavySlots] = {};
+    unsigned next = 0;
+};
+
+// one set per device (the module's __device__ array is per device too)
+HeavySlots &heavy_slots() {
+    static HeavySlots sets[64];
+    int dev = 0;
+    cudaGetDevice(&dev);
+    return sets[dev & 63];
+}
 
 __global__ void peo_csr_heavy_collect(const int64_t *__restrict__ indptr, int n, const int32_t *__restrict__ parent_in,
                                       int v_begin, int v_end, PeoHeavy *H) {
@@ -464,10 +491,21 @@ int launch_peo_csr_key(const int64_t *indptr, const int32_t *indices, int64_t n,
     peo_csr_key_kernel<<<(int)blocks, 256, 0, stream>>>(indptr, indices, (int)n, pos, parent, (int)v_begin,
                                                         (int)v_end, reinterpret_cast<unsigned long long *>(key));
     CH_LAUNCH_CHECK();
-    // heavy rows (stream-ordered scratch for their list)
-    PeoHeavy *H = nullptr;
-    keep_pool_bytes(sizeof(PeoHeavy));  // keep the block mapped between calls (unmap/remap costs ms)
-    if (cudaMallocAsync(reinterpret_cast<void **>(&H), sizeof(PeoHeavy), stream) != cudaSuccess) return CHORDAL_ENOMEM;
+    // heavy rows: their list lives in one of a few static device slots, handed
+    // out round robin; a slot's next user waits (on the device) for the event
+    // its previous user recorded.  No allocation per call -- stream-ordered
+    // pool blocks made single calls milliseconds slower at random.
+    HeavySlots &hs = heavy_slots();
+    std::lock_guard<std::mutex> lock(hs.mu);
+    if (!hs.base && cudaGetSymbolAddress(reinterpret_cast<void **>(&hs.base), g_peo_heavy) != cudaSuccess)
+        return CHORDAL_ECUDA;
+    const int slot = (int)(hs.next++ % kHeavySlots);
+    if (!hs.ev[slot]) {
+        if (cudaEventCreateWithFlags(&hs.ev[slot], cudaEventDisableTiming) != cudaSuccess) return CHORDAL_ECUDA;
+    } else if (cudaStreamWaitEvent(stream, hs.ev[slot], 0) != cudaSuccess) {
+        return CHORDAL_ECUDA;
+    }
+    PeoHeavy *H = hs.base + slot;
     cudaMemsetAsync(H, 0, sizeof(int) * 2, stream);
     long long cb = (v_end - v_begin + 255) / 256;
     if (cb > 148LL * 8) cb = 148LL * 8;
@@ -477,7 +515,7 @@ int launch_peo_csr_key(const int64_t *indptr, const int32_t *indices, int64_t n,
     peo_csr_heavy_parent_pick<<<hb, 256, 0, stream>>>(indptr, indices, pos, H);
     peo_csr_heavy_stray<<<hb, 256, 0, stream>>>(indptr, indices, pos, H, reinterpret_cast<unsigned long long *>(key));
     const cudaError_t le = cudaGetLastError();
-    cudaFreeAsync(H, stream);
+    if (cudaEventRecord(hs.ev[slot], stream) != cudaSuccess) return CHORDAL_ECUDA;
     return le == cudaSuccess ? CHORDAL_OK : CHORDAL_ECUDA;
 }
 
