@@ -637,3 +637,39 @@ def test_new_orderings_edge_cases():
             assert list(P.bfs_order(g, P.seeded(5))) == [x + 1 for x in oracle.other_order(g._packed, n, "bfs", 5)]
     c = CSRGraph.from_edges0(3, np.array([0]), np.array([2]))
     assert list(P.bfs_order(c)) == [1, 3, 2]
+
+
+@pytest.mark.gpu
+def test_csr_global_engine_tie_rules_and_components():
+    """The global-memory slot engine (CSR, n > 32768) with its <= 32-neighbour fast
+    step: LOWEST_INDEX against the oracle's PartitionList, and the descending rule
+    through the relabelling v -> n - v (v >= 1) that turns it into LOWEST_INDEX
+    (the initial class [1, n, n-1, ..., 2] of parallel/lexbfs.py:173 becomes
+    ascending); graphs with many components exercise the new-component steps."""
+    from paper_1508_06329_b200.csr import CSRGraph
+    from paper_1508_06329_b200.generate import chordal_random_edges
+
+    rng = np.random.default_rng(1508)
+    n = 40000
+    cases = []
+    u, v = chordal_random_edges(n, 6, 11)
+    cases.append(("chordal", u, v))
+    a = rng.integers(0, n, 30000)
+    b = rng.integers(0, n, 30000)
+    keep = a != b
+    cases.append(("forest-ish", a[keep], b[keep]))
+    hub = np.zeros(5000, dtype=np.int64) + 7  # one vertex with > 32 neighbours among small ones
+    cases.append(("hub", np.concatenate([a[keep], hub]), np.concatenate([b[keep], rng.integers(0, n, 5000)])))
+    relabel = np.concatenate([[0], n - np.arange(1, n)])  # f(0) = 0, f(v) = n - v
+    for name, uu, vv in cases:
+        lo, hi = np.minimum(uu, vv), np.maximum(uu, vv)
+        pairs = np.unique(np.stack([lo, hi], 1)[lo != hi], axis=0)
+        g = CSRGraph.from_edges0(n, pairs[:, 0], pairs[:, 1])
+        want = oracle.lexbfs_partition_csr(g.indptr, g.indices, n)
+        assert o0(P.lexbfs_partition(g)) == want.tolist(), name
+        ok, w = oracle.is_peo_csr(g.indptr, g.indices, n, want)
+        verdict = P.is_chordal(g)
+        assert verdict.chordal == ok and w0(verdict.witness) == (None if w is None else list(w)), name
+        gr = CSRGraph.from_edges0(n, relabel[pairs[:, 0]], relabel[pairs[:, 1]])
+        want_desc = relabel[oracle.lexbfs_partition_csr(gr.indptr, gr.indices, n)]  # f is an involution
+        assert o0(P.parallel_lexbfs(g, DESC)) == want_desc.tolist(), name
