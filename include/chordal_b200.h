@@ -19,11 +19,14 @@
  *    symmetric, no self loops) -- the adjacency_lists0() shape (graph.py:152).
  *  - "_dev" arguments are device pointers; every call is asynchronous on
  *    `stream` (a cudaStream_t; NULL = legacy default stream) unless the name
- *    ends in _host.  The library keeps no global mutable state, holds no
- *    caller pointer after return and is reentrant per stream.  The _host
- *    entry points allocate stream-ordered from the device's default memory
- *    pool and raise that pool's release threshold to one call's footprint so
- *    the buffers stay mapped between calls (the only process-wide effect).
+ *    ends in _host.  The library holds no caller pointer after return and is
+ *    reentrant per stream.  Its only global state: four static 48 KB device
+ *    slots per device for the CSR PEO check's heavy-row list, handed out
+ *    round robin under a mutex, each reuse ordered on the device after its
+ *    previous user by an event.  The _host entry points without a workspace
+ *    argument allocate stream-ordered from the device's default memory pool
+ *    and raise that pool's release threshold to one call's footprint so the
+ *    buffers stay mapped between calls (a process-wide setting).
  *  - Witness triples are int32[3] = (v, p, z) -- WitnessTriple (peo.py:26-45),
  *    0-based -- or (-1, -1, -1) when the ordering is a PEO.
  *  - Every function returns a chordal status code (CHORDAL_OK == 0).

@@ -9,10 +9,6 @@
 
 #include "../paper_1508_06329_b200/csrc/csr.cu"
 
-namespace chordal {
-void keep_pool_bytes(size_t) {}  // capi.cu's pool setting; not needed here
-}  // namespace chordal
-
 int main(int argc, char **argv) {
     if (argc < 3) return 1;
     FILE *f = fopen(argv[1], "rb");
