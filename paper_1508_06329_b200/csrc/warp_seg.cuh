@@ -288,38 +288,109 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
                 const uint32_t tmask = __ballot_sync(CH_FULL, touched);
                 // ---- stable partition of every split class: movers first -----------
                 int nsp = 0;
-                for (uint32_t tm = tmask; tm; tm &= tm - 1) {
-                    const int q = __ffs(tm) - 1;
-                    const uint32_t bq = __shfl_sync(CH_FULL, b, q), fq = __shfl_sync(CH_FULL, Fl, q);
-                    const int lbq = __shfl_sync(CH_FULL, LBr, q), nbq = __shfl_sync(CH_FULL, NBr, q);
-                    const int pcq = __shfl_sync(CH_FULL, Pc, q);
-                    const int p = 32 * q + l;
-                    const bool ok = p >= hpos && p < tail0;
-                    const uint32_t bl = bq & mask_below(l + 1), ab = bq & ~mask_below(l + 1);
-                    const int s = bl ? 32 * q + highest_bit(bl) : lbq;
-                    const int e = ab ? 32 * q + __ffs(ab) - 1 : nbq;
-                    const int cs = cntb(s), T = cntb(e) - cs;
-                    const int v = M.A[p];
-                    if (ok) {
-                        int dst = p;
-                        if (T > 0 && T < e - s) {
-                            const int fb = pcq + __popc(fq & mask_below(l)) - cs;
-                            dst = ((fq >> l) & 1u) ? s + fb : s + T + (p - s - fb);
-                            if (p == s) {
-                                atomicOr(&M.NB[(s + T) >> 5], 1u << ((s + T) & 31));
+                if (LATENCY) {
+                    // Several touched words per round, branch-free up to the stores, so
+                    // their shuffle / shared-memory chains overlap (single graphs:
+                    // the step is a latency chain; the batch keeps one word per
+                    // round -- fewer instructions, its latency is hidden).
+                    auto word = [&](int q, int &v, int &dst, bool &ok, bool &start, int &ns) {
+                        const uint32_t bq = __shfl_sync(CH_FULL, b, q), fq = __shfl_sync(CH_FULL, Fl, q);
+                        const int lbq = __shfl_sync(CH_FULL, LBr, q), nbq = __shfl_sync(CH_FULL, NBr, q);
+                        const int pcq = __shfl_sync(CH_FULL, Pc, q);
+                        const int p = 32 * q + l;
+                        ok = p >= hpos && p < tail0;
+                        const uint32_t bl = bq & mask_below(l + 1), ab = bq & ~mask_below(l + 1);
+                        const int s = bl ? 32 * q + highest_bit(bl) : lbq;
+                        const int e = ab ? 32 * q + __ffs(ab) - 1 : nbq;
+                        const int cs = cntb(s), T = cntb(e) - cs;
+                        v = M.A[p];
+                        const bool split = T > 0 && T < e - s;
+                        const int fb = pcq + __popc(fq & mask_below(l)) - cs;
+                        const int to = ((fq >> l) & 1u) ? s + fb : s + T + (p - s - fb);
+                        dst = split ? to : p;
+                        start = ok && split && p == s;
+                        ns = s + T;
+                    };
+#ifndef WSEG_SPLIT_K
+#define WSEG_SPLIT_K 2
+#endif
+                    // words per round: 2 on config 1 (chordal n = 1000: split steps 633 ->
+                    // 446 cycles per step; 4 words: 468, 8: 631, tools/warp_profile.cu)
+                    constexpr int K = WSEG_SPLIT_K;
+                    for (uint32_t tm = tmask; tm;) {
+                        int q[K], v[K], dst[K], ns[K];
+                        bool has[K], ok[K], st[K];
+#pragma unroll
+                        for (int u = 0; u < K; ++u) {
+                            has[u] = tm != 0;
+                            q[u] = has[u] ? __ffs(tm) - 1 : q[0];
+                            tm &= tm - 1;
+                        }
+#pragma unroll
+                        for (int u = 0; u < K; ++u) word(q[u], v[u], dst[u], ok[u], st[u], ns[u]);
+#pragma unroll
+                        for (int u = 0; u < K; ++u)
+                            if (has[u] && ok[u]) M.An[dst[u]] = (uint16_t)v[u];
+#pragma unroll
+                        for (int u = 0; u < K; ++u)
+                            if (has[u] && st[u]) {
+                                atomicOr(&M.NB[ns[u] >> 5], 1u << (ns[u] & 31));
                                 ++nsp;
                             }
-                        }
-                        M.An[dst] = (uint16_t)v;
                     }
-                }
-                __syncwarp();
-                for (uint32_t tm = tmask; tm; tm &= tm - 1) {
-                    const int p = 32 * (__ffs(tm) - 1) + l;
-                    if (p >= hpos && p < tail0) {
-                        const int v = M.An[p];
-                        M.A[p] = (uint16_t)v;
-                        M.P[v] = (uint16_t)p;
+                    __syncwarp();
+                    for (uint32_t tm = tmask; tm;) {
+                        int p[K], v[K];
+                        bool ok[K];
+#pragma unroll
+                        for (int u = 0; u < K; ++u) {
+                            const bool h = tm != 0;
+                            p[u] = h ? 32 * (__ffs(tm) - 1) + l : p[0];
+                            tm &= tm - 1;
+                            ok[u] = h && p[u] >= hpos && p[u] < tail0;
+                            v[u] = M.An[p[u]];
+                        }
+#pragma unroll
+                        for (int u = 0; u < K; ++u)
+                            if (ok[u]) {
+                                M.A[p[u]] = (uint16_t)v[u];
+                                M.P[v[u]] = (uint16_t)p[u];
+                            }
+                    }
+                } else {
+                    for (uint32_t tm = tmask; tm; tm &= tm - 1) {
+                        const int q = __ffs(tm) - 1;
+                        const uint32_t bq = __shfl_sync(CH_FULL, b, q), fq = __shfl_sync(CH_FULL, Fl, q);
+                        const int lbq = __shfl_sync(CH_FULL, LBr, q), nbq = __shfl_sync(CH_FULL, NBr, q);
+                        const int pcq = __shfl_sync(CH_FULL, Pc, q);
+                        const int p = 32 * q + l;
+                        const bool ok = p >= hpos && p < tail0;
+                        const uint32_t bl = bq & mask_below(l + 1), ab = bq & ~mask_below(l + 1);
+                        const int s = bl ? 32 * q + highest_bit(bl) : lbq;
+                        const int e = ab ? 32 * q + __ffs(ab) - 1 : nbq;
+                        const int cs = cntb(s), T = cntb(e) - cs;
+                        const int v = M.A[p];
+                        if (ok) {
+                            int dst = p;
+                            if (T > 0 && T < e - s) {
+                                const int fb = pcq + __popc(fq & mask_below(l)) - cs;
+                                dst = ((fq >> l) & 1u) ? s + fb : s + T + (p - s - fb);
+                                if (p == s) {
+                                    atomicOr(&M.NB[(s + T) >> 5], 1u << ((s + T) & 31));
+                                    ++nsp;
+                                }
+                            }
+                            M.An[dst] = (uint16_t)v;
+                        }
+                    }
+                    __syncwarp();
+                    for (uint32_t tm = tmask; tm; tm &= tm - 1) {
+                        const int p = 32 * (__ffs(tm) - 1) + l;
+                        if (p >= hpos && p < tail0) {
+                            const int v = M.An[p];
+                            M.A[p] = (uint16_t)v;
+                            M.P[v] = (uint16_t)p;
+                        }
                     }
                 }
                 nclasses += __reduce_add_sync(CH_FULL, nsp);
