@@ -62,7 +62,9 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if not os.path.exists(src):
             continue
         obj = os.path.join(LIBDIR, os.path.splitext(s)[0] + ".o")
-        cmd = [_nvcc(), *ARCH, *FLAGS, "-I", INCLUDE, "-c", src, "-o", obj]
+        # CHORDAL_NVCC_EXTRA: extra nvcc flags for kernel experiments (e.g. -DWSEG_SPLIT_K=4)
+        extra = os.environ.get("CHORDAL_NVCC_EXTRA", "").split()
+        cmd = [_nvcc(), *ARCH, *FLAGS, *extra, "-I", INCLUDE, "-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         log.append(r.stdout + r.stderr)
         if r.returncode != 0:

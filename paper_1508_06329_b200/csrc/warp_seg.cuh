@@ -315,7 +315,8 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
 #define WSEG_SPLIT_K 2
 #endif
                     // words per round: 2 on config 1 (chordal n = 1000: split steps 633 ->
-                    // 446 cycles per step; 4 words: 468, 8: 631, tools/warp_profile.cu)
+                    // 446 cycles per step; 4 words: 468, 8: 631, tools/warp_profile.cu);
+                    // the batch kernel with 2: 7.52 -> 8.01 ms (tools/ab_batch.sh)
                     constexpr int K = WSEG_SPLIT_K;
                     for (uint32_t tm = tmask; tm;) {
                         int q[K], v[K], dst[K], ns[K];
