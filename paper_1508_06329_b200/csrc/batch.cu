@@ -229,10 +229,12 @@ int launch_batch(const uint8_t *adj, int64_t batch, int64_t n, int64_t stride, i
                  int32_t *witness, cudaStream_t stream) {
     if (batch <= 0) return CHORDAL_OK;
     if (n > 1024) return CHORDAL_ETOOLARGE;
-    // Four warps per CTA, warp w of CTA b on graph b + w * gridDim.x: the
-    // measured best of {1, 2, 4} warps per CTA x register caps (higher
-    // occupancy only spills; tools/batch_split.py, round 1).
-    return launch_batch_cfg<4, 1>(adj, batch, n, stride, orders, witness, stream);
+    // Four warps per CTA, warp w of CTA b on graph b + w * gridDim.x, registers
+    // capped at 56 per thread (9 CTAs = 36 warps per SM, 12 bytes of spill):
+    // 7.56 ms per config-4 batch uncapped (71 registers, 28 warps), 7.12 at 64
+    // (<4, 8>), 7.02 here, 7.20 at 48 (<4, 10>), 8.58 at 40; <2, 18> 7.40,
+    // <8, 4> 7.25 (tools/ab_multi.sh).
+    return launch_batch_cfg<4, 9>(adj, batch, n, stride, orders, witness, stream);
 }
 
 }  // namespace chordal
