@@ -98,6 +98,11 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, long long batch, int n
 
     // ---- PEO check: lanes stride over vertices -----------------------------------
     unsigned long long best = ~0ULL;
+    // the warp's smallest violation key so far, shared through the (now idle)
+    // mover-flag words so that every lane skips the vertices it cannot beat
+    unsigned long long *sbest = reinterpret_cast<unsigned long long *>(M.F);
+    if (lane == 0) *sbest = ~0ULL;
+    __syncwarp();
     for (int v = lane; v < n; v += 32) {
         const int pv = pos[v];
         if (pv == 0) continue;
@@ -126,7 +131,7 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, long long batch, int n
         }
         if (parent < 0) continue;
         const unsigned long long k64 = ((unsigned long long)parent << 32) | (unsigned)v;
-        if (k64 >= best) continue;
+        if (k64 >= best || k64 >= *(volatile unsigned long long *)sbest) continue;
         const int pp = pos[parent];
         const uint4 *rv4 = reinterpret_cast<const uint4 *>(rv);
         const uint4 *rp4 = reinterpret_cast<const uint4 *>(A32 + parent * sw);
@@ -156,7 +161,10 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, long long batch, int n
                 }
             }
         }
-        if (viol) best = k64;
+        if (viol) {
+            best = k64;
+            atomicMin(sbest, k64);
+        }
     }
 #pragma unroll
     for (int d = 16; d >= 1; d >>= 1) {
