@@ -111,9 +111,16 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, long long batch, int n
         if (parent == -2) {  // not produced by the search: backward scan, then full pass
             parent = -1;
             const int lim = pv > 64 ? pv - 64 : 0;
-            for (int q = pv - 1; q >= lim; --q) {
-                int u = ord[q];
-                if ((rv[u >> 5] >> (u & 31)) & 1u) { parent = u; break; }
+            for (int q0 = pv - 1; q0 >= lim && parent < 0; q0 -= 4) {  // four probes per round trip
+                int u[4];
+                uint32_t w[4];
+#pragma unroll
+                for (int k = 0; k < 4; ++k) u[k] = q0 - k >= lim ? (int)ord[q0 - k] : 0;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) w[k] = q0 - k >= lim ? rv[u[k] >> 5] : 0u;
+#pragma unroll
+                for (int k = 0; k < 4; ++k)
+                    if (parent < 0 && ((w[k] >> (u[k] & 31)) & 1u)) parent = u[k];
             }
             if (parent < 0 && lim > 0) {
                 int bp = -1;
