@@ -66,7 +66,7 @@ constexpr int kSegBig = 0x7FFFFFFF;
 constexpr int kSegDenseFrac = 8;  // edge density (2m / n^2) from which the kernel runs 512 threads: 1 / 8
 
 struct SegLayout {
-    size_t A, An, P, U, RA, F, NB, bnd, Pc, LB, NBq, TW, wt, misc, total;
+    size_t A, An, P, U, RA, F, NB, bnd, Pc, LB, NBq, TW, wt, misc, wslot, total;
     __host__ __device__ static size_t align16(size_t x) { return (x + 15) & ~size_t(15); }
     __host__ __device__ SegLayout(int W) {
         const size_t np = size_t(W) * 32;
@@ -86,6 +86,7 @@ struct SegLayout {
         TW = o; o = align16(o + WP * 2);
         wt = o; o = align16(o + 4 * 32 * 4);
         misc = o; o = align16(o + 24 * 4);
+        wslot = o; o = align16(o + 3 * 32 * 4);  // per-warp mover count / min / max position
         total = o;
     }
 };
@@ -216,9 +217,10 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
     uint16_t *TW = (uint16_t *)(smem + L.TW);
     int *wt = (int *)(smem + L.wt);
     // Per-step counters in 3 rotating sets of 8: [0] any vertex newly reached,
-    // [1] #movers, [2] min / [3] max mover position, [4] #split-class words,
-    // [5] #splits.  Step i uses set i % 3 and resets set (i + 1) % 3, whose
-    // last readers (step i - 2) are two barriers behind.
+    // [4] #split-class words, [5] #splits, [6] re-aimed row guess (the mover
+    // count and range come from per-warp slots, L.wslot).  Step i uses set
+    // i % 3 and resets set (i + 1) % 3, whose last readers (step i - 2) are two
+    // barriers behind.
     int *misc = (int *)(smem + L.misc);
     uint64_t *red_s = (uint64_t *)(smem + L.wt);  // block_max scratch aliases wt (never live at once)
     int32_t *red_i = (int32_t *)(smem + L.wt + 32 * 8);
@@ -423,16 +425,18 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
         // (c3 chordal 90.5 -> 86.5 ms); an extra L2 prefetch of the row after
         // it no longer pays once the load sits here.
         if (guess >= 0 && own) nxt = ld_nc_v4(rows + (long long)guess * sw + w0);
-        {  // mover count and position range: one shared atomic per warp
+        // mover count and position range: per-warp slots, reduced after B1 by
+        // every warp (lane w reads warp w's slot) -- same-address shared atomics
+        // from every warp cost ~1 % of a step at N = 32768
+        int *ws_ = (int *)(smem + L.wslot);
+        {
             const int wc = __reduce_add_sync(CH_FULL, cnt);
-            if (wc) {
-                const int wmn = (int)__reduce_min_sync(CH_FULL, (unsigned)pmn);
-                const int wmx = __reduce_max_sync(CH_FULL, pmx);
-                if (lane == 0) {
-                    atomicAdd(fl + 1, wc);
-                    atomicMin(fl + 2, wmn);
-                    atomicMax(fl + 3, wmx);
-                }
+            const int wmn = (int)__reduce_min_sync(CH_FULL, (unsigned)pmn);
+            const int wmx = __reduce_max_sync(CH_FULL, pmx);
+            if (lane == 0) {
+                ws_[warp] = wc;
+                ws_[32 + warp] = wmn;
+                ws_[64 + warp] = wmx;
             }
         }
         if (t < 8) misc[8 * ((i + 1) % 3) + t] = t == 2 ? kSegBig : (t == 3 ? -1 : 0);
@@ -443,8 +447,9 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
         seg_acc[14] += fl[7];
 #endif
         const bool anyE = fl[0] != 0;
-        const int cntA = fl[1];
-        const int gmn = fl[2], gmx = fl[3];
+        const int cntA = __reduce_add_sync(CH_FULL, lane < NW ? ws_[lane] : 0);
+        const int gmn = (int)__reduce_min_sync(CH_FULL, lane < NW ? (unsigned)ws_[32 + lane] : (unsigned)kSegBig);
+        const int gmx = __reduce_max_sync(CH_FULL, lane < NW ? ws_[64 + lane] : -1);
         // Movers that fill a run of whole classes change nothing (every class
         // they touch moves in one hop, search.py:448-453).
         const bool full = cntA > 0 &&
