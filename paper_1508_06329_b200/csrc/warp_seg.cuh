@@ -276,7 +276,11 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
                 // a class entering from the previous word / leaving into the next one
                 const int s_in = LBr, e_in = b ? 32 * l + __ffs(b) - 1 : NBr;
                 const int s_out = b ? 32 * l + highest_bit(b) : 0, e_out = NBr;
-                const int c1 = cntb(s_in), c2 = cntb(e_in), c3 = cntb(s_out), c4 = cntb(e_out);
+                // bounds inside this lane's own word need no shuffle; e_in is NBr
+                // (= e_out) when the word has no class start
+                const int c1 = cntb(s_in), c4 = cntb(e_out);
+                const int c2 = b ? Pc + __popc(Fl & mask_below(e_in & 31)) : c4;
+                const int c3 = Pc + __popc(Fl & mask_below(s_out & 31));
                 if (inr && !touched && !((b >> lob) & 1u)) {
                     const int T = c2 - c1;
                     touched = T > 0 && T < e_in - s_in;
