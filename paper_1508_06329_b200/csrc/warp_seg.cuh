@@ -281,6 +281,10 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
                 const int c1 = cntb(s_in), c4 = cntb(e_out);
                 const int c2 = b ? Pc + __popc(Fl & mask_below(e_in & 31)) : c4;
                 const int c3 = Pc + __popc(Fl & mask_below(s_out & 31));
+                // the word's class bounds outside it and their mover counts, packed
+                // 16 + 16 bits (all <= n <= 1024) so a touched word costs two shuffles
+                const uint32_t pkb = (uint32_t)LBr | ((uint32_t)NBr << 16);
+                const uint32_t pkc = (uint32_t)c1 | ((uint32_t)c4 << 16);
                 if (inr && !touched && !((b >> lob) & 1u)) {
                     const int T = c2 - c1;
                     touched = T > 0 && T < e_in - s_in;
@@ -299,14 +303,15 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
                     // round -- fewer instructions, its latency is hidden).
                     auto word = [&](int q, int &v, int &dst, bool &ok, bool &start, int &ns) {
                         const uint32_t bq = __shfl_sync(CH_FULL, b, q), fq = __shfl_sync(CH_FULL, Fl, q);
-                        const int lbq = __shfl_sync(CH_FULL, LBr, q), nbq = __shfl_sync(CH_FULL, NBr, q);
+                        const uint32_t pbq = __shfl_sync(CH_FULL, pkb, q), pcq2 = __shfl_sync(CH_FULL, pkc, q);
                         const int pcq = __shfl_sync(CH_FULL, Pc, q);
                         const int p = 32 * q + l;
                         ok = p >= hpos && p < tail0;
                         const uint32_t bl = bq & mask_below(l + 1), ab = bq & ~mask_below(l + 1);
-                        const int s = bl ? 32 * q + highest_bit(bl) : lbq;
-                        const int e = ab ? 32 * q + __ffs(ab) - 1 : nbq;
-                        const int cs = cntb(s), T = cntb(e) - cs;
+                        const int s = bl ? 32 * q + highest_bit(bl) : (int)(pbq & 0xFFFFu);
+                        const int e = ab ? 32 * q + __ffs(ab) - 1 : (int)(pbq >> 16);
+                        const int cs = bl ? pcq + __popc(fq & mask_below(s & 31)) : (int)(pcq2 & 0xFFFFu);
+                        const int T = (ab ? pcq + __popc(fq & mask_below(e & 31)) : (int)(pcq2 >> 16)) - cs;
                         v = M.A[p];
                         const bool split = T > 0 && T < e - s;
                         const int fb = pcq + __popc(fq & mask_below(l)) - cs;
@@ -366,14 +371,15 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
                     for (uint32_t tm = tmask; tm; tm &= tm - 1) {
                         const int q = __ffs(tm) - 1;
                         const uint32_t bq = __shfl_sync(CH_FULL, b, q), fq = __shfl_sync(CH_FULL, Fl, q);
-                        const int lbq = __shfl_sync(CH_FULL, LBr, q), nbq = __shfl_sync(CH_FULL, NBr, q);
+                        const uint32_t pbq = __shfl_sync(CH_FULL, pkb, q), pcq2 = __shfl_sync(CH_FULL, pkc, q);
                         const int pcq = __shfl_sync(CH_FULL, Pc, q);
                         const int p = 32 * q + l;
                         const bool ok = p >= hpos && p < tail0;
                         const uint32_t bl = bq & mask_below(l + 1), ab = bq & ~mask_below(l + 1);
-                        const int s = bl ? 32 * q + highest_bit(bl) : lbq;
-                        const int e = ab ? 32 * q + __ffs(ab) - 1 : nbq;
-                        const int cs = cntb(s), T = cntb(e) - cs;
+                        const int s = bl ? 32 * q + highest_bit(bl) : (int)(pbq & 0xFFFFu);
+                        const int e = ab ? 32 * q + __ffs(ab) - 1 : (int)(pbq >> 16);
+                        const int cs = bl ? pcq + __popc(fq & mask_below(s & 31)) : (int)(pcq2 & 0xFFFFu);
+                        const int T = (ab ? pcq + __popc(fq & mask_below(e & 31)) : (int)(pcq2 >> 16)) - cs;
                         const int v = M.A[p];
                         if (ok) {
                             int dst = p;
