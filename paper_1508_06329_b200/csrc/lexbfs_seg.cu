@@ -195,7 +195,10 @@ __device__ __forceinline__ int seg_scan1(int e, int *wt, int &te) {
 
 }  // namespace
 
-template <int MODE>
+// MV: movers handled per round of a thread's mover loop (their position loads
+// overlap): 4 for dense graphs (many movers per thread), 2 otherwise (config 2
+// chordal 12.53 -> 12.07 ms; G(8192, 0.5) would go 0.260 -> 0.274 ms with 2).
+template <int MODE, int MV>
 __global__ void __launch_bounds__(512, 1)
 lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint64_t seed, uint64_t cell,
                   int32_t *__restrict__ order, int32_t *__restrict__ pos_out, int32_t *__restrict__ parent) {
@@ -376,18 +379,18 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                 uint32_t m2 = r[k] & ra[k];
                 ext[k] = r[k] & uu[k];
                 extc += __popc(ext[k]);
-                while (m2) {  // four movers per round: their position loads overlap
-                    int y[4], pp[4], c = 0;
+                while (m2) {  // MV movers per round: their position loads overlap
+                    int y[MV], pp[MV], c = 0;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < MV; ++u) {
                         y[u] = 32 * (w0 + k) + __ffs(m2) - 1;
                         if (m2) ++c;
                         m2 &= m2 - 1;
                     }
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) pp[u] = u < c ? (int)P[y[u]] : 0;
+                    for (int u = 0; u < MV; ++u) pp[u] = u < c ? (int)P[y[u]] : 0;
 #pragma unroll
-                    for (int u = 0; u < 4; ++u) {
+                    for (int u = 0; u < MV; ++u) {
                         if (u < c) {
                             atomicOr(&F[pp[u] >> 5], 1u << (pp[u] & 31));
                             if (parent) parent[y[u]] = x;
@@ -812,16 +815,23 @@ int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int64_t m, 
     // configuration-3 chordal graph (average degree 1005) is faster on 256
     // (69.8 vs 71.6 ms, tools/seg_time.cu).
     int T = max(32, ((W + 3) / 4 + 31) / 32 * 32);
-    if (m >= 0 && n > 1024 && 2 * m * kSegDenseFrac >= n * n) T = max(T, 512);
+    const bool dense = m >= 0 && n > 1024 && 2 * m * kSegDenseFrac >= n * n;
+    if (dense) T = max(T, 512);
 #ifdef SEG_THREADS_ENV
     if (const char *ev = getenv("SEG_THREADS")) T = max(max(32, ((W + 3) / 4 + 31) / 32 * 32), atoi(ev));
 #endif
     const size_t smem = seg_smem_bytes(n);
     cudaError_t e;
-#define SEG_LAUNCH(M)                                                                                          \
-    e = cudaFuncSetAttribute(lexbfs_seg_kernel<M>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
-    if (e != cudaSuccess) return CHORDAL_ECUDA;                                                                 \
-    lexbfs_seg_kernel<M><<<1, T, smem, stream>>>(adj, (int)n, stride, seed, cell, order, pos, parent);
+#define SEG_LAUNCH_MV(M, K)                                                                                       \
+    e = cudaFuncSetAttribute(lexbfs_seg_kernel<M, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+    if (e != cudaSuccess) return CHORDAL_ECUDA;                                                                    \
+    lexbfs_seg_kernel<M, K><<<1, T, smem, stream>>>(adj, (int)n, stride, seed, cell, order, pos, parent);
+#define SEG_LAUNCH(M)                \
+    if (dense) {                     \
+        SEG_LAUNCH_MV(M, 4)          \
+    } else {                         \
+        SEG_LAUNCH_MV(M, 2)          \
+    }
     switch (tie_rule) {
         case CHORDAL_TIE_ASCENDING: SEG_LAUNCH(CHORDAL_TIE_ASCENDING); break;
         case CHORDAL_TIE_DESCENDING: SEG_LAUNCH(CHORDAL_TIE_DESCENDING); break;
@@ -829,6 +839,7 @@ int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int64_t m, 
         default: return CHORDAL_EINVAL;
     }
 #undef SEG_LAUNCH
+#undef SEG_LAUNCH_MV
     CH_LAUNCH_CHECK();
     return CHORDAL_OK;
 }
