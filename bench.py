@@ -38,6 +38,7 @@ import numpy as np
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
+DATA = "synthetic (the reference generators replayed bit-exact)"
 METRIC = "chordality-test ms/graph (N=32k dense) and graphs/sec batched at 1/2/4/8 B200 vs CPU"
 N512, STRIDE512, K512 = 512, 64, 8
 TOTAL_GRAPHS = 65536
@@ -130,12 +131,8 @@ def measured_peaks() -> tuple[dict, str]:
 
 
 def shard(total: int, rank: int, world: int) -> tuple[int, int]:
-    per = total // world
-    lo = rank * per
-    hi = total if rank == world - 1 else lo + per
-    if lo % 2:
-        lo += 1
-    return lo, hi
+    """Contiguous seed range of `rank`: the ranges tile [0, total) exactly for any world."""
+    return total * rank // world, total * (rank + 1) // world
 
 
 def build_batch(lo: int, hi: int, device):
@@ -168,6 +165,18 @@ def reduce_max(x: float, world: int) -> float:
     return float(t.item())
 
 
+def reduce_sum_ints(vals: list[int], world: int) -> list[int]:
+    if world == 1:
+        return list(vals)
+    import torch
+    import torch.distributed as dist
+
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor(vals, dtype=torch.int64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return [int(x) for x in t.tolist()]
+
+
 def barrier(world: int):
     if world > 1:
         import torch.distributed as dist
@@ -178,22 +187,46 @@ def barrier(world: int):
 # ------------------------------------------------------------- cpu baseline --
 
 
-def cpu_batch_baseline(adj_host: np.ndarray, budget_s: float = 15.0) -> dict:
-    """The reference algorithm (C port, oracle/) on a bounded prefix, all host threads."""
+PARITY_SAMPLE = 8192  # graphs of each rank's shard checked against the oracle every run
+
+
+def check_batch_parity(adj_host: np.ndarray, orders, wit, seed_lo: int, time_it: bool) -> dict:
+    """The oracle (C port of the reference's is_chordal, oracle/) on the first
+    PARITY_SAMPLE graphs of this rank's shard -- the graphs the timed loop ran --
+    compared bit for bit with the GPU's orders, verdicts and witnesses; raises on
+    any difference.  When time_it, the same run is the cpu_baseline (all host
+    threads; rank 0 at N=1)."""
     import oracle
 
+    S = min(len(adj_host), PARITY_SAMPLE)
     threads = oracle.max_threads()
-    probe = min(len(adj_host), max(2 * threads, 64))
+    # the inputs themselves: the GPU generator's graphs against the oracle's C
+    # restatement of the reference generators (sha-pinned to the reference)
+    ref_adj = oracle.gen_config4_batch(seed_lo, S, N512, 0.5, K512, STRIDE512, nthreads=threads)
+    if not np.array_equal(ref_adj, adj_host[:S]):
+        raise SystemExit(f"PARITY FAILURE on configuration 4: the device-generated graphs of seeds "
+                         f"{seed_lo}..{seed_lo + S - 1} differ from the reference generators")
+    del ref_adj
     t0 = time.perf_counter()
-    oracle.is_chordal_batch(adj_host[:probe], N512, nthreads=threads)
-    per = (time.perf_counter() - t0) / probe
-    S = int(min(len(adj_host), max(probe, budget_s / max(per, 1e-9)))) // 2 * 2
-    t0 = time.perf_counter()
-    oracle.is_chordal_batch(adj_host[:S], N512, nthreads=threads)
+    verdict, o_ref, w_ref = oracle.is_chordal_batch(adj_host[:S], N512, nthreads=threads)
     dt = time.perf_counter() - t0
-    return {"value": S / dt, "unit": "graphs/s", "cores": threads, "kind": "port",
-            "sample": f"first {S} graphs (seeds 0..{S - 1}) of configuration 4, LexBFS (PartitionList) + list "
-                      f"PEO test per graph, {threads} host threads"}
+    o_gpu = orders[:S].cpu().numpy()
+    w_gpu = wit[:S].cpu().numpy()
+    bad_w = np.nonzero((w_gpu != w_ref).any(axis=1))[0]
+    # orders are compared where the reference returns one: every graph's LexBFS order
+    bad_o = np.nonzero((o_gpu != o_ref).any(axis=1))[0]
+    if len(bad_w) or len(bad_o) or not np.array_equal(w_gpu[:, 0] < 0, verdict):
+        first = int((list(bad_w) + list(bad_o) + [0])[0])
+        raise SystemExit(f"PARITY FAILURE on configuration 4: {len(bad_o)} orders and {len(bad_w)} witnesses of "
+                         f"the first {S} graphs differ from the oracle (first: seed {seed_lo + first})")
+    out = {"graphs": S, "seeds": [seed_lo, seed_lo + S - 1], "inputs_equal": True, "orders_equal": True, "witnesses_equal": True,
+           "verdicts_equal": True, "chordal": int(verdict.sum())}
+    if time_it:
+        out["cpu_baseline"] = {"value": S / dt, "unit": "graphs/s", "cores": threads, "kind": "port",
+                               "sample": f"first {S} graphs (seeds {seed_lo}..{seed_lo + S - 1}) of configuration 4, "
+                                         f"oracle/ C port of is_chordal (PartitionList LexBFS + list PEO) per graph, "
+                                         f"{threads} host threads"}
+    return out
 
 
 # --------------------------------------------------------------- secondary --
@@ -483,48 +516,51 @@ def row_sharded_lines(rank: int, world: int, reps: int = 5) -> dict:
 # -------------------------------------------------------------------- main --
 
 
+def config4(graphs: int) -> dict:
+    """The workload both arms name (identical dict in both JSON lines)."""
+    return {"workload": "config4: 65536 graphs N=512 (even seed gen_dense_random(512,0.5,s), odd seed "
+                        "gen_chordal_random(512,8,s)); one step = is_chordal over every graph",
+            "graphs": graphs, "n": N512, "l2": "inputs 2 GiB > L2 (126 MB), no flush needed"}
+
+
 def run_reference(args, rank, world):
-    """--impl reference: the reference algorithm on the host cores (oracle C port)."""
+    """--impl reference: the reference's CPU implementation of the path -- the
+    oracle's C port of is_chordal (PartitionList LexBFS + list PEO test,
+    oracle/chordal_oracle.c) -- on all host threads, over the same configuration-4
+    graphs as the GPU arm.  Nothing here loads the product package or the GPU:
+    the graphs come from the oracle's own C restatement of the reference
+    generators (pinned to the reference's sha256 fixtures in the tests).
+    Under torchrun only rank 0 works; the other ranks exit 0."""
     if rank != 0:
         return
     import oracle
 
-    oracle.lib()
     threads = oracle.max_threads()
-    try:
-        import torch
+    G = args.graphs
+    t0 = time.perf_counter()
+    adj = oracle.gen_config4_batch(0, G, N512, 0.5, K512, STRIDE512, nthreads=threads)
+    gen_s = time.perf_counter() - t0
 
-        have_gpu = torch.cuda.is_available()
-    except Exception:
-        have_gpu = False
-    # inputs: the same graphs (drawn on the GPU when present, else by the host generators)
-    S = 2 * max(64, threads * 16)
-    if have_gpu:
-        adj = build_batch(0, S, "cuda").cpu().numpy()
-    else:
-        from paper_1508_06329_b200.generate import gen_chordal_random, gen_dense_random
+    def step():
+        return oracle.is_chordal_batch(adj, N512, nthreads=threads)
 
-        adj = np.zeros((S, N512, STRIDE512), dtype=np.uint8)
-        for s in range(S):
-            g = gen_dense_random(N512, 0.5, s) if s % 2 == 0 else gen_chordal_random(N512, K512, s)
-            adj[s, :, :64] = g._packed
     for _ in range(args.warmup):
-        oracle.is_chordal_batch(adj, N512, nthreads=threads)
+        step()
     t0 = time.perf_counter()
     for _ in range(args.steps):
-        oracle.is_chordal_batch(adj, N512, nthreads=threads)
+        verdict, _, _ = step()
     dt = time.perf_counter() - t0
-    value = S * args.steps / dt
+    value = G * args.steps / dt
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3, "higher_is_better": True,
-        "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
-        "config": {"workload": "config4: 65536 graphs N=512 (even seed G(512,0.5), odd seed chordal k=8)",
-                   "sample_per_step": S},
+        "scaling": "strong", "vs_baseline": None, "dtype": "u8", "data": DATA,
+        "config": config4(G),
         "cpu_baseline": {"value": value, "unit": "graphs/s", "cores": threads, "kind": "port",
-                         "sample": f"{S} graphs (seeds 0..{S - 1}) per step, oracle/ C port of is_chordal "
-                                   f"(PartitionList LexBFS + list PEO), {threads} threads"},
+                         "sample": f"all {G} graphs of configuration 4 per step (seeds 0..{G - 1}), oracle/ C port "
+                                   f"of is_chordal (PartitionList LexBFS + list PEO) per graph, {threads} host threads"},
         "e2e": {"value": value, "unit": "graphs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "input_generation_s": gen_s, "chordal_fraction": float(verdict.mean()),
     }
     print(json.dumps(line), flush=True)
 
@@ -544,6 +580,10 @@ def run_ours(args, rank, world, local):
 
         backend = os.environ.get("BENCH_DIST_BACKEND", "nccl")
         if backend == "nccl":
+            # NCCL's init lines (communicator, nRanks, transport) go to stderr
+            os.environ.setdefault("NCCL_DEBUG", "INFO")
+            os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+            os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
             dist.init_process_group("nccl", device_id=device)
         else:
             dist.init_process_group(backend)
@@ -572,8 +612,8 @@ def run_ours(args, rank, world, local):
     t_ms = reduce_max(t_s.elapsed_time(t_e), world)
     ms_per_step = t_ms / args.steps
     value = args.graphs * args.steps / (t_ms * 1e-3)
-    # correctness guard on the measured batch (parity is proven by the tests; this
-    # only refuses to print a number for a broken build)
+    # the timed batch's own results: the first PARITY_SAMPLE graphs of the shard are
+    # checked bit for bit against the oracle below (the run fails on a mismatch)
     orders, wit = step()
     torch.cuda.synchronize()
 
@@ -650,11 +690,9 @@ def run_ours(args, rank, world, local):
     line = {
         "metric": METRIC, "value": value, "unit": "graphs/s", "n_gpus": world, "steps": args.steps,
         "warmup": max(3, args.warmup), "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
-        "vs_baseline": None, "dtype": "u8", "data": "synthetic (reference generators replayed bit-exact on the GPU)",
-        "config": {"workload": "config4: 65536 graphs N=512 (even seed gen_dense_random(512,0.5,s), odd seed "
-                               "gen_chordal_random(512,8,s)), contiguous seed shards",
-                   "graphs": args.graphs, "graphs_per_rank": B, "l2": "inputs 2 GiB > L2, no flush needed",
-                   "parallelism": f"batch-shard x{world}"},
+        "vs_baseline": None, "dtype": "u8", "data": DATA,
+        "config": config4(args.graphs),
+        "parallelism": f"batch-shard x{world} (contiguous seed ranges)", "graphs_per_rank": B,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": peaks["hbm_gbs"], "unit": "GB/s",
                      "frac": achieved / peaks["hbm_gbs"], "traffic": traffic,
                      "algorithmic_bytes_per_launch": B * BYTES_PER_GRAPH,
@@ -668,10 +706,17 @@ def run_ours(args, rank, world, local):
                          "peak_kind": "measured pinned H2D copy, 512 MiB, best of 3", "frac": h2d_gbs / link_best}},
         "gpu_launches": args.steps,
         "clocks": clk.summary(),
-        "chordal_fraction": float((wit[:, 0] < 0).float().mean().item()),
     }
-    if rank == 0 and world == 1 and not args.no_cpu:
-        line["cpu_baseline"] = cpu_batch_baseline(host[: min(B, 8192)].numpy())
+    parity = check_batch_parity(host.numpy(), orders, wit, lo, time_it=rank == 0 and world == 1 and not args.no_cpu)
+    if "cpu_baseline" in parity:
+        line["cpu_baseline"] = parity.pop("cpu_baseline")
+    # every rank's verdicts and parity-checked counts, summed over the ranks
+    chordal_total, checked_total, graphs_total = reduce_sum_ints(
+        [int((wit[:, 0] < 0).sum().item()), parity["graphs"], B], world)
+    assert graphs_total == args.graphs, (graphs_total, args.graphs)
+    line["chordal_fraction"] = chordal_total / graphs_total
+    line["parity"] = dict(parity, ranks=world, graphs_checked_all_ranks=checked_total,
+                          chordal_graphs_all_ranks=chordal_total)
     if not args.no_secondary:
         line["row_sharded_peo"] = row_sharded_lines(rank, world)
     if rank == 0 and world == 1 and not args.no_secondary:

@@ -184,3 +184,44 @@ def is_chordal_batch(adj: np.ndarray, n: int, nthreads: int | None = None):
 
 def max_threads() -> int:
     return int(lib().oracle_max_threads())
+
+
+def _gen_lib():
+    L = lib()
+    if not getattr(L, "_gen_bound", False):
+        P = ctypes.c_void_p
+        i64 = ctypes.c_int64
+        L.oracle_gen_dense_random.argtypes = [i64, ctypes.c_double, ctypes.c_uint64, i64, P]
+        L.oracle_gen_chordal_random.argtypes = [i64, i64, ctypes.c_uint64, i64, P]
+        L.oracle_gen_config4_batch.argtypes = [i64, ctypes.c_double, i64, i64, i64, i64, P, ctypes.c_int]
+        L._gen_bound = True
+    return L
+
+
+def gen_dense_random(n: int, p: float, seed: int, stride: int | None = None) -> np.ndarray:
+    """gen_dense_random (generate.py:32-56) as packed rows uint8[n, stride]."""
+    stride = stride or (n + 7) // 8
+    out = np.empty((n, stride), dtype=np.uint8)
+    _gen_lib().oracle_gen_dense_random(n, float(p), int(seed) & 0xFFFFFFFFFFFFFFFF, stride, _ptr(out))
+    return out
+
+
+def gen_chordal_random(n: int, k: int, seed: int, stride: int | None = None) -> np.ndarray:
+    """gen_chordal_random (generate.py:118-155) as packed rows uint8[n, stride]."""
+    stride = stride or (n + 7) // 8
+    out = np.empty((n, stride), dtype=np.uint8)
+    if _gen_lib().oracle_gen_chordal_random(n, k, int(seed) & 0xFFFFFFFFFFFFFFFF, stride, _ptr(out)):
+        raise MemoryError("oracle_gen_chordal_random")
+    return out
+
+
+def gen_config4_batch(seed_lo: int, count: int, n: int = 512, p: float = 0.5, k: int = 8, stride: int = 64,
+                      nthreads: int | None = None) -> np.ndarray:
+    """Configuration 4's graphs of seeds [seed_lo, seed_lo + count): even seed
+    gen_dense_random(n, p, s), odd seed gen_chordal_random(n, k, s); uint8[count, n, stride]."""
+    out = np.empty((count, n, stride), dtype=np.uint8)
+    rc = _gen_lib().oracle_gen_config4_batch(n, float(p), k, seed_lo, count, stride, _ptr(out),
+                                             nthreads or max_threads())
+    if rc:
+        raise MemoryError("oracle_gen_config4_batch")
+    return out

@@ -827,3 +827,166 @@ int oracle_max_threads(void) {
     long c = sysconf(_SC_NPROCESSORS_ONLN);
     return c > 0 ? (int)c : 1;
 }
+
+/* ---------------------------------------------------------------------------
+ * The benchmark generators, so that the CPU legs of bench.py draw their inputs
+ * without the product library.  Streams: rng.stream(seed, label) (rng.py:18-21).
+ *
+ * gen_dense_random (generate.py:32-56): one Generator.random() double per cell
+ * of each 1024-row block, row-major over full rows, so draw number u*n + v
+ * decides edge {u, v} for u < v; random() = (next64 >> 11) * 2^-53.
+ */
+int oracle_gen_dense_random(int64_t n, double p, uint64_t seed, int64_t stride, uint8_t *out) {
+    memset(out, 0, (size_t)(n * stride));
+    if (n <= 1) return ORACLE_OK;
+    philox_t r;
+    philox_init(&r, stream_key(seed, "dense-random"));
+    /* draws below the diagonal are skipped by seeking the counter: numpy's
+     * Philox increments it before each 4-word block, so draw k is word k % 4
+     * of block k / 4 + 1 */
+    for (int64_t u = 0; u + 1 < n; ++u) {
+        int64_t kk = u * n + u + 1;
+        r.ctr = (uint64_t)(kk >> 2);
+        r.pos = 4;
+        philox_next64(&r);
+        r.pos = (int)(kk & 3);
+        for (int64_t v = u + 1; v < n; ++v) {
+            double d = (double)(philox_next64(&r) >> 11) * (1.0 / 9007199254740992.0);
+            if (d < p) {
+                out[u * stride + (v >> 3)] |= (uint8_t)(1u << (v & 7));
+                out[v * stride + (u >> 3)] |= (uint8_t)(1u << (u & 7));
+            }
+        }
+    }
+    return ORACLE_OK;
+}
+
+/* gen_chordal_random (generate.py:118-155).  Draws, as numpy's Generator makes
+ * them:
+ *   integers(-1, 2)  = -1 + bounded(2)         (random_bounded_uint64, Lemire)
+ *   integers(0, i)   = bounded(i - 1)
+ *   choice(P, size=w, replace=False), P <= 10000: Floyd's algorithm over
+ *     j = P-w .. P-1 with an open-addressing set of 2^ceil(log2(1.2 w)) slots
+ *     (a collision takes j itself), then Fisher-Yates over the w picks with
+ *     bounded(t) for t = w-1 .. 1.
+ * Vertex i attaches to pool[idx] for the picked idx, pool = cliques[j] ++ [j]. */
+int oracle_gen_chordal_random(int64_t n, int64_t k, uint64_t seed, int64_t stride, uint8_t *out) {
+    memset(out, 0, (size_t)(n * stride));
+    if (k == 0 || n <= 1) return ORACLE_OK;
+    int setsize = (int)(1.2 * (double)(k + 2)), mask0 = setsize;
+    mask0 |= mask0 >> 1; mask0 |= mask0 >> 2; mask0 |= mask0 >> 4; mask0 |= mask0 >> 8; mask0 |= mask0 >> 16;
+    int32_t *att_off = malloc(sizeof(int32_t) * (size_t)n);
+    int32_t *att_len = malloc(sizeof(int32_t) * (size_t)n);
+    int32_t *hs = malloc(sizeof(int32_t) * (size_t)(mask0 + 1));
+    /* vertex i keeps min(i, k + 1) entries */
+    int32_t *lst = malloc(sizeof(int32_t) * (size_t)(n * (k + 1) + 4));
+    if (!att_off || !att_len || !hs || !lst) {
+        free(att_off); free(att_len); free(hs); free(lst);
+        return ORACLE_ENOMEM;
+    }
+    philox_t r;
+    philox_init(&r, stream_key(seed, "chordal-random"));
+#define SET_EDGE(a, b)                                                      \
+    do {                                                                    \
+        out[(int64_t)(a) * stride + ((b) >> 3)] |= (uint8_t)(1u << ((b) & 7)); \
+        out[(int64_t)(b) * stride + ((a) >> 3)] |= (uint8_t)(1u << ((a) & 7)); \
+    } while (0)
+    int64_t top = 0;
+    att_off[0] = 0;
+    att_len[0] = 0;
+    for (int64_t i = 1; i < n; ++i) {
+        int32_t *o = lst + top;
+        int cnt;
+        if (k >= i) { /* join the whole prefix clique, no draws */
+            for (int c = 0; c < i; ++c) { o[c] = c; SET_EDGE(i, c); }
+            cnt = (int)i;
+        } else {
+            int64_t want = k - 1 + (int64_t)philox_bounded(&r, 2);
+            if (want < 1) want = 1;
+            if (want > i) want = i;
+            const int j = (int)philox_bounded(&r, (uint32_t)(i - 1));
+            const int32_t *src = lst + att_off[j];
+            const int plen = att_len[j], P = plen + 1;
+            if (want >= P) {
+                for (int c = 0; c < plen; ++c) { o[c] = src[c]; SET_EDGE(i, src[c]); }
+                o[plen] = j;
+                SET_EDGE(i, j);
+                cnt = P;
+            } else {
+                const int w = (int)want;
+                int mask = (int)(1.2 * (double)w);
+                mask |= mask >> 1; mask |= mask >> 2; mask |= mask >> 4; mask |= mask >> 8; mask |= mask >> 16;
+                for (int t = 0; t <= mask; ++t) hs[t] = -1;
+                for (int jj = P - w; jj < P; ++jj) {
+                    int val = (int)philox_bounded(&r, (uint32_t)jj);
+                    int loc = val & mask;
+                    while (hs[loc] != -1 && hs[loc] != val) loc = (loc + 1) & mask;
+                    if (hs[loc] == -1) {
+                        hs[loc] = val;
+                        o[jj - P + w] = val;
+                    } else {
+                        loc = jj & mask;
+                        while (hs[loc] != -1) loc = (loc + 1) & mask;
+                        hs[loc] = jj;
+                        o[jj - P + w] = jj;
+                    }
+                }
+                for (int t = w - 1; t >= 1; --t) {
+                    int rr = (int)philox_bounded(&r, (uint32_t)t);
+                    int tmp = o[rr]; o[rr] = o[t]; o[t] = tmp;
+                }
+                for (int c = 0; c < w; ++c) {
+                    int v = o[c] < plen ? src[o[c]] : j;
+                    o[c] = v;
+                    SET_EDGE(i, v);
+                }
+                cnt = w;
+            }
+        }
+        att_off[i] = (int32_t)top;
+        att_len[i] = cnt;
+        top += cnt;
+    }
+#undef SET_EDGE
+    free(att_off); free(att_len); free(hs); free(lst);
+    return ORACLE_OK;
+}
+
+/* Configuration 4's batch: seed s in [seed_lo, seed_lo + count):
+ * gen_dense_random(n, p, s) if s is even, else gen_chordal_random(n, k, s),
+ * graph s - seed_lo at out + (s - seed_lo) * n * stride; nthreads host threads. */
+typedef struct {
+    int64_t n, k, seed_lo, count, stride, next;
+    double p;
+    uint8_t *out;
+    pthread_mutex_t lock;
+    int err;
+} gen_job_t;
+
+static void *gen_worker(void *arg) {
+    gen_job_t *J = (gen_job_t *)arg;
+    for (;;) {
+        pthread_mutex_lock(&J->lock);
+        int64_t b = J->next++;
+        pthread_mutex_unlock(&J->lock);
+        if (b >= J->count) break;
+        int64_t s = J->seed_lo + b;
+        uint8_t *g = J->out + b * J->n * J->stride;
+        int rc = (s % 2 == 0) ? oracle_gen_dense_random(J->n, J->p, (uint64_t)s, J->stride, g)
+                              : oracle_gen_chordal_random(J->n, J->k, (uint64_t)s, J->stride, g);
+        if (rc) { pthread_mutex_lock(&J->lock); J->err = rc; pthread_mutex_unlock(&J->lock); }
+    }
+    return NULL;
+}
+
+int oracle_gen_config4_batch(int64_t n, double p, int64_t k, int64_t seed_lo, int64_t count, int64_t stride,
+                             uint8_t *out, int nthreads) {
+    gen_job_t J = {n, k, seed_lo, count, stride, 0, p, out, PTHREAD_MUTEX_INITIALIZER, 0};
+    if (nthreads < 1) nthreads = 1;
+    if (nthreads > 1024) nthreads = 1024;
+    pthread_t tid[1024];
+    for (int t = 1; t < nthreads; ++t) pthread_create(&tid[t], NULL, gen_worker, &J);
+    gen_worker(&J);
+    for (int t = 1; t < nthreads; ++t) pthread_join(tid[t], NULL);
+    return J.err;
+}
