@@ -173,6 +173,22 @@ int chordal_peo_csr_witness(const int64_t *indptr_dev, const int32_t *indices_de
 int chordal_peo_csr(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, const int32_t *pos_dev,
                     const int32_t *parent_dev, uint64_t *key_dev, int32_t *witness_dev, void *stream);
 
+/* ---- left neighbourhoods (graph.py:284-302) ----------------------------- */
+
+/* left_neighborhoods(g, ordering): LN(v) = the neighbours of v placed before
+ * it, parent(v) = the member of LN(v) with the greatest position (-1 if
+ * none).  order_dev/pos_dev: a 0-based permutation and its inverse.  Each
+ * output is optional (NULL = not written): ln_rows_dev uint8[n][stride] (LN
+ * rows in the input's packed layout, padding zero), parent_dev int32[n],
+ * ln_size_dev int32[n] = |LN(v)|, deg_dev int32[n] = deg(v).  The sizes feed
+ * the reference's list-scan read count (ScanStats, peo.py:100-149). */
+int chordal_left_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, const int32_t *order_dev,
+                       const int32_t *pos_dev, uint8_t *ln_rows_dev, int32_t *parent_dev, int32_t *ln_size_dev,
+                       int32_t *deg_dev, void *stream);
+/* The same on CSR adjacency (deg(v) = indptr[v+1] - indptr[v]). */
+int chordal_left_csr(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, const int32_t *order_dev,
+                     const int32_t *pos_dev, int32_t *parent_dev, int32_t *ln_size_dev, void *stream);
+
 /* The host-buffer pipeline over a caller-provided device workspace of
  * chordal_dense_host_workspace_bytes(n, m) bytes (256-byte aligned; m = the edge
  * count, Graph.m), reused across calls, on the calling thread's default stream. */

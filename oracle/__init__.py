@@ -53,6 +53,7 @@ def lib():
         L.oracle_lexbfs_arbitrated.argtypes = [P, i64, i64, ctypes.c_int, ctypes.c_uint64, P]
         L.oracle_is_peo.argtypes = [P, i64, i64, P, P]
         L.oracle_is_peo_csr.argtypes = [P, P, i64, P, P]
+        L.oracle_peo_lists_stats.argtypes = [P, P, i64, P, P, P, P, P]
         L.oracle_is_chordal_batch.argtypes = [P, i64, i64, i64, i64, P, P, P, ctypes.c_int]
         L.oracle_splitmix64.argtypes = [ctypes.c_uint64]
         L.oracle_splitmix64.restype = ctypes.c_uint64
@@ -157,6 +158,33 @@ def is_peo_csr(indptr, indices, n: int, order0) -> tuple[bool, tuple[int, int, i
     if rc < 0:
         raise MemoryError("oracle_is_peo_csr")
     return (True, None) if rc == 1 else (False, (int(w[0]), int(w[1]), int(w[2])))
+
+
+def peo_lists_stats(indptr, indices, n: int, order0):
+    """_is_peo_lists with its ScanStats count (peo.py:100-149):
+    (ok, witness0|None, parent int32[n], ln_size int32[n], reads)."""
+    ip = np.ascontiguousarray(indptr, dtype=np.int64)
+    ix = np.ascontiguousarray(indices, dtype=np.int32)
+    o = np.ascontiguousarray(order0, dtype=np.int32)
+    w = np.full(3, -1, dtype=np.int32)
+    parent = np.empty(max(n, 1), dtype=np.int32)
+    lnsz = np.empty(max(n, 1), dtype=np.int32)
+    reads = ctypes.c_int64()
+    rc = lib().oracle_peo_lists_stats(_ptr(ip), _ptr(ix), n, _ptr(o), _ptr(w), _ptr(parent), _ptr(lnsz),
+                                      ctypes.byref(reads))
+    if rc < 0:
+        raise MemoryError("oracle_peo_lists_stats")
+    wit = None if rc == 1 else (int(w[0]), int(w[1]), int(w[2]))
+    return rc == 1, wit, parent[:n], lnsz[:n], int(reads.value)
+
+
+def csr_from_packed(packed: np.ndarray, n: int):
+    """(indptr int64, indices int32) of packed rows (ascending neighbours)."""
+    rows = np.unpackbits(np.asarray(packed, dtype=np.uint8), axis=1, bitorder="little", count=n).astype(bool) \
+        if n else np.zeros((0, 0), bool)
+    indptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(rows.sum(axis=1), out=indptr[1:])
+    return indptr, (np.flatnonzero(rows.reshape(-1)) % max(n, 1)).astype(np.int32)
 
 
 def is_chordal(packed: np.ndarray, n: int):

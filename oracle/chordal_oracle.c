@@ -777,6 +777,74 @@ int oracle_is_peo_csr(const int64_t *indptr, const int32_t *indices, int64_t n,
     return ok;
 }
 
+/* _is_peo_lists with its instrumentation (peo.py:100-149), literally: the
+ * list-element reads of the four scans (ScanStats.reads, peo.py:48-56,
+ * 146-148), and scan 1's parents and left-list sizes -- what
+ * left_neighborhoods (graph.py:284-302) defines as parent(v) and |LN(v)|.
+ * parent_out / ln_size_out / reads_out may be NULL. */
+int oracle_peo_lists_stats(const int64_t *indptr, const int32_t *indices, int64_t n, const int32_t *order,
+                           int32_t *witness, int32_t *parent_out, int32_t *ln_size_out, int64_t *reads_out) {
+    witness[0] = witness[1] = witness[2] = -1;
+    if (reads_out) *reads_out = 0;
+    if (n <= 0) return 1;
+    int32_t *pos = malloc(sizeof(int32_t) * n);
+    int32_t *parent = malloc(sizeof(int32_t) * n);
+    int32_t *lnsz = calloc((size_t)n, sizeof(int32_t));
+    uint8_t *visited = calloc((size_t)n, 1);
+    if (!pos || !parent || !lnsz || !visited) {
+        free(pos); free(parent); free(lnsz); free(visited);
+        return -ORACLE_ENOMEM;
+    }
+    for (int64_t k = 0; k < n; ++k) pos[order[k]] = (int32_t)k;
+    int64_t reads = 0;
+    /* scan 1 (peo.py:106-121) */
+    for (int64_t v = 0; v < n; ++v) {
+        int32_t best = -1, best_pos = -1;
+        for (int64_t e = indptr[v]; e < indptr[v + 1]; ++e) {
+            int32_t w = indices[e];
+            reads += 1;
+            if (pos[w] < pos[v]) {
+                lnsz[v] += 1;
+                if (pos[w] > best_pos) { best_pos = pos[w]; best = w; }
+            }
+        }
+        parent[v] = best;
+    }
+    /* scans 2-4 (peo.py:124-145); ln[y] holds y's left neighbours in adjacency order */
+    int ok = 1;
+    for (int64_t x = 0; x < n && ok; ++x) {
+        for (int64_t e = indptr[x]; e < indptr[x + 1]; ++e) {
+            int32_t w = indices[e];
+            if (pos[w] < pos[x]) { visited[w] = 1; reads += 1; }
+        }
+        for (int64_t e = indptr[x]; e < indptr[x + 1] && ok; ++e) {
+            int32_t y = indices[e];
+            reads += 1;
+            if (parent[y] != x) continue;
+            for (int64_t f = indptr[y]; f < indptr[y + 1]; ++f) {
+                int32_t z = indices[f];
+                if (pos[z] >= pos[y]) continue;
+                reads += 1;
+                if (z != x && !visited[z]) {
+                    witness[0] = y; witness[1] = (int32_t)x; witness[2] = z;
+                    ok = 0;
+                    break;
+                }
+            }
+        }
+        if (!ok) break;
+        for (int64_t e = indptr[x]; e < indptr[x + 1]; ++e) {
+            int32_t w = indices[e];
+            if (pos[w] < pos[x]) { visited[w] = 0; reads += 1; }
+        }
+    }
+    if (parent_out) memcpy(parent_out, parent, sizeof(int32_t) * n);
+    if (ln_size_out) memcpy(ln_size_out, lnsz, sizeof(int32_t) * n);
+    if (reads_out) *reads_out = reads;
+    free(pos); free(parent); free(lnsz); free(visited);
+    return ok;
+}
+
 /* ---------------------------------------------------------------------------
  * is_chordal (peo.py:177-202) over a batch of independent dense graphs, with
  * `nthreads` host threads (the CPU baseline for the batched configuration).

@@ -43,6 +43,8 @@ SIGNATURES = {
     "chordal_peo_csr_witness": [_P, _P, _I64, _P, _P, _P, _P],
     "chordal_peo_csr": [_P, _P, _I64, _P, _P, _P, _P, _P],
     "chordal_dense_to_csr": [_P, _I64, _I64, _P, _P, _P],
+    "chordal_left_dense": [_P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P],
+    "chordal_left_csr": [_P, _P, _I64, _P, _P, _P, _P, _P],
     "chordal_permute_dense": [_P, _I64, _I64, _P, _P, _P],
     "chordal_is_chordal_batch": [_P, _I64, _I64, _I64, _P, _P, _P],
     "chordal_is_chordal_batch_host": [_P, _I64, _I64, _I64, _P, _P, _I64],

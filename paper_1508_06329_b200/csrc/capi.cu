@@ -43,6 +43,10 @@ int launch_gen_chordal_edges(int64_t, int64_t, int64_t, uint32_t, int32_t *, int
                              cudaStream_t);
 int launch_gen_chordal_random(uint8_t *, int64_t, int64_t, int64_t, int64_t, int64_t, int64_t, uint32_t, int32_t *,
                               cudaStream_t);
+int launch_left_dense(const uint8_t *, int64_t, int64_t, const int32_t *, const int32_t *, uint8_t *, int32_t *,
+                      int32_t *, int32_t *, cudaStream_t);
+int launch_left_csr(const int64_t *, const int32_t *, int64_t, const int32_t *, const int32_t *, int32_t *, int32_t *,
+                    cudaStream_t);
 void keep_pool_bytes(size_t bytes) {
     int dev = 0;
     cudaMemPool_t pool;
@@ -143,6 +147,17 @@ static int count_edges_sync(const uint8_t *adj, int64_t n, int64_t stride, cudaS
     return rc;
 }
 
+// indptr[n] <= 2m, or EINVAL: buffers sized from a caller's m must hold every
+// adjacency entry (one 8-byte read back + a sync of the stream; only on the
+// slot-engine routes, whose searches take milliseconds to seconds).
+static int check_nnz(const int64_t *indptr, int64_t n, int64_t m, cudaStream_t s) {
+    int64_t tot = 0;
+    if (cudaMemcpyAsync(&tot, indptr + n, sizeof(int64_t), cudaMemcpyDeviceToHost, s) != cudaSuccess ||
+        cudaStreamSynchronize(s) != cudaSuccess)
+        return CHORDAL_ECUDA;
+    return (tot < 0 || tot > 2 * m) ? CHORDAL_EINVAL : CHORDAL_OK;
+}
+
 size_t chordal_dense_workspace_bytes(int64_t n, int64_t m) {
     if (n < 0 || m < 0) return 0;
     return DenseWs(n, m).total;
@@ -170,6 +185,8 @@ int chordal_lexbfs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int6
     int64_t *indptr = reinterpret_cast<int64_t *>(w + L.indptr);
     int32_t *indices = reinterpret_cast<int32_t *>(w + L.indices);
     rc = launch_dense_degrees(adj_dev, n, stride, indptr, s);
+    if (rc) return rc;
+    rc = check_nnz(indptr, n, m, s);  // the workspace was sized from m
     if (rc) return rc;
     rc = launch_dense_fill(adj_dev, n, stride, indptr, indices, 2 * m + 1, s);
     if (rc) return rc;
@@ -283,7 +300,8 @@ int chordal_is_chordal_dense_host(const uint8_t *adj_host, int64_t n, int64_t ro
             break;
         }
         order = reinterpret_cast<int32_t *>(adj + adj_bytes);
-        if (stride != row_bytes && cudaMemsetAsync(adj, 0, adj_bytes, s) != cudaSuccess) { rc = CHORDAL_ECUDA; break; }
+        // the copy writes (n+7)/8 bytes per row: the rest of the pitch must be zero
+        if (stride != (n + 7) / 8 && cudaMemsetAsync(adj, 0, adj_bytes, s) != cudaSuccess) { rc = CHORDAL_ECUDA; break; }
         if (cudaMemcpy2DAsync(adj, stride, adj_host, row_bytes, (n + 7) / 8, n, cudaMemcpyHostToDevice, s) !=
             cudaSuccess) { rc = CHORDAL_ECUDA; break; }
         if (n > 1024) {  // the engine choice (CSR route) and its thread count depend on the density
@@ -343,7 +361,8 @@ int chordal_is_chordal_dense_host_ws(const uint8_t *adj_host, int64_t n, int64_t
     cudaStream_t s = cudaStreamPerThread;
     int rc = CHORDAL_OK;
     do {
-        if (stride != row_bytes && cudaMemsetAsync(adj, 0, adj_bytes, s) != cudaSuccess) { rc = CHORDAL_ECUDA; break; }
+        // the copy writes (n+7)/8 bytes per row: the rest of the pitch must be zero
+        if (stride != (n + 7) / 8 && cudaMemsetAsync(adj, 0, adj_bytes, s) != cudaSuccess) { rc = CHORDAL_ECUDA; break; }
         if (cudaMemcpy2DAsync(adj, stride, adj_host, row_bytes, (n + 7) / 8, n, cudaMemcpyHostToDevice, s) !=
             cudaSuccess) { rc = CHORDAL_ECUDA; break; }
         rc = chordal_is_chordal_dense(adj, n, stride, m, tie_rule, seed, order, order + n, ws, wsb, wit, s);
@@ -377,6 +396,8 @@ int chordal_lexbfs_csr(const int64_t *indptr_dev, const int32_t *indices_dev, in
         seed = splitmix64(splitmix64(seed) ^ (uint64_t)crc32_str("lexbfs-partition"));
     else if (tie_rule == CHORDAL_TIE_SEEDED_LABELS)
         seed = splitmix64(splitmix64(seed) ^ (uint64_t)crc32_str("lexbfs-labels"));
+    int rc = check_nnz(indptr_dev, n, m, as_stream(stream));
+    if (rc) return rc;
     return launch_lexbfs_csr(indptr_dev, indices_dev, n, m, tie_rule, seed, current_cell(crc32_str("current")),
                              order_dev, pos_dev, parent_dev, ws, as_stream(stream));
 }
@@ -444,6 +465,28 @@ int chordal_peo_csr(const int64_t *indptr_dev, const int32_t *indices_dev, int64
     return chordal_peo_csr_witness(indptr_dev, indices_dev, n, pos_dev, key_dev, witness_dev, stream);
 }
 
+int chordal_left_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, const int32_t *order_dev,
+                       const int32_t *pos_dev, uint8_t *ln_rows_dev, int32_t *parent_dev, int32_t *ln_size_dev,
+                       int32_t *deg_dev, void *stream) {
+    int rc = check_dense(adj_dev, n, stride);
+    if (rc) return rc;
+    if (n == 0) return CHORDAL_OK;
+    if (!order_dev || !pos_dev) return CHORDAL_EINVAL;
+    if (ln_rows_dev && reinterpret_cast<uintptr_t>(ln_rows_dev) % 16 != 0) return CHORDAL_EINVAL;
+    return launch_left_dense(adj_dev, n, stride, order_dev, pos_dev, ln_rows_dev, parent_dev, ln_size_dev, deg_dev,
+                             as_stream(stream));
+}
+
+int chordal_left_csr(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, const int32_t *order_dev,
+                     const int32_t *pos_dev, int32_t *parent_dev, int32_t *ln_size_dev, void *stream) {
+    if (n < 0) return CHORDAL_EINVAL;
+    if (n == 0) return CHORDAL_OK;
+    if (n > 0x7FFFFFFF) return CHORDAL_ETOOLARGE;
+    if (!indptr_dev || !indices_dev || !order_dev || !pos_dev) return CHORDAL_EINVAL;
+    return launch_left_csr(indptr_dev, indices_dev, n, order_dev, pos_dev, parent_dev, ln_size_dev,
+                           as_stream(stream));
+}
+
 int chordal_dense_to_csr(const uint8_t *adj_dev, int64_t n, int64_t stride, int64_t *indptr_dev,
                          int32_t *indices_dev, void *stream) {
     int rc = check_dense(adj_dev, n, stride);
@@ -470,7 +513,12 @@ int chordal_permute_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, con
 int chordal_is_chordal_batch(const uint8_t *adj_dev, int64_t batch, int64_t n, int64_t stride,
                              int32_t *orders_dev, int32_t *witness_dev, void *stream) {
     if (batch < 0 || n < 0) return CHORDAL_EINVAL;
-    if (batch == 0 || n == 0) return CHORDAL_OK;
+    if (batch == 0) return CHORDAL_OK;
+    if (n == 0) {  // every empty graph is chordal: witness (-1, -1, -1)
+        if (!witness_dev) return CHORDAL_EINVAL;
+        return cudaMemsetAsync(witness_dev, 0xFF, sizeof(int32_t) * 3 * (size_t)batch, as_stream(stream)) ==
+                       cudaSuccess ? CHORDAL_OK : CHORDAL_ECUDA;
+    }
     if (n > CHORDAL_BATCH_MAX_N) return CHORDAL_ETOOLARGE;
     int rc = check_dense(adj_dev, n, stride);
     if (rc) return rc;
@@ -497,6 +545,9 @@ static int batch_host_run(const uint8_t *adj_host, int64_t batch, int64_t n, int
     const size_t gbytes = (size_t)n * stride;
     constexpr int NB = 3;  // H2D of chunk c+1 and D2H of c-1 overlap the search of c
     const size_t per_set = batch_host_set_bytes(n, chunk);
+    // one flat copy only when host rows, device rows and the vertex bytes coincide;
+    // otherwise (n+7)/8 bytes per row into rows whose padding was zeroed once
+    const bool flat = row_bytes == stride && stride == (n + 7) / 8;
     cudaEvent_t ready = nullptr;
     cudaStream_t st[NB] = {};
     uint8_t *buf[NB] = {};
@@ -516,14 +567,14 @@ static int batch_host_run(const uint8_t *adj_host, int64_t batch, int64_t n, int
             rc = CHORDAL_ECUDA;
             break;
         }
-        if (stride != row_bytes && cudaMemsetAsync(buf[k], 0, gbytes * chunk, st[k]) != cudaSuccess)
+        if (!flat && cudaMemsetAsync(buf[k], 0, gbytes * chunk, st[k]) != cudaSuccess)
             rc = CHORDAL_ECUDA;
     }
     for (int64_t b0 = 0, c = 0; b0 < batch && rc == CHORDAL_OK; b0 += chunk, ++c) {
         const int k = (int)(c % NB);
         const int64_t nb = (batch - b0 < chunk) ? batch - b0 : chunk;
         const uint8_t *src = adj_host + b0 * n * row_bytes;
-        cudaError_t e = (stride == row_bytes)
+        cudaError_t e = flat
                             ? cudaMemcpyAsync(buf[k], src, gbytes * nb, cudaMemcpyHostToDevice, st[k])
                             : cudaMemcpy2DAsync(buf[k], stride, src, row_bytes, (n + 7) / 8, n * nb,
                                                 cudaMemcpyHostToDevice, st[k]);
@@ -547,9 +598,13 @@ static int batch_host_run(const uint8_t *adj_host, int64_t batch, int64_t n, int
 
 static int batch_host_check(const uint8_t *adj_host, int64_t batch, int64_t n, int64_t row_bytes,
                             int32_t *orders_host, int32_t *witness_host) {
-    if (batch < 0 || n < 0 || (batch > 0 && n > 0 && (!adj_host || !orders_host || !witness_host)))
+    if (batch < 0 || n < 0 || (batch > 0 && (!witness_host || (n > 0 && (!adj_host || !orders_host)))))
         return CHORDAL_EINVAL;
-    if (batch == 0 || n == 0) return -1;  // nothing to do
+    if (batch == 0) return -1;  // nothing to do
+    if (n == 0) {  // every empty graph is chordal
+        for (int64_t b = 0; b < 3 * batch; ++b) witness_host[b] = -1;
+        return -1;
+    }
     if (n > CHORDAL_BATCH_MAX_N) return CHORDAL_ETOOLARGE;
     if (row_bytes < (n + 7) / 8) return CHORDAL_EINVAL;
     return CHORDAL_OK;

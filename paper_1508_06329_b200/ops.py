@@ -220,6 +220,28 @@ def peo_csr_witness(indptr, indices, n: int, pos, key, stream=None):
     return wit[:3]
 
 
+def left_dense(rows: DeviceRows, order, pos, want_rows: bool = True, stream=None):
+    """(LN rows uint8[n, stride] or None, parent, |LN|, deg) int32 device tensors
+    (left_neighborhoods, graph.py:284-302)."""
+    torch = _native.require_cuda()
+    n, dev = rows.n, rows.data.device
+    ln = torch.empty((n, rows.stride), dtype=torch.uint8, device=dev) if want_rows else None
+    parent, ln_size, deg = (_i32(torch, n, dev) for _ in range(3))
+    check(lib.chordal_left_dense(rows.ptr, n, rows.stride, ptr(order), ptr(pos), ptr(ln) if want_rows else None,
+                                 ptr(parent), ptr(ln_size), ptr(deg), stream_ptr(stream)), "chordal_left_dense")
+    return ln, parent, ln_size, deg
+
+
+def left_csr(indptr, indices, n: int, order, pos, stream=None):
+    """(parent, |LN|) int32 device tensors of a CSR graph under an ordering."""
+    torch = _native.require_cuda()
+    dev = indptr.device
+    parent, ln_size = _i32(torch, n, dev), _i32(torch, n, dev)
+    check(lib.chordal_left_csr(ptr(indptr), ptr(indices), n, ptr(order), ptr(pos), ptr(parent), ptr(ln_size),
+                               stream_ptr(stream)), "chordal_left_csr")
+    return parent, ln_size
+
+
 def dense_to_csr(rows: DeviceRows, stream=None):
     """Packed rows -> (indptr int64[n+1], indices int32[2m]) on the device."""
     torch = _native.require_cuda()
@@ -242,8 +264,9 @@ def is_chordal_batch(adj, n: int, stride: int, stream=None):
     torch = _native.require_cuda()
     B = int(adj.shape[0])
     orders = torch.empty((max(B, 1), max(n, 1)), dtype=torch.int32, device=adj.device)
+    # empty graphs are chordal: witness (-1, -1, -1) (the library writes it for n == 0 too)
     wit = torch.empty((max(B, 1), 3), dtype=torch.int32, device=adj.device)
-    if B and n:
+    if B:
         check(
             lib.chordal_is_chordal_batch(ptr(adj), B, n, stride, ptr(orders), ptr(wit), stream_ptr(stream)),
             "chordal_is_chordal_batch",

@@ -112,38 +112,44 @@ def is_peo(g, ordering, *, stats: ScanStats | None = None, method: str = "auto")
     return (w0 is None), _witness(w0)
 
 
+def _row0(g, u: int) -> np.ndarray:
+    """Sorted 0-based neighbours of vertex u (one row, host side)."""
+    if hasattr(g, "_packed"):
+        return np.flatnonzero(np.unpackbits(np.asarray(g._packed)[u], bitorder="little", count=int(g.n)))
+    if hasattr(g, "indptr") and hasattr(g, "indices"):
+        ip = np.asarray(g.indptr)
+        return np.asarray(g.indices)[ip[u] : ip[u + 1]].astype(np.int64)
+    return np.asarray(sorted(g.adjacency_lists0()[u]), dtype=np.int64)
+
+
 def _list_scan_reads(g, o: VertexOrdering, w0) -> int:
     """Reads the reference's list scan (peo.py:100-149) performs on this input.
 
-    Instrumentation only (the verdict above comes from the device): scan 1
-    reads every adjacency entry; scans 2-4 read, per parent x in ascending
-    order, ln[x] twice, adj[x] once and ln[y] of each child -- up to the
-    witness, where the scan stops.
+    Instrumentation only (the verdict comes from the device).  Scan 1 reads
+    every adjacency entry; scans 2-4 read, per parent x in ascending order,
+    ln[x] twice, adj[x] once and ln[y] of each child y -- up to the witness,
+    where the scan stops.  deg, |ln| and the parents come from the device
+    (csrc/left.cu), so the count costs O(n) on the host plus the two rows of
+    the witness pair, for dense and CSR inputs alike.
     """
     n = int(g.n)
-    rows = np.unpackbits(np.asarray(g._packed), axis=1, bitorder="little", count=n).astype(bool)
-    pos = o.pos0
-    left = rows & (pos[None, :] < pos[:, None])
-    ln_size = left.sum(axis=1)
-    deg = rows.sum(axis=1)
-    lpos = np.where(left, pos[None, :], -1)
-    has = ln_size > 0
-    parent = np.full(n, -1, dtype=np.int64)
-    parent[has] = o.order0[lpos[has].max(axis=1)]
-    child_ln = np.zeros(n, dtype=np.int64)
-    np.add.at(child_ln, parent[has], ln_size[has])
+    _, parent, ln_size, deg = pipeline.left_arrays(g, o, want_rows=False)
+    ln_size = ln_size.astype(np.int64)
+    has = parent >= 0
+    child_ln = np.bincount(parent[has], weights=ln_size[has], minlength=n).astype(np.int64)
     reads = int(deg.sum())
     if w0 is None:
         return reads + int((2 * ln_size + deg + child_ln).sum())
     v, p, z = w0
     reads += int((2 * ln_size[:p] + deg[:p] + child_ln[:p]).sum())
     reads += int(ln_size[p])
-    nbrs = np.flatnonzero(rows[p])
+    nbrs = _row0(g, p)
     upto = nbrs[nbrs <= v]
     reads += int(upto.size)
     before = upto[(upto < v) & (parent[upto] == p)]
     reads += int(ln_size[before].sum())
-    lny = np.flatnonzero(left[v])
+    nv = _row0(g, v)
+    lny = nv[o.pos0[nv] < o.pos0[v]]
     reads += int(np.searchsorted(lny, z) + 1)
     return reads
 

@@ -54,6 +54,25 @@ def peo_witness(g, o: VertexOrdering):
     return ops.witness_tuple(ops.peo(rows, order, ops.positions(order)))
 
 
+def left_arrays(g, o: VertexOrdering, want_rows: bool):
+    """Host arrays of the left-neighbourhood kernels (csrc/left.cu) under ``o``:
+    (LN rows uint8[n, ceil(n/8)] or None, parent int32[n] (-1: none), |LN| int32[n],
+    deg int64[n]).  LN rows exist for dense inputs only."""
+    torch = _native.require_cuda()
+    n = int(g.n)
+    if is_csr(g):
+        ip, ix = device_csr(g)
+        order = torch.as_tensor(np.ascontiguousarray(o.order0, dtype=np.int32)).to(ip.device)
+        parent, ln_size = ops.left_csr(ip, ix, n, order, ops.positions(order))
+        deg = np.diff(ip.cpu().numpy())
+        return None, parent[:n].cpu().numpy(), ln_size[:n].cpu().numpy(), deg
+    rows = device_rows(g)
+    order = torch.as_tensor(np.ascontiguousarray(o.order0, dtype=np.int32)).to(rows.data.device)
+    ln, parent, ln_size, deg = ops.left_dense(rows, order, ops.positions(order), want_rows)
+    ln_h = ln[:, : (n + 7) // 8].cpu().numpy() if want_rows else None
+    return ln_h, parent[:n].cpu().numpy(), ln_size[:n].cpu().numpy(), deg[:n].cpu().numpy().astype(np.int64)
+
+
 def is_chordal(g, tie_rule: int, seed: int = 0):
     """LexBFS + PEO test on the device: (VertexOrdering, 0-based witness or None)."""
     n = int(g.n)

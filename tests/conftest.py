@@ -88,3 +88,31 @@ def named_packed(rec):
     for u, v in rec["edges"]:
         rows[u - 1, v - 1] = rows[v - 1, u - 1] = True
     return np.packbits(rows, axis=1, bitorder="little")
+
+
+class LeftCorpus:
+    """Decoded left_scan.npz (tests/golden/make_left_golden.py): one record per
+    (graph, ordering) case with the reference's left_neighborhoods parents,
+    |LN(v)|, is_peo verdict / witness and ScanStats reads / budget."""
+
+    def __init__(self):
+        z = load_npz("left_scan.npz")
+        self.z = z
+        self.ns = z["n"].astype(int)
+        self.off = z["packed_off"]
+        self.voff = np.concatenate([[0], np.cumsum(self.ns)])
+
+    def __len__(self):
+        return len(self.ns)
+
+    def packed(self, i):
+        n = int(self.ns[i])
+        return self.z["packed"][self.off[i]:self.off[i + 1]].reshape(n, (n + 7) // 8)
+
+    def vec(self, key, i):
+        return self.z[key][self.voff[i]:self.voff[i + 1]]
+
+
+@pytest.fixture(scope="session")
+def left_corpus():
+    return LeftCorpus()
