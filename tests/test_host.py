@@ -93,10 +93,12 @@ def test_generators_match_reference_fingerprints():
         assert packed_sha256(h._packed) == cfg["1"]["nonchordal"]["packed_sha256"]
 
 
+@pytest.mark.gpu
 def test_scan_stats_formula_matches_reference_counts():
-    """The reconstructed list-scan read count equals the reference's own count.
-
-    Expected values were produced by chordalkit's instrumented list method."""
+    """The reconstructed list-scan read count equals the reference's own count
+    (the degrees, |LN| and parents come from the device; 600 more cases in
+    test_gpu_left.py).  Expected values were produced by chordalkit's
+    instrumented list method."""
     from paper_1508_06329_b200.peo import _list_scan_reads
 
     g = c4()
