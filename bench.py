@@ -275,6 +275,25 @@ def single_graph_lines(with_cpu: bool) -> dict:
         u, v = chordal_random_edges(n, k, seed)
         return DeviceRows(n, device_stride(n), ops.edges_to_dense(u, v, n, device_stride(n)))
 
+    cpu = {}
+
+    def cpu_leg(name, packed, n, w_gpu, order_gpu):
+        """The oracle C port of is_chordal (PartitionList LexBFS + list PEO, 1 core)
+        on the same graph, and the GPU result checked against it."""
+        import oracle
+
+        packed = np.ascontiguousarray(packed)
+        t0 = time.perf_counter()
+        o_ref = oracle.lexbfs_partition(packed, n)
+        t1 = time.perf_counter()
+        ok, w_ref = oracle.is_peo(packed, n, o_ref)
+        t2 = time.perf_counter()
+        same = bool(np.array_equal(o_ref, order_gpu)) and (w_ref == w_gpu)
+        if not same:
+            raise SystemExit(f"PARITY FAILURE on {name}: GPU order/witness differ from the oracle")
+        cpu[name] = {"ms_per_graph": (t2 - t0) * 1e3, "lexbfs_ms": (t1 - t0) * 1e3, "peo_ms": (t2 - t1) * 1e3,
+                     "cores": 1, "kind": "port", "same_order_and_witness": same}
+
     def measure(name, rows: DeviceRows, host_packed=None):
         n = rows.n
         if rows.m < 0:  # Graph.m, as the public API passes it (picks the engine's thread count)
@@ -324,6 +343,10 @@ def single_graph_lines(with_cpu: bool) -> dict:
                 e2e()
             rec["total_ms_host_buffers"] = (time.perf_counter() - t0) / 3 * 1e3
         out[name] = rec
+        if with_cpu:
+            packed = host_packed if host_packed is not None else rows.data[:, : (n + 7) // 8].cpu().numpy()
+            cpu_leg(name, packed, n, w, order.cpu().numpy())
+            rec["cpu_baseline"] = cpu[name]
 
     # configuration 3 (N = 32768)
     r3 = rows_from_edges(32768, 1024, 0)
@@ -401,11 +424,6 @@ def single_graph_lines(with_cpu: bool) -> dict:
     if with_cpu:
         import oracle
 
-        cpu = {}
-        for name, packed, n in (("c1_nonchordal", h1._packed, 1000), ("c3_nonchordal", h3._packed, 32768)):
-            t0 = time.perf_counter()
-            oracle.is_chordal(packed, n)
-            cpu[name] = {"ms_per_graph": (time.perf_counter() - t0) * 1e3, "cores": 1, "kind": "port"}
         ip_h, ix_h = ip5.cpu().numpy(), ix5.cpu().numpy()
         t0 = time.perf_counter()
         o_h = oracle.lexbfs_partition_csr(ip_h, ix_h, n5)
@@ -415,6 +433,9 @@ def single_graph_lines(with_cpu: bool) -> dict:
         cpu["c5_csr_chordal_k8_n1e6"] = {"ms_per_graph": (t2 - t0) * 1e3, "lexbfs_ms": (t1 - t0) * 1e3,
                                          "peo_ms": (t2 - t1) * 1e3, "cores": 1, "kind": "port",
                                          "same_order": bool((o_h == o5.cpu().numpy()).all())}
+        if not cpu["c5_csr_chordal_k8_n1e6"]["same_order"]:
+            raise SystemExit("PARITY FAILURE on c5: GPU order differs from the oracle")
+        out["c5_csr_chordal_k8_n1e6"]["cpu_baseline"] = cpu["c5_csr_chordal_k8_n1e6"]
         out["cpu_baseline"] = cpu
     return out
 
