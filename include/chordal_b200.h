@@ -20,10 +20,8 @@
  *  - "_dev" arguments are device pointers; every call is asynchronous on
  *    `stream` (a cudaStream_t; NULL = legacy default stream) unless the name
  *    ends in _host.  The library holds no caller pointer after return and is
- *    reentrant per stream.  Its only global state: four static 48 KB device
- *    slots per device for the CSR PEO check's heavy-row list, handed out
- *    round robin under a mutex, each reuse ordered on the device after its
- *    previous user by an event.  The _host entry points without a workspace
+ *    reentrant per stream; it keeps no global state of its own (scratch space
+ *    comes from caller workspaces).  The _host entry points without a workspace
  *    argument allocate stream-ordered from the device's default memory pool
  *    and raise that pool's release threshold to one call's footprint so the
  *    buffers stay mapped between calls (a process-wide setting).
@@ -163,15 +161,24 @@ int chordal_lexbfs_csr(const int64_t *indptr_dev, const int32_t *indices_dev, in
                        uint64_t seed, int32_t *order_dev, int32_t *pos_dev, int32_t *parent_dev, void *ws,
                        size_t ws_bytes, void *stream);
 
+/* Workspace (device bytes, 16-byte aligned) of the CSR PEO check: the queue of
+ * heavy rows (more than 1024 neighbours) whose lists the whole grid splits. */
+size_t chordal_peo_csr_workspace_bytes(int64_t n);
+
 /* PEO check on CSR over v in [v_begin, v_end) (row shards), as
- * chordal_peo_dense_key; membership z in N(p) by binary search in p's row. */
+ * chordal_peo_dense_key: parent_dev optional (NULL or -2 entries: searched);
+ * membership z in N(p) by binary search in the shorter of N(p), N(z).  ws:
+ * chordal_peo_csr_workspace_bytes(n) bytes, cleared on `stream` by the call;
+ * one workspace per concurrent call. */
 int chordal_peo_csr_key(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, const int32_t *pos_dev,
-                        const int32_t *parent_dev, int64_t v_begin, int64_t v_end, uint64_t *key_dev, void *stream);
+                        const int32_t *parent_dev, int64_t v_begin, int64_t v_end, uint64_t *key_dev, void *ws,
+                        size_t ws_bytes, void *stream);
 int chordal_peo_csr_witness(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n,
                             const int32_t *pos_dev, const uint64_t *key_dev, int32_t *witness_dev, void *stream);
 /* _is_peo_lists (peo.py:100-149) on CSR: init + key over all v + witness. */
 int chordal_peo_csr(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, const int32_t *pos_dev,
-                    const int32_t *parent_dev, uint64_t *key_dev, int32_t *witness_dev, void *stream);
+                    const int32_t *parent_dev, uint64_t *key_dev, int32_t *witness_dev, void *ws, size_t ws_bytes,
+                    void *stream);
 
 /* ---- left neighbourhoods (graph.py:284-302) ----------------------------- */
 

@@ -19,7 +19,7 @@ LIB = os.path.join(LIBDIR, "libchordal_b200.so")
 ROOT = os.path.dirname(HERE)
 INCLUDE = os.path.join(ROOT, "include")
 
-SOURCES = ["capi.cu", "dense_util.cu", "lexbfs_seg.cu", "peo_dense.cu", "batch.cu", "gen.cu", "csr.cu", "orders.cu", "left.cu", "textio.cpp"]
+SOURCES = ["capi.cu", "dense_util.cu", "lexbfs_seg.cu", "peo_dense.cu", "batch.cu", "gen.cu", "csr.cu", "peo_csr.cu", "orders.cu", "left.cu", "textio.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = [
     "-O3",

@@ -39,9 +39,10 @@ SIGNATURES = {
     "chordal_is_chordal_dense_host_ws": [_P, _I64, _I64, _I64, _I32, _U64, _P, _P, _P, _P, _SZ],
     "chordal_lexbfs_csr_workspace_bytes": [_I64, _I64],
     "chordal_lexbfs_csr": [_P, _P, _I64, _I64, _I32, _U64, _P, _P, _P, _P, _SZ, _P],
-    "chordal_peo_csr_key": [_P, _P, _I64, _P, _P, _I64, _I64, _P, _P],
+    "chordal_peo_csr_workspace_bytes": [_I64],
+    "chordal_peo_csr_key": [_P, _P, _I64, _P, _P, _I64, _I64, _P, _P, _SZ, _P],
     "chordal_peo_csr_witness": [_P, _P, _I64, _P, _P, _P, _P],
-    "chordal_peo_csr": [_P, _P, _I64, _P, _P, _P, _P, _P],
+    "chordal_peo_csr": [_P, _P, _I64, _P, _P, _P, _P, _P, _SZ, _P],
     "chordal_dense_to_csr": [_P, _I64, _I64, _P, _P, _P],
     "chordal_left_dense": [_P, _I64, _I64, _P, _P, _P, _P, _P, _P, _P],
     "chordal_left_csr": [_P, _P, _I64, _P, _P, _P, _P, _P],
@@ -67,6 +68,7 @@ _RESTYPES = {
     "chordal_strerror": ctypes.c_char_p,
     "chordal_gen_chordal_random_scratch_bytes": _SZ,
     "chordal_dense_workspace_bytes": _SZ,
+    "chordal_peo_csr_workspace_bytes": _SZ,
     "chordal_lexbfs_csr_workspace_bytes": _SZ,
     "chordal_write_graph_text": _I64,
     "chordal_bfs_csr_workspace_bytes": _SZ,

@@ -19,7 +19,8 @@ int launch_lexbfs_csr(const int64_t *, const int32_t *, int64_t, int64_t, int32_
                       int32_t *,
                       int32_t *, void *, cudaStream_t);
 int launch_peo_csr_key(const int64_t *, const int32_t *, int64_t, const int32_t *, const int32_t *, int64_t, int64_t,
-                       uint64_t *, cudaStream_t);
+                       uint64_t *, void *, cudaStream_t);
+size_t peo_csr_workspace_bytes();
 int launch_peo_csr_witness(const int64_t *, const int32_t *, const int32_t *, const uint64_t *, int32_t *,
                            cudaStream_t);
 int launch_dense_degrees(const uint8_t *, int64_t, int64_t, int64_t *, cudaStream_t);
@@ -95,7 +96,7 @@ int check_dense(const void *adj, int64_t n, int64_t stride) {
 
 extern "C" {
 
-int chordal_abi_version(void) { return 1; }
+int chordal_abi_version(void) { return 2; }
 
 const char *chordal_strerror(int status) {
     switch (status) {
@@ -435,12 +436,17 @@ int chordal_bfs_csr(const int64_t *indptr_dev, const int32_t *indices_dev, int64
                           pos_dev, as_stream(stream));
 }
 
+size_t chordal_peo_csr_workspace_bytes(int64_t n) { return n > 0 ? peo_csr_workspace_bytes() : 0; }
+
 int chordal_peo_csr_key(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, const int32_t *pos_dev,
-                        const int32_t *parent_dev, int64_t v_begin, int64_t v_end, uint64_t *key_dev, void *stream) {
+                        const int32_t *parent_dev, int64_t v_begin, int64_t v_end, uint64_t *key_dev, void *ws,
+                        size_t ws_bytes, void *stream) {
     if (n < 0) return CHORDAL_EINVAL;
     if (n == 0) return CHORDAL_OK;
+    if (n > 0x7FFFFFFF) return CHORDAL_ETOOLARGE;
     if (!indptr_dev || !indices_dev || !pos_dev || !key_dev) return CHORDAL_EINVAL;
-    return launch_peo_csr_key(indptr_dev, indices_dev, n, pos_dev, parent_dev, v_begin, v_end, key_dev,
+    if (!ws || ws_bytes < peo_csr_workspace_bytes() || (reinterpret_cast<uintptr_t>(ws) & 15)) return CHORDAL_EINVAL;
+    return launch_peo_csr_key(indptr_dev, indices_dev, n, pos_dev, parent_dev, v_begin, v_end, key_dev, ws,
                               as_stream(stream));
 }
 
@@ -457,10 +463,11 @@ int chordal_peo_csr_witness(const int64_t *indptr_dev, const int32_t *indices_de
 }
 
 int chordal_peo_csr(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, const int32_t *pos_dev,
-                    const int32_t *parent_dev, uint64_t *key_dev, int32_t *witness_dev, void *stream) {
+                    const int32_t *parent_dev, uint64_t *key_dev, int32_t *witness_dev, void *ws, size_t ws_bytes,
+                    void *stream) {
     int rc = chordal_key_init(key_dev, stream);
     if (rc) return rc;
-    rc = chordal_peo_csr_key(indptr_dev, indices_dev, n, pos_dev, parent_dev, 0, n, key_dev, stream);
+    rc = chordal_peo_csr_key(indptr_dev, indices_dev, n, pos_dev, parent_dev, 0, n, key_dev, ws, ws_bytes, stream);
     if (rc) return rc;
     return chordal_peo_csr_witness(indptr_dev, indices_dev, n, pos_dev, key_dev, witness_dev, stream);
 }

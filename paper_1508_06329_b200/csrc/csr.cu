@@ -1,13 +1,11 @@
-// csr.cu -- sparse (CSR) chordality test: LexBFS via the slot engine with its
-// state in global memory (L2-resident), a vertex-parallel CSR PEO check, and
-// the bitset -> CSR conversion used to route sparse dense-stored graphs here.
+// csr.cu -- sparse (CSR) LexBFS via the slot engine with its state in global
+// memory (L2-resident), and the bitset -> CSR conversion used to route sparse
+// dense-stored graphs here.  The CSR PEO check is in peo_csr.cu.
 //
 // Replaces, for adjacency-list inputs, lexbfs_partition(method="linked")
 // (search.py:500-532) and _is_peo_lists (peo.py:100-149) -- the pair the
 // reference runs on graphs that only expose n, m and adjacency_lists0()
 // (the N = 10^6 configuration).
-#include <mutex>
-
 #include "common.cuh"
 #include "slot_engine.cuh"
 
@@ -46,27 +44,8 @@ struct CsrWs {
 // u16 vertex/class ids (NIL = 0xFFFF) for n <= 32768; the per-neighbour arrays
 // (cls, c_cnt, c_tgt) then fit in shared memory next to the staging buffer.
 constexpr long long kSmemMaxN = 32768;
-constexpr int kPeoHeavy = 4096;     // rows longer than this are checked by the whole grid
-constexpr int kPeoHeavyMax = 4096;  // capacity of the heavy-row list
-
-// rows with more neighbours than this are "heavy"; at least kPeoHeavy, raised
-// with the edge count so that at most nnz / threshold < kPeoHeavyMax rows qualify
-__device__ __forceinline__ int64_t heavy_threshold(const int64_t *__restrict__ indptr, int n) {
-    const int64_t t = __ldg(indptr + n) / kPeoHeavyMax + 1;
-    return t > kPeoHeavy ? t : (int64_t)kPeoHeavy;
-}
 constexpr int kNbrBuf = 4096;  // neighbour-list staging entries
 inline size_t smem16_bytes(long long n) { return (size_t)(3 * n + 24 + kNbrBuf) * sizeof(uint16_t) + 64; }
-
-__device__ __forceinline__ bool contains(const int32_t *__restrict__ a, int64_t lo, int64_t hi, int key) {
-    // lower_bound then equality test
-    int64_t l = lo, h = hi;
-    while (l < h) {
-        int64_t mid = (l + h) >> 1;
-        if (__ldg(a + mid) < key) l = mid + 1; else h = mid;
-    }
-    return l < hi && __ldg(a + l) == key;
-}
 
 }  // namespace
 
@@ -121,235 +100,6 @@ lexbfs_csr_smem_kernel(const int64_t *__restrict__ indptr, const int32_t *__rest
     CsrStagedSource<uint16_t> src{indptr, indices, nbuf, kNbrBuf, 0};
     slot_lexbfs<uint16_t, int32_t, MODE, CsrStagedSource<uint16_t>, int32_t>(src, n, M, order, pos, parent, seed,
                                                                               cell);
-}
-
-// ---------------------------------------------------------------------------
-// PEO check on CSR: one warp per vertex v in [v_begin, v_end).
-//   parent  given (from LexBFS) or the neighbour with the greatest position
-//           before pos(v) (peo.py:106-121);
-//   stray   some z in N(v), z != p, pos(z) < pos(p), z not in N(p) -- each
-//           candidate is looked up in p's sorted list by binary search.
-__global__ void __launch_bounds__(256)
-peo_csr_key_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices, int n,
-                   const int32_t *__restrict__ pos, const int32_t *__restrict__ parent_in, int v_begin, int v_end,
-                   unsigned long long *__restrict__ key) {
-    const int lane = threadIdx.x & 31;
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nw = (gridDim.x * blockDim.x) >> 5;
-    const int64_t heavy = heavy_threshold(indptr, n);
-    // The current minimum key, refreshed every 16 vertices of this warp: read per
-    // vertex, a million warps' loads of one address queued at one L2 slice and
-    // made the check's time swing 0.8-1.8 ms between runs on configuration 5.
-    unsigned long long kmin = ~0ULL;
-    int it = 0;
-    for (int v = v_begin + gw; v < v_end; v += nw, ++it) {
-        if ((it & 15) == 0) kmin = *(volatile unsigned long long *)key;
-        const int pv = __ldg(pos + v);
-        const int64_t b = __ldg(indptr + v), e = __ldg(indptr + v + 1);
-        if (e - b > heavy) continue;  // heavy rows: split over the grid (peo_csr_heavy_*)
-        int p = parent_in ? __ldg(parent_in + v) : -2;
-        if (p == -2) {  // unknown: max position among the neighbours preceding v
-            int best = -1;
-            for (int64_t k = b + lane; k < e; k += 32) {
-                int pu = __ldg(pos + __ldg(indices + k));
-                if (pu < pv && pu > best) best = pu;
-            }
-#pragma unroll
-            for (int d = 16; d >= 1; d >>= 1) best = max(best, __shfl_xor_sync(CH_FULL, best, d));
-            p = -1;
-            if (best >= 0) {
-                // the neighbour at that position
-                for (int64_t k = b + lane; k < e; k += 32) {
-                    int u = __ldg(indices + k);
-                    if (__ldg(pos + u) == best) p = u;
-                }
-#pragma unroll
-                for (int d = 16; d >= 1; d >>= 1) p = max(p, __shfl_xor_sync(CH_FULL, p, d));
-            }
-        }
-        if (p < 0) continue;
-        const unsigned long long k64 = ((unsigned long long)p << 32) | (unsigned)v;
-        if (k64 >= kmin) continue;
-        const int pp = __ldg(pos + p);
-        const int64_t pb = __ldg(indptr + p), pe = __ldg(indptr + p + 1);
-        bool viol = false;
-        for (int64_t k0 = b; k0 < e; k0 += 32) {
-            int64_t k = k0 + lane;
-            if (k < e) {
-                int z = __ldg(indices + k);
-                if (z != p && __ldg(pos + z) < pp && !contains(indices, pb, pe, z)) viol = true;
-            }
-            if (__any_sync(CH_FULL, viol)) { viol = true; break; }
-        }
-        if (viol) {
-            if (lane == 0) atomicMin(key, k64);
-            kmin = min(kmin, k64);
-        }
-    }
-}
-
-// ---- rows with more than kPeoHeavy neighbours (config 5: vertex 0 has 419,309)
-// One warp per row would serialise the whole check behind them, so their
-// neighbour lists are split into 1024-entry slices spread over the grid:
-//   collect  list the heavy rows of [v_begin, v_end)
-//   parent   (only where the search left it unknown) max position before
-//            pos(v) over the slices (atomicMax), then the neighbour holding it
-//   stray    every slice tests its candidates (z != p, pos(z) < pos(p),
-//            z not in N(p)) and lowers the key on a hit.
-struct PeoHeavy {
-    int count;
-    int pad;
-    int v[kPeoHeavyMax];
-    int best[kPeoHeavyMax];    // max position before pos(v) (parent search)
-    int parent[kPeoHeavyMax];  // resolved parent, -1 none
-};
-
-constexpr int kHeavySlots = 4;
-__device__ PeoHeavy g_peo_heavy[kHeavySlots];  // 4 x 48 KB per device
-
-struct HeavySlots {
-    std::mutex mu;
-    PeoHeavy *base = nullptr;
-    cudaEvent_t ev[kHeavySlots] = {};
-    unsigned next = 0;
-};
-
-// one set per device (the module's __device__ array is per device too)
-HeavySlots &heavy_slots() {
-    static HeavySlots sets[64];
-    int dev = 0;
-    cudaGetDevice(&dev);
-    return sets[dev & 63];
-}
-
-__global__ void peo_csr_heavy_collect(const int64_t *__restrict__ indptr, int n, const int32_t *__restrict__ parent_in,
-                                      int v_begin, int v_end, PeoHeavy *H) {
-    const int64_t heavy = heavy_threshold(indptr, n);
-    for (int v = v_begin + blockIdx.x * blockDim.x + threadIdx.x; v < v_end; v += gridDim.x * blockDim.x) {
-        if (__ldg(indptr + v + 1) - __ldg(indptr + v) > heavy) {
-            const int k = atomicAdd(&H->count, 1);
-            if (k < kPeoHeavyMax) {
-                H->v[k] = v;
-                H->best[k] = -1;
-                H->parent[k] = parent_in ? __ldg(parent_in + v) : -2;
-            }
-        }
-    }
-}
-
-constexpr int kSlice = 1024;  // neighbours per warp work item
-
-// every warp of the grid walks the (heavy row, slice) items
-template <typename Fn>
-__device__ __forceinline__ void for_each_heavy_slice(const int64_t *__restrict__ indptr, const PeoHeavy *H, Fn &&fn) {
-    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-    const int nw = (gridDim.x * blockDim.x) >> 5;
-    const int cnt = min(H->count, kPeoHeavyMax);
-    long long item = 0;
-    for (int j = 0; j < cnt; ++j) {
-        const int v = H->v[j];
-        const int64_t b = __ldg(indptr + v), e = __ldg(indptr + v + 1);
-        const long long ns = (e - b + kSlice - 1) / kSlice;
-        for (long long sidx = ((gw - item) % nw + nw) % nw; sidx < ns; sidx += nw) {
-            const int64_t lo = b + sidx * kSlice, hi = min(e, lo + kSlice);
-            fn(j, v, lo, hi);
-        }
-        item += ns;
-    }
-}
-
-__global__ void __launch_bounds__(256) peo_csr_heavy_parent_max(const int64_t *__restrict__ indptr,
-                                                                const int32_t *__restrict__ indices,
-                                                                const int32_t *__restrict__ pos, PeoHeavy *H) {
-    const int lane = threadIdx.x & 31;
-    for_each_heavy_slice(indptr, H, [&](int j, int v, int64_t lo, int64_t hi) {
-        if (H->parent[j] != -2) return;  // given by the search
-        const int pv = __ldg(pos + v);
-        int best = -1;
-        for (int64_t k = lo + lane; k < hi; k += 32) {
-            const int pu = __ldg(pos + __ldg(indices + k));
-            if (pu < pv && pu > best) best = pu;
-        }
-        best = __reduce_max_sync(CH_FULL, best);
-        if (lane == 0 && best >= 0) atomicMax(&H->best[j], best);
-    });
-}
-
-__global__ void __launch_bounds__(256) peo_csr_heavy_parent_pick(const int64_t *__restrict__ indptr,
-                                                                 const int32_t *__restrict__ indices,
-                                                                 const int32_t *__restrict__ pos, PeoHeavy *H) {
-    const int lane = threadIdx.x & 31;
-    for_each_heavy_slice(indptr, H, [&](int j, int v, int64_t lo, int64_t hi) {
-        if (H->parent[j] != -2) return;
-        const int best = H->best[j];
-        if (best < 0) {
-            if (lo == __ldg(indptr + v) && lane == 0) H->parent[j] = -1;  // no left neighbour
-            return;
-        }
-        for (int64_t k = lo + lane; k < hi; k += 32) {
-            const int u = __ldg(indices + k);
-            if (__ldg(pos + u) == best) H->parent[j] = u;  // unique: positions are distinct
-        }
-    });
-}
-
-__global__ void __launch_bounds__(256) peo_csr_heavy_stray(const int64_t *__restrict__ indptr,
-                                                           const int32_t *__restrict__ indices,
-                                                           const int32_t *__restrict__ pos, const PeoHeavy *H,
-                                                           unsigned long long *__restrict__ key) {
-    const int lane = threadIdx.x & 31;
-    for_each_heavy_slice(indptr, H, [&](int j, int v, int64_t lo, int64_t hi) {
-        const int p = H->parent[j];
-        if (p < 0 || __ldg(pos + v) == 0) return;
-        const unsigned long long k64 = ((unsigned long long)p << 32) | (unsigned)v;
-        if (k64 >= *(volatile unsigned long long *)key) return;
-        const int pp = __ldg(pos + p);
-        const int64_t pb = __ldg(indptr + p), pe = __ldg(indptr + p + 1);
-        bool viol = false;
-        for (int64_t k0 = lo; k0 < hi; k0 += 32) {
-            const int64_t k = k0 + lane;
-            if (k < hi) {
-                const int z = __ldg(indices + k);
-                if (z != p && __ldg(pos + z) < pp && !contains(indices, pb, pe, z)) viol = true;
-            }
-            if (__any_sync(CH_FULL, viol)) { viol = true; break; }
-        }
-        if (viol && lane == 0) atomicMin(key, k64);
-    });
-}
-
-__global__ void peo_csr_witness_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices,
-                                       const int32_t *__restrict__ pos, const unsigned long long *__restrict__ key,
-                                       int32_t *__restrict__ witness) {
-    const int lane = threadIdx.x & 31;
-    const unsigned long long k64 = *key;
-    if (k64 == ~0ULL) {
-        if (lane < 3) witness[lane] = -1;
-        return;
-    }
-    const int p = (int)(k64 >> 32), v = (int)(k64 & 0xFFFFFFFFu);
-    const int pp = pos[p];
-    const int64_t b = indptr[v], e = indptr[v + 1], pb = indptr[p], pe = indptr[p + 1];
-    int z = -1;
-    for (int64_t k0 = b; k0 < e; k0 += 32) {  // N(v) ascending: the first hit is the smallest z
-        int64_t k = k0 + lane;
-        bool hit = false;
-        int zz = 0;
-        if (k < e) {
-            zz = indices[k];
-            hit = zz != p && pos[zz] < pp && !contains(indices, pb, pe, zz);
-        }
-        uint32_t m = __ballot_sync(CH_FULL, hit);
-        if (m) {
-            z = __shfl_sync(CH_FULL, zz, __ffs(m) - 1);
-            break;
-        }
-    }
-    if (lane == 0) {
-        witness[0] = v;
-        witness[1] = p;
-        witness[2] = z;
-    }
 }
 
 // ---------------------------------------------------------------------------
@@ -479,52 +229,6 @@ int launch_lexbfs_csr(const int64_t *indptr, const int32_t *indices, int64_t n, 
         default:
             return CHORDAL_EINVAL;
     }
-}
-
-int launch_peo_csr_key(const int64_t *indptr, const int32_t *indices, int64_t n, const int32_t *pos,
-                       const int32_t *parent, int64_t v_begin, int64_t v_end, uint64_t *key, cudaStream_t stream) {
-    if (v_begin < 0) v_begin = 0;
-    if (v_end > n) v_end = n;
-    if (v_end <= v_begin) return CHORDAL_OK;
-    long long blocks = ((v_end - v_begin) * 32 + 255) / 256;
-    if (blocks > 148LL * 16) blocks = 148LL * 16;
-    peo_csr_key_kernel<<<(int)blocks, 256, 0, stream>>>(indptr, indices, (int)n, pos, parent, (int)v_begin,
-                                                        (int)v_end, reinterpret_cast<unsigned long long *>(key));
-    CH_LAUNCH_CHECK();
-    // heavy rows: their list lives in one of a few static device slots, handed
-    // out round robin; a slot's next user waits (on the device) for the event
-    // its previous user recorded.  No allocation per call -- stream-ordered
-    // pool blocks made single calls milliseconds slower at random.
-    HeavySlots &hs = heavy_slots();
-    std::lock_guard<std::mutex> lock(hs.mu);
-    if (!hs.base && cudaGetSymbolAddress(reinterpret_cast<void **>(&hs.base), g_peo_heavy) != cudaSuccess)
-        return CHORDAL_ECUDA;
-    const int slot = (int)(hs.next++ % kHeavySlots);
-    if (!hs.ev[slot]) {
-        if (cudaEventCreateWithFlags(&hs.ev[slot], cudaEventDisableTiming) != cudaSuccess) return CHORDAL_ECUDA;
-    } else if (cudaStreamWaitEvent(stream, hs.ev[slot], 0) != cudaSuccess) {
-        return CHORDAL_ECUDA;
-    }
-    PeoHeavy *H = hs.base + slot;
-    cudaMemsetAsync(H, 0, sizeof(int) * 2, stream);
-    long long cb = (v_end - v_begin + 255) / 256;
-    if (cb > 148LL * 8) cb = 148LL * 8;
-    peo_csr_heavy_collect<<<(int)cb, 256, 0, stream>>>(indptr, (int)n, parent, (int)v_begin, (int)v_end, H);
-    const int hb = 148 * 8;
-    peo_csr_heavy_parent_max<<<hb, 256, 0, stream>>>(indptr, indices, pos, H);
-    peo_csr_heavy_parent_pick<<<hb, 256, 0, stream>>>(indptr, indices, pos, H);
-    peo_csr_heavy_stray<<<hb, 256, 0, stream>>>(indptr, indices, pos, H, reinterpret_cast<unsigned long long *>(key));
-    const cudaError_t le = cudaGetLastError();
-    if (cudaEventRecord(hs.ev[slot], stream) != cudaSuccess) return CHORDAL_ECUDA;
-    return le == cudaSuccess ? CHORDAL_OK : CHORDAL_ECUDA;
-}
-
-int launch_peo_csr_witness(const int64_t *indptr, const int32_t *indices, const int32_t *pos, const uint64_t *key,
-                           int32_t *witness, cudaStream_t stream) {
-    peo_csr_witness_kernel<<<1, 32, 0, stream>>>(indptr, indices, pos,
-                                                 reinterpret_cast<const unsigned long long *>(key), witness);
-    CH_LAUNCH_CHECK();
-    return CHORDAL_OK;
 }
 
 int launch_dense_degrees(const uint8_t *adj, int64_t n, int64_t stride, int64_t *indptr, cudaStream_t stream) {

@@ -190,24 +190,31 @@ def lexbfs_csr(indptr, indices, n: int, tie_rule: int = _native.TIE_ASCENDING, s
     return order[:n], pos[:n], parent[:n]
 
 
-def peo_csr(indptr, indices, n: int, pos, parent=None, stream=None):
+def peo_csr_workspace(n: int, device):
+    torch = _native.require_cuda()
+    return _ws(torch, lib.chordal_peo_csr_workspace_bytes(n), device)
+
+
+def peo_csr(indptr, indices, n: int, pos, parent=None, stream=None, ws=None):
     torch = _native.require_cuda()
     dev = indptr.device
     key = torch.empty(1, dtype=torch.int64, device=dev)
     wit = torch.empty(4, dtype=torch.int32, device=dev)
+    ws = ws if ws is not None else peo_csr_workspace(n, dev)
     check(
         lib.chordal_peo_csr(ptr(indptr), ptr(indices), n, ptr(pos) if n else None,
                             ptr(parent) if (n and parent is not None) else None, ptr(key), ptr(wit),
-                            stream_ptr(stream)),
+                            ptr(ws), ws.numel(), stream_ptr(stream)),
         "chordal_peo_csr",
     )
     return wit[:3]
 
 
-def peo_csr_key(indptr, indices, n: int, pos, v_begin: int, v_end: int, key, parent=None, stream=None):
+def peo_csr_key(indptr, indices, n: int, pos, v_begin: int, v_end: int, key, parent=None, stream=None, ws=None):
+    ws = ws if ws is not None else peo_csr_workspace(n, indptr.device)
     check(
         lib.chordal_peo_csr_key(ptr(indptr), ptr(indices), n, ptr(pos), ptr(parent) if parent is not None else None,
-                                v_begin, v_end, ptr(key), stream_ptr(stream)),
+                                v_begin, v_end, ptr(key), ptr(ws), ws.numel(), stream_ptr(stream)),
         "chordal_peo_csr_key",
     )
 

@@ -1,6 +1,6 @@
 """Small driver for ncu captures: runs each hot kernel a few times on config inputs.
 
-    python tools/profile_driver.py {batch|batch_chordal|batch_dense|lexbfs32k|peo32k|lexbfs1k|csr1m|all}
+    python tools/profile_driver.py {batch|batch_chordal|batch_dense|lexbfs32k|peo32k|lexbfs1k|csr1m|peo_csr1m|all}
 """
 import os
 import sys
@@ -45,6 +45,14 @@ def main(what):
 
         ip, ix = gen_chordal_random_csr_device(1_000_000, 8, 0)
         ops.lexbfs_csr(ip, ix, 1_000_000)
+    if what == "peo_csr1m":
+        from paper_1508_06329_b200.generate import gen_chordal_random_csr_device
+
+        ip, ix = gen_chordal_random_csr_device(1_000_000, 8, 0)
+        order, pos, parent = ops.lexbfs_csr(ip, ix, 1_000_000)
+        ws = ops.peo_csr_workspace(1_000_000, ip.device)
+        for _ in range(3):
+            ops.peo_csr(ip, ix, 1_000_000, pos, parent, ws=ws)
     if what in ("lexbfs1k", "all"):
         r = rows_chordal(1000, 8, 0)
         for _ in range(3):
