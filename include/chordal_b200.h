@@ -23,8 +23,8 @@
  *    reentrant per stream; it keeps no global state of its own (scratch space
  *    comes from caller workspaces).  The _host entry points without a workspace
  *    argument allocate stream-ordered from the device's default memory pool
- *    and raise that pool's release threshold to one call's footprint so the
- *    buffers stay mapped between calls (a process-wide setting).
+ *    and free before returning (the pool's settings are left to the caller);
+ *    repeated callers use the _ws forms with a workspace they keep.
  *  - Witness triples are int32[3] = (v, p, z) -- WitnessTriple (peo.py:26-45),
  *    0-based -- or (-1, -1, -1) when the ordering is a PEO.
  *  - Every function returns a chordal status code (CHORDAL_OK == 0).

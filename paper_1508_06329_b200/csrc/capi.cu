@@ -48,15 +48,6 @@ int launch_left_dense(const uint8_t *, int64_t, int64_t, const int32_t *, const 
                       int32_t *, int32_t *, cudaStream_t);
 int launch_left_csr(const int64_t *, const int32_t *, int64_t, const int32_t *, const int32_t *, int32_t *, int32_t *,
                     cudaStream_t);
-void keep_pool_bytes(size_t bytes) {
-    int dev = 0;
-    cudaMemPool_t pool;
-    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetDefaultMemPool(&pool, dev) != cudaSuccess) return;
-    uint64_t cur = 0;
-    if (cudaMemPoolGetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &cur) != cudaSuccess) return;
-    uint64_t want = bytes;
-    if (cur < want) cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &want);
-}
 
 }  // namespace chordal
 
@@ -76,11 +67,11 @@ uint32_t crc32_str(const char *s) {
 
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
-// The host-buffer entry points allocate their device buffers stream-ordered
-// from the device's default pool.  With the pool's default release threshold
-// (0) every call would hand the memory back to the driver and map it again on
-// the next call (tens of ms for the batch staging buffers); raising the
-// threshold to the bytes one call needs keeps them cached.  Only ever raised.
+// The host-buffer entry points without a workspace argument allocate their
+// device buffers stream-ordered from the device's default pool and free them
+// before returning; the pool's settings are the caller's (with the default
+// release threshold the memory goes back to the driver at each sync, so
+// repeated calls should use the _ws forms with a workspace kept by the caller).
 
 int check_dense(const void *adj, int64_t n, int64_t stride) {
     if (n < 0) return CHORDAL_EINVAL;
@@ -310,7 +301,6 @@ int chordal_is_chordal_dense_host(const uint8_t *adj_host, int64_t n, int64_t ro
             if (rc) break;
         }
         const size_t wsb = DenseWs(n, m).total;
-        keep_pool_bytes(adj_bytes + sizeof(int32_t) * (2 * n + 4) + wsb + 16);
         if (cudaMallocAsync((void **)&ws, wsb + 16, s) != cudaSuccess) { rc = CHORDAL_ENOMEM; break; }
         int32_t *wit = reinterpret_cast<int32_t *>(ws + wsb);
         rc = chordal_is_chordal_dense(adj, n, stride, m, tie_rule, seed, order, order + n, ws, wsb, wit, s);
@@ -626,7 +616,6 @@ int chordal_is_chordal_batch_host(const uint8_t *adj_host, int64_t batch, int64_
     // one stream-ordered block per call on the calling thread's default stream
     // (see chordal_is_chordal_batch_host_ws for the jitter-free form)
     const size_t wsb = chordal_batch_host_workspace_bytes(n, chunk);
-    keep_pool_bytes(wsb);
     cudaStream_t home = cudaStreamPerThread;
     uint8_t *block = nullptr;
     if (cudaMallocAsync((void **)&block, wsb, home) != cudaSuccess) return CHORDAL_ENOMEM;
