@@ -46,6 +46,7 @@ extern "C" {
 #define CHORDAL_ENOMEM 4     /* device allocation failed (host-buffer entry points) */
 #define CHORDAL_EPARSE 5     /* text input rejected (maps to ParseError; line + message returned) */
 #define CHORDAL_EUTF8 6      /* text input is not valid UTF-8 (maps to ParseError) */
+#define CHORDAL_ENCCL 7      /* NCCL not loadable in the process, or a collective failed */
 
 /* LexBFS tie rules.
  *  ASCENDING  : max label, ties -> smallest vertex id.  = lexbfs_partition /
@@ -101,6 +102,20 @@ size_t chordal_dense_workspace_bytes(int64_t n, int64_t m);
 int chordal_lexbfs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int64_t m, int32_t tie_rule,
                          uint64_t seed, int32_t *order_dev, int32_t *pos_dev, int32_t *parent_dev, void *ws,
                          size_t ws_bytes, void *stream);
+
+/* LexBFS certificate of a given order (the invariant behind lexbfs_labels(debug=True),
+ * search.py:270-271, 313-322, and parallel_lexbfs(audit=True), parallel/lexbfs.py:82-129:
+ * every pivot carries the lexicographically largest label of the unvisited
+ * vertices).  Replays the search with pivot i forced to order_dev[i] (a
+ * permutation of 0..n-1) and writes status_dev[0] = the first step whose pivot
+ * is not in the maximum-label class (-1: order_dev is a LexBFS order) and
+ * status_dev[1] = the first step whose pivot differs from the LOWEST_INDEX
+ * choice (-1: it is the LOWEST_INDEX order).  n <= 32768 (single-CTA engine);
+ * ws >= chordal_lexbfs_certify_workspace_bytes(n). */
+size_t chordal_lexbfs_certify_workspace_bytes(int64_t n);
+int chordal_lexbfs_certify_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int64_t m,
+                                 const int32_t *order_dev, int32_t *status_dev, void *ws, size_t ws_bytes,
+                                 void *stream);
 
 /* pos_dev[order_dev[i]] = i  (VertexOrdering.pos0, graph.py:224-230). */
 int chordal_positions(const int32_t *order_dev, int64_t n, int32_t *pos_dev, void *stream);
@@ -328,6 +343,27 @@ int64_t chordal_write_graph_text(const uint8_t *rows, int64_t n, int64_t row_byt
  * permutation mismatch. */
 int chordal_parse_ordering_text(const char *text, int64_t len, int64_t n, int64_t *order_out, int64_t *count_out,
                                 int64_t *err_line, char *err_msg, int64_t err_cap);
+
+/* ---- multi-GPU: row-sharded chordality test over NCCL ----------------- */
+
+/* is_chordal of one graph replicated on every rank of `nccl_comm` (the caller's
+ * ncclComm_t, one GPU per rank), the protocol of distributed.sharded_is_chordal:
+ * rank `root` runs LexBFS (a single graph's step chain stays on one GPU),
+ * broadcasts order + PEO parents, every rank checks its row shard (contiguous,
+ * rank r of W gets n / W rows, +1 for r < n % W; chordal_peo_*_key), one 8-byte MIN all-reduce of
+ * the witness key, z resolved on every rank.  On return (stream order) every
+ * rank holds order_dev, pos_dev and witness_dev.  NCCL is resolved from the
+ * process by soname (libnccl.so.2, the library that created the communicator)
+ * at the first call: CHORDAL_ENCCL if it cannot be.  Dense graphs with
+ * n > 32768 need m >= 0.  ws: chordal_{dense,csr}_nccl_workspace_bytes(n, m). */
+size_t chordal_dense_nccl_workspace_bytes(int64_t n, int64_t m);
+int chordal_is_chordal_dense_nccl(const uint8_t *adj_dev, int64_t n, int64_t stride, int64_t m, int32_t tie_rule,
+                                  uint64_t seed, int32_t root, void *nccl_comm, int32_t *order_dev, int32_t *pos_dev,
+                                  int32_t *witness_dev, void *ws, size_t ws_bytes, void *stream);
+size_t chordal_csr_nccl_workspace_bytes(int64_t n, int64_t m);
+int chordal_is_chordal_csr_nccl(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, int64_t m,
+                                int32_t tie_rule, uint64_t seed, int32_t root, void *nccl_comm, int32_t *order_dev,
+                                int32_t *pos_dev, int32_t *witness_dev, void *ws, size_t ws_bytes, void *stream);
 
 #ifdef __cplusplus
 }

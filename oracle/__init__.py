@@ -253,3 +253,31 @@ def gen_config4_batch(seed_lo: int, count: int, n: int = 512, p: float = 0.5, k:
     if rc:
         raise MemoryError("oracle_gen_config4_batch")
     return out
+
+
+def lexbfs_certify(packed: np.ndarray, n: int, order0) -> tuple[int, int]:
+    """LexBFS certificate of ``order0`` (pure Python, small n): replay the
+    search with pivot i forced to order0[i], labels materialised as in the
+    reference's debug mode (search.py:270-271: digit n - i appended at step i,
+    _check_chain search.py:313-322: the chain's labels ascend to the class the
+    pivot is taken from; parallel/lexbfs.py:82-129 audits the same set-list
+    invariant).  Returns (first step whose pivot does not carry the largest
+    label, first step whose pivot is not the smallest id among the vertices
+    with the largest label), -1 for none."""
+    rows = np.unpackbits(np.asarray(packed, dtype=np.uint8), axis=1, bitorder="little", count=n).astype(bool) \
+        if n else np.zeros((0, 0), bool)
+    adj = [np.flatnonzero(rows[v]).tolist() for v in range(n)]
+    label: list[list[int]] = [[] for _ in range(n)]
+    visited = [False] * n
+    off = -1
+    for i, x in enumerate(int(v) for v in order0):
+        best = max(label[v] for v in range(n) if not visited[v])
+        if label[x] != best:
+            return i, (i if off < 0 else off)
+        if off < 0 and x != min(v for v in range(n) if not visited[v] and label[v] == best):
+            off = i
+        visited[x] = True
+        for y in adj[x]:
+            if not visited[y]:
+                label[y].append(n - i)
+    return -1, off

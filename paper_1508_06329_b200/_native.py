@@ -15,7 +15,7 @@ from .errors import DeviceError, GraphTooLarge, InvalidOrdering
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "lib", "libchordal_b200.so")
 
-OK, EINVAL, ETOOLARGE, ECUDA, ENOMEM, EPARSE, EUTF8 = 0, 1, 2, 3, 4, 5, 6
+OK, EINVAL, ETOOLARGE, ECUDA, ENOMEM, EPARSE, EUTF8, ENCCL = 0, 1, 2, 3, 4, 5, 6, 7
 TIE_ASCENDING, TIE_DESCENDING, TIE_SEEDED_ARB, TIE_SEEDED_PARTITION, TIE_SEEDED_LABELS = 0, 1, 2, 3, 4
 DENSE_LEXBFS_MAX_N = 32768
 BATCH_MAX_N = 1024
@@ -28,7 +28,13 @@ SIGNATURES = {
     "chordal_strerror": [ctypes.c_int],
     "chordal_dense_workspace_bytes": [_I64, _I64],
     "chordal_lexbfs_dense": [_P, _I64, _I64, _I64, _I32, _U64, _P, _P, _P, _P, _SZ, _P],
+    "chordal_lexbfs_certify_workspace_bytes": [_I64],
+    "chordal_lexbfs_certify_dense": [_P, _I64, _I64, _I64, _P, _P, _P, _SZ, _P],
     "chordal_positions": [_P, _I64, _P, _P],
+    "chordal_dense_nccl_workspace_bytes": [_I64, _I64],
+    "chordal_is_chordal_dense_nccl": [_P, _I64, _I64, _I64, _I32, _U64, _I32, _P, _P, _P, _P, _P, _SZ, _P],
+    "chordal_csr_nccl_workspace_bytes": [_I64, _I64],
+    "chordal_is_chordal_csr_nccl": [_P, _P, _I64, _I64, _I32, _U64, _I32, _P, _P, _P, _P, _P, _SZ, _P],
     "chordal_key_init": [_P, _P],
     "chordal_peo_dense_key": [_P, _I64, _I64, _P, _P, _P, _I64, _I64, _P, _P],
     "chordal_peo_dense_witness": [_P, _I64, _I64, _P, _P, _P, _P],
@@ -68,6 +74,9 @@ _RESTYPES = {
     "chordal_strerror": ctypes.c_char_p,
     "chordal_gen_chordal_random_scratch_bytes": _SZ,
     "chordal_dense_workspace_bytes": _SZ,
+    "chordal_lexbfs_certify_workspace_bytes": _SZ,
+    "chordal_dense_nccl_workspace_bytes": _SZ,
+    "chordal_csr_nccl_workspace_bytes": _SZ,
     "chordal_peo_csr_workspace_bytes": _SZ,
     "chordal_lexbfs_csr_workspace_bytes": _SZ,
     "chordal_write_graph_text": _I64,

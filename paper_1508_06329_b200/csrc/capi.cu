@@ -3,12 +3,13 @@
 // Thin validation + launch layer: no global mutable state, no retained caller
 // pointers; every device entry point is asynchronous on the caller's stream.
 #include <cstring>
+#include <dlfcn.h>
 
 #include "common.cuh"
 
 namespace chordal {
 int launch_lexbfs_seg(const uint8_t *, int64_t, int64_t, int64_t, int32_t, uint64_t, uint64_t, int32_t *, int32_t *,
-                      int32_t *, cudaStream_t);
+                      int32_t *, cudaStream_t, const int32_t * = nullptr, int32_t * = nullptr);
 int launch_positions(const int32_t *, int64_t, int32_t *, cudaStream_t);
 int launch_fill_i32(int32_t *, int64_t, int32_t, cudaStream_t);
 int launch_key_init(uint64_t *, cudaStream_t);
@@ -87,7 +88,7 @@ int check_dense(const void *adj, int64_t n, int64_t stride) {
 
 extern "C" {
 
-int chordal_abi_version(void) { return 2; }
+int chordal_abi_version(void) { return 3; }
 
 const char *chordal_strerror(int status) {
     switch (status) {
@@ -98,6 +99,7 @@ const char *chordal_strerror(int status) {
         case CHORDAL_ENOMEM: return "device allocation failed";
         case CHORDAL_EPARSE: return "text input rejected";
         case CHORDAL_EUTF8: return "text input is not valid UTF-8";
+        case CHORDAL_ENCCL: return "NCCL not loadable in this process, or a collective failed";
         default: return "unknown status";
     }
 }
@@ -184,6 +186,26 @@ int chordal_lexbfs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int6
     if (rc) return rc;
     return launch_lexbfs_csr(indptr, indices, n, m, tie_rule, seed, cell, order_dev, pos_dev, parent_dev,
                              w + L.slot, s);
+}
+
+size_t chordal_lexbfs_certify_workspace_bytes(int64_t n) { return n > 0 ? (size_t)n * 8 : 0; }
+
+int chordal_lexbfs_certify_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int64_t m,
+                                 const int32_t *order_dev, int32_t *status_dev, void *ws, size_t ws_bytes,
+                                 void *stream) {
+    int rc = check_dense(adj_dev, n, stride);
+    if (rc) return rc;
+    if (!status_dev) return CHORDAL_EINVAL;
+    cudaStream_t s = as_stream(stream);
+    if (n == 0) return cudaMemsetAsync(status_dev, 0xFF, 2 * sizeof(int32_t), s) == cudaSuccess ? CHORDAL_OK
+                                                                                                 : CHORDAL_ECUDA;
+    if (!order_dev) return CHORDAL_EINVAL;
+    if (n > CHORDAL_DENSE_LEXBFS_MAX_N) return CHORDAL_ETOOLARGE;
+    if (!ws || ws_bytes < chordal_lexbfs_certify_workspace_bytes(n)) return CHORDAL_EINVAL;
+    int32_t *replay = reinterpret_cast<int32_t *>(ws);
+    rc = launch_lexbfs_seg(adj_dev, n, stride, m, 5 /* kTieCertify */, 0, 0, replay, replay + n, nullptr, s,
+                           order_dev, status_dev);
+    return rc;
 }
 
 int chordal_positions(const int32_t *order_dev, int64_t n, int32_t *pos_dev, void *stream) {
@@ -689,3 +711,170 @@ int chordal_gen_chordal_random(uint8_t *adj_dev, int64_t batch, int64_t n, int64
 }
 
 }  // extern "C"
+
+// ---------------------------------------------------------------------------
+// Multi-GPU (row-sharded PEO check) over the caller's NCCL communicator.
+//
+// The protocol of distributed.sharded_is_chordal, for callers without torch:
+// the root rank runs LexBFS (a single graph's step chain stays on one GPU),
+// order + parents are broadcast, every rank checks its contiguous row shard
+// [n r / W, n (r + 1) / W), one 8-byte MIN all-reduce of the witness key, and
+// every rank resolves z locally.  NCCL is not linked: its entry points are
+// resolved from the process (the library that created `comm`, found by its
+// soname) at the first call, so libchordal_b200.so loads without NCCL.
+namespace {
+
+// nccl.h enum values (stable across NCCL 2.x)
+constexpr int kNcclInt32 = 2, kNcclUint64 = 5, kNcclMin = 3;
+
+struct NcclApi {
+    typedef int (*count_t)(void *, int *);
+    typedef int (*bcast_t)(const void *, void *, size_t, int, int, void *, cudaStream_t);
+    typedef int (*allred_t)(const void *, void *, size_t, int, int, void *, cudaStream_t);
+    typedef int (*group_t)();
+    count_t count = nullptr, user_rank = nullptr;
+    bcast_t bcast = nullptr;
+    allred_t allreduce = nullptr;
+    group_t gstart = nullptr, gend = nullptr;
+    bool ok = false;
+};
+
+const NcclApi &nccl_api() {
+    // resolved once; read-only afterwards (a function-local static: thread-safe
+    // initialisation, no mutable state after it)
+    static const NcclApi api = [] {
+        NcclApi a;
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_LOCAL);
+        if (!h) return a;
+        a.count = (NcclApi::count_t)dlsym(h, "ncclCommCount");
+        a.user_rank = (NcclApi::count_t)dlsym(h, "ncclCommUserRank");
+        a.bcast = (NcclApi::bcast_t)dlsym(h, "ncclBroadcast");
+        a.allreduce = (NcclApi::allred_t)dlsym(h, "ncclAllReduce");
+        a.gstart = (NcclApi::group_t)dlsym(h, "ncclGroupStart");
+        a.gend = (NcclApi::group_t)dlsym(h, "ncclGroupEnd");
+        a.ok = a.count && a.user_rank && a.bcast && a.allreduce && a.gstart && a.gend;
+        return a;
+    }();
+    return api;
+}
+
+struct ShardWs {  // key + parent, then the LexBFS workspace
+    size_t key, parent, rest, total;
+    ShardWs(int64_t n, size_t rest_bytes) {
+        auto a = [](size_t x) { return (x + 255) & ~size_t(255); };
+        key = 0;
+        parent = 256;
+        rest = a(parent + sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+        total = rest + rest_bytes;
+    }
+};
+
+// order + parent from the root, positions, this rank's shard of the key, MIN
+// all-reduce.  `key_fn(lo, hi)` launches the shard's key kernel.
+template <typename KeyFn>
+int shard_exchange(const NcclApi &api, void *comm, int root, int64_t n, int32_t *order, int32_t *pos,
+                   int32_t *parent, uint64_t *key, cudaStream_t s, KeyFn key_fn) {
+    int world = 0, rank = 0;
+    if (api.count(comm, &world) || api.user_rank(comm, &rank) || world <= 0) return CHORDAL_ENCCL;
+    if (api.gstart()) return CHORDAL_ENCCL;
+    const int b1 = api.bcast(order, order, (size_t)n, kNcclInt32, root, comm, s);
+    const int b2 = api.bcast(parent, parent, (size_t)n, kNcclInt32, root, comm, s);
+    if (api.gend() || b1 || b2) return CHORDAL_ENCCL;
+    int rc = launch_positions(order, n, pos, s);
+    if (rc) return rc;
+    rc = launch_key_init(key, s);
+    if (rc) return rc;
+    // distributed.shard_bounds: contiguous, balanced to +-1
+    const int64_t base = n / world, extra = n % world;
+    const int64_t lo = rank * base + (rank < extra ? rank : extra), hi = lo + base + (rank < extra ? 1 : 0);
+    if (lo < hi) {
+        rc = key_fn(lo, hi);
+        if (rc) return rc;
+    }
+    // UINT64_MAX ("no violation") is the MIN identity of the unsigned key
+    if (api.allreduce(key, key, 1, kNcclUint64, kNcclMin, comm, s)) return CHORDAL_ENCCL;
+    return CHORDAL_OK;
+}
+
+}  // namespace
+
+size_t chordal_dense_nccl_workspace_bytes(int64_t n, int64_t m) {
+    return ShardWs(n, DenseWs(n, m < 0 ? 0 : m).total).total;
+}
+
+int chordal_is_chordal_dense_nccl(const uint8_t *adj_dev, int64_t n, int64_t stride, int64_t m, int32_t tie_rule,
+                                  uint64_t seed, int32_t root, void *nccl_comm, int32_t *order_dev, int32_t *pos_dev,
+                                  int32_t *witness_dev, void *ws, size_t ws_bytes, void *stream) {
+    int rc = check_dense(adj_dev, n, stride);
+    if (rc) return rc;
+    if (!nccl_comm || !witness_dev || root < 0) return CHORDAL_EINVAL;
+    cudaStream_t s = as_stream(stream);
+    if (n == 0) return cudaMemsetAsync(witness_dev, 0xFF, 3 * sizeof(int32_t), s) == cudaSuccess ? CHORDAL_OK
+                                                                                                  : CHORDAL_ECUDA;
+    if (!order_dev || !pos_dev || !ws) return CHORDAL_EINVAL;
+    if (!use_seg(n) && m < 0) return CHORDAL_EINVAL;  // every rank sizes the same workspace
+    const ShardWs L(n, DenseWs(n, m < 0 ? 0 : m).total);
+    if (ws_bytes < L.total) return CHORDAL_EINVAL;
+    const NcclApi &api = nccl_api();
+    if (!api.ok) return CHORDAL_ENCCL;
+    int world = 0, rank = 0;
+    if (api.count(nccl_comm, &world) || api.user_rank(nccl_comm, &rank)) return CHORDAL_ENCCL;
+    if (root >= world) return CHORDAL_EINVAL;
+    uint8_t *w = reinterpret_cast<uint8_t *>(ws);
+    uint64_t *key = reinterpret_cast<uint64_t *>(w + L.key);
+    int32_t *parent = reinterpret_cast<int32_t *>(w + L.parent);
+    if (rank == root) {
+        // the CTA engine leaves the parents to the PEO check (-2 = search them)
+        if (use_seg(n)) {
+            rc = launch_fill_i32(parent, n, -2, s);
+            if (rc) return rc;
+        }
+        rc = chordal_lexbfs_dense(adj_dev, n, stride, m, tie_rule, seed, order_dev, pos_dev,
+                                  use_seg(n) ? nullptr : parent, w + L.rest, ws_bytes - L.rest, stream);
+        if (rc) return rc;
+    }
+    rc = shard_exchange(api, nccl_comm, root, n, order_dev, pos_dev, parent, key, s, [&](int64_t lo, int64_t hi) {
+        return launch_peo_dense_key(adj_dev, n, stride, order_dev, pos_dev, parent, lo, hi, key, s);
+    });
+    if (rc) return rc;
+    return launch_peo_dense_witness(adj_dev, n, stride, pos_dev, key, witness_dev, s);
+}
+
+size_t chordal_csr_nccl_workspace_bytes(int64_t n, int64_t m) {
+    const size_t peo = (peo_csr_workspace_bytes() + 255) & ~size_t(255);
+    return ShardWs(n, peo + csr_workspace_bytes(n, m < 0 ? 0 : m)).total;
+}
+
+int chordal_is_chordal_csr_nccl(const int64_t *indptr_dev, const int32_t *indices_dev, int64_t n, int64_t m,
+                                int32_t tie_rule, uint64_t seed, int32_t root, void *nccl_comm, int32_t *order_dev,
+                                int32_t *pos_dev, int32_t *witness_dev, void *ws, size_t ws_bytes, void *stream) {
+    if (n < 0 || m < 0 || !nccl_comm || !witness_dev || root < 0) return CHORDAL_EINVAL;
+    cudaStream_t s = as_stream(stream);
+    if (n == 0) return cudaMemsetAsync(witness_dev, 0xFF, 3 * sizeof(int32_t), s) == cudaSuccess ? CHORDAL_OK
+                                                                                                  : CHORDAL_ECUDA;
+    if (!indptr_dev || !indices_dev || !order_dev || !pos_dev || !ws) return CHORDAL_EINVAL;
+    const size_t peo = (peo_csr_workspace_bytes() + 255) & ~size_t(255);
+    const ShardWs L(n, peo + csr_workspace_bytes(n, m));
+    if (ws_bytes < L.total) return CHORDAL_EINVAL;
+    const NcclApi &api = nccl_api();
+    if (!api.ok) return CHORDAL_ENCCL;
+    int world = 0, rank = 0;
+    if (api.count(nccl_comm, &world) || api.user_rank(nccl_comm, &rank)) return CHORDAL_ENCCL;
+    if (root >= world) return CHORDAL_EINVAL;
+    uint8_t *w = reinterpret_cast<uint8_t *>(ws);
+    uint64_t *key = reinterpret_cast<uint64_t *>(w + L.key);
+    int32_t *parent = reinterpret_cast<int32_t *>(w + L.parent);
+    uint8_t *peo_ws = w + L.rest;
+    int rc;
+    if (rank == root) {
+        rc = chordal_lexbfs_csr(indptr_dev, indices_dev, n, m, tie_rule, seed, order_dev, pos_dev, parent,
+                                peo_ws + peo, ws_bytes - L.rest - peo, stream);
+        if (rc) return rc;
+    }
+    rc = shard_exchange(api, nccl_comm, root, n, order_dev, pos_dev, parent, key, s, [&](int64_t lo, int64_t hi) {
+        return chordal_peo_csr_key(indptr_dev, indices_dev, n, pos_dev, parent, lo, hi, key, peo_ws, peo, stream);
+    });
+    if (rc) return rc;
+    return launch_peo_csr_witness(indptr_dev, indices_dev, pos_dev, key, witness_dev, s);
+}

@@ -63,7 +63,22 @@ __device__ unsigned long long seg_prof[16];
 namespace {
 
 constexpr int kSegBig = 0x7FFFFFFF;
+// Internal mode (not an ABI tie rule): replay a given order, pivot i forced to
+// forced[i], and report the first step whose pivot is not in the maximum-label
+// class (the LexBFS invariant the reference's debug / audit modes assert:
+// search.py:270-271 / 313-322, parallel/lexbfs.py:82-129) and the first step
+// whose pivot differs from the LOWEST_INDEX choice.
+constexpr int kTieCertify = 5;
 constexpr int kSegDenseFrac = 8;  // edge density (2m / n^2) from which the kernel runs 512 threads: 1 / 8
+// The one-warp form (ONEWARP, 4 G words per lane) for sparse graphs up to this
+// n: no block barriers, but measured slower -- config 2 chordal 11.9 -> 18.4 ms
+// with one warp of 8 words per lane against two warps of 4 (the second warp's
+// independent work hides more latency than the barriers cost).  Off by default
+// (-DSEG_ONEWARP_MAX_N=16384 builds it).
+#ifndef SEG_ONEWARP_MAX_N
+#define SEG_ONEWARP_MAX_N 0
+#endif
+constexpr int kOneWarpMaxN = SEG_ONEWARP_MAX_N;
 
 struct SegLayout {
     size_t A, An, P, U, RA, F, NB, bnd, Pc, LB, NBq, TW, wt, misc, wslot, total;
@@ -74,7 +89,7 @@ struct SegLayout {
         A = o; o = align16(o + np * 2);
         An = o; o = align16(o + np * 2);
         P = o; o = align16(o + np * 2);
-        const size_t WP = size_t(W + 3) & ~size_t(3);  // words rounded up to 128-bit groups
+        const size_t WP = size_t(W + 31) & ~size_t(31);  // words rounded up to a thread's word group (<= 32)
         U = o; o = align16(o + WP * 4);
         RA = o; o = align16(o + WP * 4);
         F = o; o = align16(o + WP * 4);
@@ -101,12 +116,14 @@ __device__ __forceinline__ bool seg_better(uint64_t s1, int32_t i1, uint64_t s2,
 
 template <int MODE>
 __device__ __forceinline__ uint64_t seg_tie_score(int32_t v, uint64_t prefix) {
-    if (MODE == CHORDAL_TIE_ASCENDING) return (uint64_t)(0x7FFFFFFF - v);
+    if (MODE == CHORDAL_TIE_ASCENDING || MODE == kTieCertify) return (uint64_t)(0x7FFFFFFF - v);
     if (MODE == CHORDAL_TIE_DESCENDING) return (uint64_t)v;
     return splitmix64(prefix ^ (uint64_t)(v + 1));  // Arbitration.choose, parallel/engine.py:47-53
 }
 
-// Block-wide (score, id) max, broadcast to every thread.  Two barriers.
+// Block-wide (score, id) max, broadcast to every thread.  Two barriers (none
+// for a one-warp block).
+template <bool ONEWARP>
 __device__ __forceinline__ void seg_block_max(uint64_t &s, int32_t &id, uint64_t *rs, int32_t *ri) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
 #pragma unroll
@@ -115,6 +132,7 @@ __device__ __forceinline__ void seg_block_max(uint64_t &s, int32_t &id, uint64_t
         int32_t i2 = __shfl_xor_sync(CH_FULL, id, d);
         if (seg_better(s2, i2, s, id)) { s = s2; id = i2; }
     }
+    if (ONEWARP) return;
     if (lane == 0) { rs[warp] = s; ri[warp] = id; }
     __syncthreads();
     s = lane < nw ? rs[lane] : 0;
@@ -130,8 +148,9 @@ __device__ __forceinline__ void seg_block_max(uint64_t &s, int32_t &id, uint64_t
 
 // Block-wide exclusive scans, thread t = word t: sums of a and e, max of h
 // (identity 0), suffix min of l (identity kSegBig).  Totals of a and e are
-// returned to every thread.  One barrier; wt (4 x 32 ints) is free again
-// after the caller's next barrier.
+// returned to every thread.  One barrier (none for a one-warp block); wt (4 x
+// 32 ints) is free again after the caller's next barrier.
+template <bool ONEWARP>
 __device__ __forceinline__ void seg_scan4(int a, int e, int h, int l, int *wt, int &xa, int &xe, int &xh, int &xl,
                                           int &ta, int &te) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
@@ -151,6 +170,11 @@ __device__ __forceinline__ void seg_scan4(int a, int e, int h, int l, int *wt, i
     xl = __shfl_down_sync(CH_FULL, il, 1);
     if (lane == 0) xh = 0;
     if (lane == 31) xl = kSegBig;
+    if (ONEWARP) {
+        ta = __shfl_sync(CH_FULL, ia, 31);
+        te = __shfl_sync(CH_FULL, ie, 31);
+        return;
+    }
     __syncthreads();
     int pa = lane < NW ? wt[lane] : 0, pe = lane < NW ? wt[32 + lane] : 0;
     int ph = lane < NW ? wt[64 + lane] : 0, pl = lane < NW ? wt[96 + lane] : kSegBig;
@@ -169,7 +193,9 @@ __device__ __forceinline__ void seg_scan4(int a, int e, int h, int l, int *wt, i
     if (warp + 1 < NW) xl = min(xl, wl);
 }
 
-// Exclusive sum scan of e only (the append-only steps).  One barrier.
+// Exclusive sum scan of e only (the append-only steps).  One barrier (none for
+// a one-warp block).
+template <bool ONEWARP>
 __device__ __forceinline__ int seg_scan1(int e, int *wt, int &te) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, NW = blockDim.x >> 5;
     int ie = e;
@@ -178,8 +204,12 @@ __device__ __forceinline__ int seg_scan1(int e, int *wt, int &te) {
         const int oe = __shfl_up_sync(CH_FULL, ie, d);
         if (lane >= d) ie += oe;
     }
-    if (lane == 31) wt[32 + warp] = ie;
     int xe = ie - e;
+    if (ONEWARP) {
+        te = __shfl_sync(CH_FULL, ie, 31);
+        return xe;
+    }
+    if (lane == 31) wt[32 + warp] = ie;
     __syncthreads();
     int pe = lane < NW ? wt[32 + lane] : 0;
 #pragma unroll
@@ -198,10 +228,14 @@ __device__ __forceinline__ int seg_scan1(int e, int *wt, int &te) {
 // MV: movers handled per round of a thread's mover loop (their position loads
 // overlap): 4 for dense graphs (many movers per thread), 2 otherwise (config 2
 // chordal 12.53 -> 12.07 ms; G(8192, 0.5) would go 0.260 -> 0.274 ms with 2).
-template <int MODE, int MV>
-__global__ void __launch_bounds__(512, 1)
+// G: 128-bit word groups per thread (thread t owns words [4 G t, 4 G (t + 1))).
+// ONEWARP: the block is one warp -- every barrier is a __syncwarp and the
+// block scans are warp scans (sparse graphs up to n = 16384, G = n / 4096).
+template <int MODE, int MV, int G, bool ONEWARP>
+__global__ void __launch_bounds__(ONEWARP ? 32 : 512, 1)
 lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint64_t seed, uint64_t cell,
-                  int32_t *__restrict__ order, int32_t *__restrict__ pos_out, int32_t *__restrict__ parent) {
+                  int32_t *__restrict__ order, int32_t *__restrict__ pos_out, int32_t *__restrict__ parent,
+                  const int32_t *__restrict__ forced, int32_t *__restrict__ status) {
     extern __shared__ __align__(16) uint8_t smem[];
     const int W = (n + 31) >> 5;
     const int WP = (W + 3) & ~3;
@@ -229,9 +263,17 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
     int32_t *red_i = (int32_t *)(smem + L.wt + 32 * 8);
 
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-    const int NT = blockDim.x, NW = NT >> 5;
-    const int w0 = 4 * t;  // this thread owns vertex / position words [w0, w0 + 4)
+    const int NT = ONEWARP ? 32 : blockDim.x, NW = NT >> 5;
+    constexpr int WT = 4 * G;                      // words per thread
+    constexpr int LG = G == 1 ? 2 : (G == 2 ? 3 : (G == 4 ? 4 : 5));  // log2(WT)
+    static_assert(G == 1 || G == 2 || G == 4 || G == 8, "G");
+    const int w0 = WT * t;  // this thread owns vertex / position words [w0, w0 + WT)
     const bool own = w0 < W;
+#define SEG_SYNC()                   \
+    do {                             \
+        if (ONEWARP) __syncwarp();   \
+        else __syncthreads();        \
+    } while (0)
 
     for (int w = t; w < WP; w += NT) {
         U[w] = w < W - 1 ? CH_FULL : (w == W - 1 ? ((n & 31) ? mask_below(n & 31) : CH_FULL) : 0u);
@@ -244,16 +286,21 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
     if (t < 24) misc[t] = (t & 7) == 2 ? kSegBig : ((t & 7) == 3 ? -1 : 0);
     if (parent)
         for (int v = t; v < n; v += NT) parent[v] = -1;
-    __syncthreads();
+    SEG_SYNC();
     // Every rule starts at vertex 0 (vertex 1 in the reference: the smallest id
     // for LOWEST_INDEX, pinned for parallel_lexbfs, parallel/lexbfs.py:173).
     if (t == 0) {
-        A[0] = 0;
-        P[0] = 0;
-        U[0] &= ~1u;
+        const int v0 = MODE == kTieCertify ? forced[0] : 0;
+        A[0] = (uint16_t)v0;
+        P[v0] = 0;
+        U[v0 >> 5] &= ~(1u << (v0 & 31));
         bnd[0] = 1u;
+        if (MODE == kTieCertify) {
+            status[0] = kSegBig;
+            status[1] = v0 != 0 ? 0 : kSegBig;
+        }
     }
-    __syncthreads();
+    SEG_SYNC();
 
     const uint32_t *rows = reinterpret_cast<const uint32_t *>(adj);
     const long long sw = stride >> 2;  // row pitch in words (a multiple of 4)
@@ -262,7 +309,9 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
 #endif
     int tail = 1, nclasses = 1;
     int guess = -1;
-    uint4 nxt = make_uint4(0, 0, 0, 0);
+    uint4 nxt[G];
+#pragma unroll
+    for (int g = 0; g < G; ++g) nxt[g] = make_uint4(0, 0, 0, 0);
 
     for (int i = 0; i < n; ++i) {
         // ---- pivot ---------------------------------------------------------
@@ -294,7 +343,22 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                 }
             }
             if (id < 0) s = 0;
-            seg_block_max(s, id, red_s, red_i);
+            // certify: the forced pivot must be unreached (every unreached vertex
+            // has the empty label); U is read before thread 0 updates it
+            const int fx = MODE == kTieCertify ? forced[i] : -1;
+            const bool fbad = MODE == kTieCertify && !((U[fx >> 5] >> (fx & 31)) & 1u);
+            seg_block_max<ONEWARP>(s, id, red_s, red_i);
+            if (MODE == kTieCertify) {
+                if (fbad) {
+                    if (t == 0) {
+                        status[0] = i;
+                        atomicMin(status + 1, i);
+                    }
+                    break;
+                }
+                if (t == 0 && fx != id) atomicMin(status + 1, i);
+                id = fx;
+            }
             if (t == 0) {
                 A[i] = (uint16_t)id;
                 P[id] = (uint16_t)i;
@@ -303,8 +367,8 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
             }
             tail = i + 1;
             nclasses = 1;
-            __syncthreads();
-        } else if (MODE == CHORDAL_TIE_SEEDED_ARB && i > 0) {
+            SEG_SYNC();
+        } else if ((MODE == CHORDAL_TIE_SEEDED_ARB || MODE == kTieCertify) && i > 0) {
             // Elect within the max-label class [i, e): all its members offer
             // themselves as `current` (parallel/lexbfs.py:216-225).
             int e = tail;
@@ -323,6 +387,29 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                     break;
                 }
             }
+            if (MODE == kTieCertify) {
+                // the forced pivot must be a reached vertex of the head class [i, e)
+                const int fx = forced[i];
+                const bool reached = ((RA[fx >> 5] >> (fx & 31)) & 1u) != 0;
+                const int fp = reached ? (int)P[fx] : -1;
+                const int a0 = A[i];
+                if (fp < i || fp >= e) {
+                    if (t == 0) {
+                        status[0] = i;
+                        atomicMin(status + 1, i);
+                    }
+                    break;
+                }
+                SEG_SYNC();  // everyone has read A[i] / P[fx]
+                if (t == 0 && fp != i) {
+                    atomicMin(status + 1, i);
+                    A[i] = (uint16_t)fx;
+                    A[fp] = (uint16_t)a0;
+                    P[fx] = (uint16_t)i;
+                    P[a0] = (uint16_t)fp;
+                }
+                SEG_SYNC();
+            } else {
             const uint64_t prefix = mix64_3(seed, (uint64_t)(4 * (i - 1) + 3), cell);
             uint64_t s = 0;
             int32_t id = -1, bp = -1;
@@ -332,7 +419,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                 if (id < 0 || seg_better(sc, v, s, id)) { s = sc; id = v; bp = p; }
             }
             const int32_t my_id = id;
-            seg_block_max(s, id, red_s, red_i);
+            seg_block_max<ONEWARP>(s, id, red_s, red_i);
             if (my_id == id && bp >= 0 && bp != i) {  // exactly one thread holds the winner
                 const uint16_t t0 = A[i];
                 A[i] = (uint16_t)id;
@@ -340,7 +427,8 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                 P[id] = (uint16_t)i;
                 P[t0] = (uint16_t)bp;
             }
-            __syncthreads();
+            SEG_SYNC();
+            }
         }
 
 #ifdef SEG_PROFILE
@@ -359,23 +447,34 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
         }
         int *fl = misc + 8 * (i % 3);
         // ---- phase 1: movers and newly reached vertices, 128-bit row loads --
-        uint32_t r[4] = {0u, 0u, 0u, 0u}, ext[4] = {0u, 0u, 0u, 0u};
+        uint32_t r[WT], ext[WT];
+#pragma unroll
+        for (int k = 0; k < WT; ++k) r[k] = ext[k] = 0u;
         int extc = 0, cnt = 0, pmn = kSegBig, pmx = -1;
         if (own) {
-            const uint4 rw = (x == guess) ? nxt : ld_nc_v4(rows + (long long)x * sw + w0);
-            r[0] = rw.x; r[1] = rw.y; r[2] = rw.z; r[3] = rw.w;
+            const bool hit = x == guess;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+                const uint4 rw = hit ? nxt[g] : ld_nc_v4(rows + (long long)x * sw + w0 + 4 * g);
+                r[4 * g] = rw.x; r[4 * g + 1] = rw.y; r[4 * g + 2] = rw.z; r[4 * g + 3] = rw.w;
+            }
         }
 #ifdef SEG_PROFILE
         const int guess_prev = guess;
 #endif
         guess = hpos < tail0 ? (int)A[hpos] : -1;
         if (own) {
-            if ((x >> 7) == t) RA[x >> 5] &= ~(1u << (x & 31));
-            const uint4 ra4 = *reinterpret_cast<const uint4 *>(RA + w0);
-            const uint4 u4 = *reinterpret_cast<const uint4 *>(U + w0);
-            const uint32_t ra[4] = {ra4.x, ra4.y, ra4.z, ra4.w}, uu[4] = {u4.x, u4.y, u4.z, u4.w};
+            if (((x >> 5) >> LG) == t) RA[x >> 5] &= ~(1u << (x & 31));
+            uint32_t ra[WT], uu[WT];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int g = 0; g < G; ++g) {
+                const uint4 ra4 = *reinterpret_cast<const uint4 *>(RA + w0 + 4 * g);
+                const uint4 u4 = *reinterpret_cast<const uint4 *>(U + w0 + 4 * g);
+                ra[4 * g] = ra4.x; ra[4 * g + 1] = ra4.y; ra[4 * g + 2] = ra4.z; ra[4 * g + 3] = ra4.w;
+                uu[4 * g] = u4.x; uu[4 * g + 1] = u4.y; uu[4 * g + 2] = u4.z; uu[4 * g + 3] = u4.w;
+            }
+#pragma unroll
+            for (int k = 0; k < WT; ++k) {
                 uint32_t m2 = r[k] & ra[k];
                 ext[k] = r[k] & uu[k];
                 extc += __popc(ext[k]);
@@ -404,7 +503,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
             if (extc) {
                 if (parent) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) {
+                    for (int k = 0; k < WT; ++k) {
                         uint32_t m3 = ext[k];
                         while (m3) {
                             const int b = __ffs(m3) - 1;
@@ -413,10 +512,14 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                         }
                     }
                 }
-                *reinterpret_cast<uint4 *>(U + w0) = make_uint4(uu[0] & ~ext[0], uu[1] & ~ext[1], uu[2] & ~ext[2],
-                                                                uu[3] & ~ext[3]);
-                *reinterpret_cast<uint4 *>(RA + w0) = make_uint4(ra[0] | ext[0], ra[1] | ext[1], ra[2] | ext[2],
-                                                                 ra[3] | ext[3]);
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const int k = 4 * g;
+                    *reinterpret_cast<uint4 *>(U + w0 + k) = make_uint4(uu[k] & ~ext[k], uu[k + 1] & ~ext[k + 1],
+                                                                        uu[k + 2] & ~ext[k + 2], uu[k + 3] & ~ext[k + 3]);
+                    *reinterpret_cast<uint4 *>(RA + w0 + k) = make_uint4(ra[k] | ext[k], ra[k + 1] | ext[k + 1],
+                                                                         ra[k + 2] | ext[k + 2], ra[k + 3] | ext[k + 3]);
+                }
                 fl[0] = 1;
             }
         }
@@ -427,7 +530,10 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
         // (into the registers the current row just left) it stalled that loop
         // (c3 chordal 90.5 -> 86.5 ms); an extra L2 prefetch of the row after
         // it no longer pays once the load sits here.
-        if (guess >= 0 && own) nxt = ld_nc_v4(rows + (long long)guess * sw + w0);
+        if (guess >= 0 && own) {
+#pragma unroll
+            for (int g = 0; g < G; ++g) nxt[g] = ld_nc_v4(rows + (long long)guess * sw + w0 + 4 * g);
+        }
         // mover count and position range: per-warp slots, reduced after B1 by
         // every warp (lane w reads warp w's slot) -- same-address shared atomics
         // from every warp cost ~1 % of a step at N = 32768
@@ -443,7 +549,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
             }
         }
         if (t < 8) misc[8 * ((i + 1) % 3) + t] = t == 2 ? kSegBig : (t == 3 ? -1 : 0);
-        __syncthreads();  // B1
+        SEG_SYNC();  // B1
         SEG_T(2);
 #ifdef SEG_PROFILE
         if (x == guess_prev) seg_acc[8]++;
@@ -459,10 +565,12 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                           !(cntA == gmx - gmn + 1 && (gmn == hpos || ((bnd[gmn >> 5] >> (gmn & 31)) & 1u)) &&
                             (gmx + 1 >= tail0 || ((bnd[(gmx + 1) >> 5] >> ((gmx + 1) & 31)) & 1u)));
         int ktot = 0, xe = 0;
-        uint32_t nbadd[4] = {0u, 0u, 0u, 0u};
+        uint32_t nbadd[WT];
+#pragma unroll
+        for (int k = 0; k < WT; ++k) nbadd[k] = 0u;
 
         if (!full) {
-            if (anyE) xe = seg_scan1(extc, wt, ktot);
+            if (anyE) xe = seg_scan1<ONEWARP>(extc, wt, ktot);
         } else {
 #ifdef SEG_PROFILE
             seg_acc[1]++;
@@ -494,15 +602,20 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                 if (lo >= 0 && lo < 32) b |= 1u << lo;
                 return b;
             };
-            uint32_t f[4] = {0u, 0u, 0u, 0u}, b[4] = {0u, 0u, 0u, 0u};
-            int cpre[4], hb[4], lbw[4];
+            uint32_t f[WT], b[WT];
+            int cpre[WT], hb[WT], lbw[WT];
             int ctot = 0, hmax = 0, lmin = kSegBig;
+#pragma unroll
+            for (int k = 0; k < WT; ++k) f[k] = b[k] = 0u;
             if (own) {
-                const uint4 f4 = *reinterpret_cast<const uint4 *>(F + w0);
-                f[0] = f4.x; f[1] = f4.y; f[2] = f4.z; f[3] = f4.w;
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const uint4 f4 = *reinterpret_cast<const uint4 *>(F + w0 + 4 * g);
+                    f[4 * g] = f4.x; f[4 * g + 1] = f4.y; f[4 * g + 2] = f4.z; f[4 * g + 3] = f4.w;
+                }
             }
 #pragma unroll
-            for (int k = 0; k < 4; ++k) {
+            for (int k = 0; k < WT; ++k) {
                 if (own) b[k] = breg(w0 + k);
                 cpre[k] = ctot;
                 ctot += __popc(f[k]);
@@ -512,32 +625,41 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                 lmin = min(lmin, lbw[k]);
             }
             int xa, xh, xl, ta;
-            seg_scan4(ctot, extc, hmax, lmin, wt, xa, xe, xh, xl, ta, ktot);
-            int nbq[4], lbq[4];
+            seg_scan4<ONEWARP>(ctot, extc, hmax, lmin, wt, xa, xe, xh, xl, ta, ktot);
+            int nbq[WT], lbq[WT];
             {
                 int run = xh;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) { lbq[k] = run; run = max(run, hb[k]); }
+                for (int k = 0; k < WT; ++k) { lbq[k] = run; run = max(run, hb[k]); }
                 run = min(xl, tail0);
 #pragma unroll
-                for (int k = 3; k >= 0; --k) { nbq[k] = run; run = min(run, lbw[k]); }
+                for (int k = WT - 1; k >= 0; --k) { nbq[k] = run; run = min(run, lbw[k]); }
             }
             if (own) {
-                *reinterpret_cast<uint2 *>(Pc + w0) =
-                    make_uint2((uint32_t)(xa + cpre[0]) | ((uint32_t)(xa + cpre[1]) << 16),
-                               (uint32_t)(xa + cpre[2]) | ((uint32_t)(xa + cpre[3]) << 16));
-                *reinterpret_cast<uint2 *>(LB + w0) = make_uint2((uint32_t)lbq[0] | ((uint32_t)lbq[1] << 16),
-                                                                 (uint32_t)lbq[2] | ((uint32_t)lbq[3] << 16));
-                *reinterpret_cast<uint2 *>(NBq + w0) = make_uint2((uint32_t)nbq[0] | ((uint32_t)nbq[1] << 16),
-                                                                  (uint32_t)nbq[2] | ((uint32_t)nbq[3] << 16));
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const int k = 4 * g;
+                    *reinterpret_cast<uint2 *>(Pc + w0 + k) =
+                        make_uint2((uint32_t)(xa + cpre[k]) | ((uint32_t)(xa + cpre[k + 1]) << 16),
+                                   (uint32_t)(xa + cpre[k + 2]) | ((uint32_t)(xa + cpre[k + 3]) << 16));
+                    *reinterpret_cast<uint2 *>(LB + w0 + k) =
+                        make_uint2((uint32_t)lbq[k] | ((uint32_t)lbq[k + 1] << 16),
+                                   (uint32_t)lbq[k + 2] | ((uint32_t)lbq[k + 3] << 16));
+                    *reinterpret_cast<uint2 *>(NBq + w0 + k) =
+                        make_uint2((uint32_t)nbq[k] | ((uint32_t)nbq[k + 1] << 16),
+                                   (uint32_t)nbq[k + 2] | ((uint32_t)nbq[k + 3] << 16));
+                }
             }
-            __syncthreads();  // B2
+            SEG_SYNC();  // B2
             SEG_T(4);
             {
                 const int g = fl[6];
                 if (g >= 0 && g != guess) {
                     guess = g;
-                    if (own) nxt = ld_nc_v4(rows + (long long)g * sw + w0);
+                    if (own) {
+#pragma unroll
+                        for (int gg = 0; gg < G; ++gg) nxt[gg] = ld_nc_v4(rows + (long long)g * sw + w0 + 4 * gg);
+                    }
                 }
             }
             // ---- phase 3a: list the words of split classes ------------------------
@@ -567,7 +689,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
             };
             if (own) {
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < WT; ++k) {
                     const int q = w0 + k;
                     const int lo = max(32 * q, max(hpos, span_s)), hi = min(32 * q + 32, min(tail0, span_e));
                     if (lo >= hi) continue;
@@ -584,7 +706,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                     if (touched) TW[atomicAdd(fl + 4, 1)] = (uint16_t)q;
                 }
             }
-            __syncthreads();  // B2.5
+            SEG_SYNC();  // B2.5
             SEG_T(5);
             const int ntouch = fl[4];
 #ifdef SEG_PROFILE
@@ -658,7 +780,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
 #ifdef SEG_PROFILE
             const long long own1 = clock64();
 #endif
-            __syncthreads();  // B3
+            SEG_SYNC();  // B3
 #ifdef SEG_PROFILE
             {  // 3b: [12] thread 0's own loop cycles, [13] cycles waiting at B3 for the others
                 seg_acc[12] += (unsigned long long)(own1 - own0);
@@ -687,24 +809,33 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                 }
             }
             if (own) {
-                const uint4 nb4 = *reinterpret_cast<const uint4 *>(NB + w0);
-                nbadd[0] = nb4.x; nbadd[1] = nb4.y; nbadd[2] = nb4.z; nbadd[3] = nb4.w;
-                if (nb4.x | nb4.y | nb4.z | nb4.w) *reinterpret_cast<uint4 *>(NB + w0) = make_uint4(0, 0, 0, 0);
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const uint4 nb4 = *reinterpret_cast<const uint4 *>(NB + w0 + 4 * g);
+                    nbadd[4 * g] = nb4.x; nbadd[4 * g + 1] = nb4.y; nbadd[4 * g + 2] = nb4.z; nbadd[4 * g + 3] = nb4.w;
+                    if (nb4.x | nb4.y | nb4.z | nb4.w)
+                        *reinterpret_cast<uint4 *>(NB + w0 + 4 * g) = make_uint4(0, 0, 0, 0);
+                }
             }
         }
         // ---- end of step: clear flags, new class starts, append -----------------
         if (own) {
-            if (cntA && (w0 + 3) >= (gmn >> 5) && w0 <= (gmx >> 5))
-                *reinterpret_cast<uint4 *>(F + w0) = make_uint4(0, 0, 0, 0);
-            if (hpos < tail0 && (hpos >> 7) == t) nbadd[(hpos >> 5) & 3] |= 1u << (hpos & 31);
-            if (ktot > 0 && (tail0 >> 7) == t) nbadd[(tail0 >> 5) & 3] |= 1u << (tail0 & 31);
+            if (cntA && (w0 + WT - 1) >= (gmn >> 5) && w0 <= (gmx >> 5)) {
 #pragma unroll
-            for (int k = 0; k < 4; ++k)
+                for (int g = 0; g < G; ++g) *reinterpret_cast<uint4 *>(F + w0 + 4 * g) = make_uint4(0, 0, 0, 0);
+            }
+#pragma unroll
+            for (int k = 0; k < WT; ++k) {
+                if (hpos < tail0 && (hpos >> 5) == w0 + k) nbadd[k] |= 1u << (hpos & 31);
+                if (ktot > 0 && (tail0 >> 5) == w0 + k) nbadd[k] |= 1u << (tail0 & 31);
+            }
+#pragma unroll
+            for (int k = 0; k < WT; ++k)
                 if (nbadd[k]) bnd[w0 + k] |= nbadd[k];
             if (extc) {  // the newly reached vertices: one class after the tail, tie order
                 int idx = xe;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
+                for (int k = 0; k < WT; ++k) {
                     uint32_t e2 = ext[k];
                     while (e2) {
                         const int b = __ffs(e2) - 1;
@@ -721,12 +852,16 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
             tail = tail0 + ktot;
             ++nclasses;
         }
-        __syncthreads();  // B4
+        SEG_SYNC();  // B4
         SEG_T(full ? 7 : 3);
         // ---- early exit: everything reached, every class a singleton ----------
         if (tail == n && nclasses == tail - hpos) {
             for (int p = hpos + t; p < n; p += NT) {
                 const int v = A[p];
+                if (MODE == kTieCertify && forced[p] != v) {  // every class a singleton: the order is fixed
+                    atomicMin(status, p);
+                    atomicMin(status + 1, p);
+                }
                 order[p] = v;
                 pos_out[v] = p;
                 // the skipped steps would still have refreshed this vertex's
@@ -736,10 +871,15 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
             break;
         }
     }
+    if (MODE == kTieCertify) {  // "no such step" -> -1
+        SEG_SYNC();
+        if (t < 2 && status[t] == kSegBig) status[t] = -1;
+    }
 #ifdef SEG_PROFILE
     if (t == 0)
         for (int k = 0; k < 16; ++k) seg_prof[k] = seg_acc[k];
 #endif
+#undef SEG_SYNC
 }
 
 size_t seg_smem_bytes(int64_t n) { return SegLayout((int)((n + 31) >> 5)).total; }
@@ -785,10 +925,12 @@ lexbfs_warp_kernel(const uint8_t *__restrict__ adj, int n, long long stride, int
 }
 
 int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int64_t m, int32_t tie_rule, uint64_t seed, uint64_t cell,
-                      int32_t *order, int32_t *pos, int32_t *parent, cudaStream_t stream) {
+                      int32_t *order, int32_t *pos, int32_t *parent, cudaStream_t stream,
+                      const int32_t *forced = nullptr, int32_t *status = nullptr) {
     if (n <= 0) return CHORDAL_OK;
     if (n > CHORDAL_DENSE_LEXBFS_MAX_N) return CHORDAL_ETOOLARGE;
-    if (n <= 1024 && tie_rule != CHORDAL_TIE_SEEDED_ARB) {
+    if (tie_rule == kTieCertify && (!forced || !status)) return CHORDAL_EINVAL;
+    if (n <= 1024 && tie_rule != CHORDAL_TIE_SEEDED_ARB && tie_rule != kTieCertify) {
         const size_t state = (size_t((n + 31) >> 5) * 32 * 2 * 4 + 256 + 15) & ~size_t(15);
         const size_t rows = (size_t)n * stride;
         const bool stage = state + rows <= 200 * 1024;  // rows staged in shared memory when they fit
@@ -813,33 +955,55 @@ int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int64_t m, 
     // steps) run their partition phases (3b / 3c, one warp per four split-class
     // words) on 512 threads: G(32768, 0.5) 0.68 -> 0.60 ms, while the sparser
     // configuration-3 chordal graph (average degree 1005) is faster on 256
-    // (69.8 vs 71.6 ms, tools/seg_time.cu).
+    // (69.8 vs 71.6 ms, tools/seg_time.cu).  Sparse graphs (m known, below that
+    // density) with n <= kOneWarpMaxN run on one warp with 4 G words per lane:
+    // no block barriers, warp scans only.
     int T = max(32, ((W + 3) / 4 + 31) / 32 * 32);
     const bool dense = m >= 0 && n > 1024 && 2 * m * kSegDenseFrac >= n * n;
+    const bool onewarp = m > 0 && !dense && n <= kOneWarpMaxN;
     if (dense) T = max(T, 512);
 #ifdef SEG_THREADS_ENV
     if (const char *ev = getenv("SEG_THREADS")) T = max(max(32, ((W + 3) / 4 + 31) / 32 * 32), atoi(ev));
+    if (const char *ev = getenv("SEG_THREADS_DENSE")) if (dense) T = atoi(ev);
 #endif
     const size_t smem = seg_smem_bytes(n);
     cudaError_t e;
-#define SEG_LAUNCH_MV(M, K)                                                                                       \
-    e = cudaFuncSetAttribute(lexbfs_seg_kernel<M, K>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);     \
+#define SEG_LAUNCH_K(M, K, GG, OW, NTH)                                                                           \
+    e = cudaFuncSetAttribute(lexbfs_seg_kernel<M, K, GG, OW>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
+                             (int)smem);                                                                           \
     if (e != cudaSuccess) return CHORDAL_ECUDA;                                                                    \
-    lexbfs_seg_kernel<M, K><<<1, T, smem, stream>>>(adj, (int)n, stride, seed, cell, order, pos, parent);
-#define SEG_LAUNCH(M)                \
-    if (dense) {                     \
-        SEG_LAUNCH_MV(M, 4)          \
-    } else {                         \
-        SEG_LAUNCH_MV(M, 2)          \
+    lexbfs_seg_kernel<M, K, GG, OW><<<1, NTH, smem, stream>>>(adj, (int)n, stride, seed, cell, order, pos, parent, \
+                                                              forced, status);
+#if SEG_ONEWARP_MAX_N > 0
+#define SEG_LAUNCH(M)                                         \
+    if (dense) {                                              \
+        SEG_LAUNCH_K(M, 4, 1, false, T)                       \
+    } else if (onewarp && W <= 128) {                         \
+        SEG_LAUNCH_K(M, 2, 1, true, 32)                       \
+    } else if (onewarp && W <= 256) {                         \
+        SEG_LAUNCH_K(M, 2, 2, true, 32)                       \
+    } else if (onewarp) {                                     \
+        SEG_LAUNCH_K(M, 2, 4, true, 32)                       \
+    } else {                                                  \
+        SEG_LAUNCH_K(M, 2, 1, false, T)                       \
     }
+#else
+#define SEG_LAUNCH(M)                                         \
+    if (dense) {                                              \
+        SEG_LAUNCH_K(M, 4, 1, false, T)                       \
+    } else {                                                  \
+        SEG_LAUNCH_K(M, 2, 1, false, T)                       \
+    }
+#endif
     switch (tie_rule) {
         case CHORDAL_TIE_ASCENDING: SEG_LAUNCH(CHORDAL_TIE_ASCENDING); break;
         case CHORDAL_TIE_DESCENDING: SEG_LAUNCH(CHORDAL_TIE_DESCENDING); break;
         case CHORDAL_TIE_SEEDED_ARB: SEG_LAUNCH(CHORDAL_TIE_SEEDED_ARB); break;
+        case kTieCertify: SEG_LAUNCH(kTieCertify); break;
         default: return CHORDAL_EINVAL;
     }
 #undef SEG_LAUNCH
-#undef SEG_LAUNCH_MV
+#undef SEG_LAUNCH_K
     CH_LAUNCH_CHECK();
     return CHORDAL_OK;
 }

@@ -254,6 +254,7 @@ __device__ void bfs_warp(const Rows &R, int n, uint64_t key, uint32_t *queued, i
                     }
                 }
             }
+            __syncwarp();  // the lanes' queued[] reads above precede lane 0's write
             if (lane == 0) {
                 queued[s >> 5] |= 1u << (s & 31);
                 order[tail] = s;

@@ -81,6 +81,16 @@ struct CsrStagedSource {
     T *buf;      // shared memory, bufcap entries
     int bufcap;
     mutable int64_t base;
+    // Each list is read once per search (when its vertex is the pivot): loaded
+    // evict-first, so the engine's class / slot state keeps its L2 lines
+    // (config 5: 64 MB of lists against ~76 MB of state in a 126 MB L2).
+#ifndef CSR_NO_EVICT_FIRST
+    __device__ __forceinline__ static uint64_t list_policy() { return l2_policy_evict_first(); }
+    __device__ __forceinline__ static int32_t ld_list(const int32_t *a, uint64_t pol) { return ld_nc_hint(a, pol); }
+#else
+    __device__ __forceinline__ static uint64_t list_policy() { return 0; }
+    __device__ __forceinline__ static int32_t ld_list(const int32_t *a, uint64_t) { return __ldg(a); }
+#endif
     __device__ __forceinline__ void bounds(int x, int64_t &b, int64_t &e) const {
         b = __ldg(indptr + x);
         e = __ldg(indptr + x + 1);
@@ -91,20 +101,21 @@ struct CsrStagedSource {
         const int cnt = (int)(hi - lo);
         const int32_t *src = indices + lo;
         int k = lane;
+        const uint64_t pol = list_policy();
         for (; k + 224 < cnt; k += 256) {
             int32_t a[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) a[j] = __ldg(src + k + 32 * j);
+            for (int j = 0; j < 8; ++j) a[j] = ld_list(src + k + 32 * j, pol);
 #pragma unroll
             for (int j = 0; j < 8; ++j) buf[k + 32 * j] = (T)a[j];
         }
-        for (; k < cnt; k += 32) buf[k] = (T)__ldg(src + k);
+        for (; k < cnt; k += 32) buf[k] = (T)ld_list(src + k, pol);
         base = lo;
         __syncwarp();
     }
     __device__ __forceinline__ int get(int64_t e) const { return (int)buf[e - base]; }
     // one list entry straight from global memory (the <= 32-neighbour fast step)
-    __device__ __forceinline__ int fetch(int64_t k) const { return __ldg(indices + k); }
+    __device__ __forceinline__ int fetch(int64_t k) const { return ld_list(indices + k, list_policy()); }
     // Row bounds of a likely next pivot, issued where they stand (their values
     // are used a step later), and an L2 prefetch of the row itself once they
     // have arrived: the next step's row fetch then skips the indptr round trip
@@ -417,6 +428,7 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
             for (int c = chead; c != (int)C::NIL; c = (int)M.c_next[c], ++k) {
                 const long long xs2 = slot_detail::first_live<I, S>(M, c, (long long)M.c_head[c],
                                                                    (long long)M.c_end[c]);
+                __syncwarp();  // every lane's cls[] reads in first_live precede lane 0's write
                 if (lane == 0) {
                     int v = (int)M.slot_v[xs2];
                     order[k] = (O)v;
@@ -426,6 +438,7 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
                     if (parent) parent[v] = (O)-2;
                     M.cls[v] = C::VISITED;
                 }
+                __syncwarp();  // the next class's first_live reads cls[] after this write
             }
             __syncwarp();
             break;
@@ -565,6 +578,7 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
                 const int ls = ok ? __ffs(peers) - 1 : 0;
                 const int dl = __shfl_sync(CH_FULL, d, ls);
                 const long long stl = __shfl_sync(CH_FULL, start, ls);
+                __syncwarp();  // the candidate-class reads above precede these writes (racecheck)
                 if (ok && ((sm >> ls) & 1u)) {
                     M.slot_v[stl + __popc(peers & lt)] = (I)y;
                     M.cls[y] = (I)dl;
@@ -744,8 +758,9 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
             if (MODE != CHORDAL_TIE_SEEDED_PARTITION) ok = ok && d != c;  // whole-class moves need no slot change
             const uint32_t vm = __ballot_sync(CH_FULL, ok);
             const uint32_t peers = __match_any_sync(CH_FULL, ok ? c : -1) & vm;
+            const int rel = ok ? (int)M.c_cnt[c] : 0;
+            __syncwarp();  // every peer has read c_cnt[c] before its leader advances it
             if (ok) {
-                const int rel = (int)M.c_cnt[c];
                 M.slot_v[top0 + rel + __popc(peers & lt)] = (I)y;
                 M.cls[y] = (I)d;
                 if ((peers & lt) == 0) M.c_cnt[c] = (I)(rel + __popc(peers));

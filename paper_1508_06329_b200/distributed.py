@@ -128,6 +128,61 @@ def sharded_is_chordal(g, *, group=None, backend=None, root: int = 0) -> Chordal
     return ChordalityVerdict(False, witness=WitnessTriple(w0[0] + 1, w0[1] + 1, w0[2] + 1))
 
 
+def _comm_ptr(comm) -> int:
+    """ncclComm_t as an integer: a raw pointer, or the PyCapsule that
+    torch.cuda.nccl.init_rank returns."""
+    import ctypes
+
+    if isinstance(comm, int):
+        return comm
+    get = ctypes.pythonapi.PyCapsule_GetPointer
+    get.restype, get.argtypes = ctypes.c_void_p, [ctypes.py_object, ctypes.c_char_p]
+    name = ctypes.pythonapi.PyCapsule_GetName
+    name.restype, name.argtypes = ctypes.c_char_p, [ctypes.py_object]
+    return int(get(comm, name(comm)))
+
+
+def sharded_is_chordal_nccl(g, comm, *, root: int = 0, tie_rule: int = _native.TIE_ASCENDING,
+                            seed: int = 0) -> ChordalityVerdict:
+    """``sharded_is_chordal`` through the library's own NCCL entry points
+    (chordal_is_chordal_{dense,csr}_nccl): the same protocol for callers that
+    hold an NCCL communicator but no torch.distributed group.  ``comm`` is an
+    ncclComm_t (int) or a torch.cuda.nccl communicator capsule; every rank
+    calls with the same graph on its own GPU."""
+    torch = _native.require_cuda()
+    n = int(g.n)
+    if n == 0:
+        return ChordalityVerdict(True, peo=VertexOrdering(()))
+    c = _comm_ptr(comm)
+    st = _native.stream_ptr()
+    if is_csr(g):
+        ip, ix = device_csr(g)
+        m = int(ix.numel()) // 2
+        dev = ip.device
+        ws = torch.empty(max(int(_native.lib.chordal_csr_nccl_workspace_bytes(n, m)), 16), dtype=torch.uint8,
+                         device=dev)
+        order, pos = (torch.empty(n, dtype=torch.int32, device=dev) for _ in range(2))
+        wit = torch.empty(3, dtype=torch.int32, device=dev)
+        _native.check(_native.lib.chordal_is_chordal_csr_nccl(
+            _native.ptr(ip), _native.ptr(ix), n, m, tie_rule, seed, root, c, _native.ptr(order), _native.ptr(pos),
+            _native.ptr(wit), _native.ptr(ws), ws.numel(), st), "chordal_is_chordal_csr_nccl")
+    else:
+        rows = device_rows(g)
+        m = rows.m if rows.m >= 0 else (ops.count_edges(rows) if n > _native.DENSE_LEXBFS_MAX_N else -1)
+        dev = rows.data.device
+        ws = torch.empty(max(int(_native.lib.chordal_dense_nccl_workspace_bytes(n, m)), 16), dtype=torch.uint8,
+                         device=dev)
+        order, pos = (torch.empty(n, dtype=torch.int32, device=dev) for _ in range(2))
+        wit = torch.empty(3, dtype=torch.int32, device=dev)
+        _native.check(_native.lib.chordal_is_chordal_dense_nccl(
+            rows.ptr, n, rows.stride, m, tie_rule, seed, root, c, _native.ptr(order), _native.ptr(pos),
+            _native.ptr(wit), _native.ptr(ws), ws.numel(), st), "chordal_is_chordal_dense_nccl")
+    w0 = ops.witness_tuple(wit)
+    if w0 is None:
+        return ChordalityVerdict(True, peo=VertexOrdering._trusted(order.cpu().numpy(), pos.cpu().numpy()))
+    return ChordalityVerdict(False, witness=WitnessTriple(w0[0] + 1, w0[1] + 1, w0[2] + 1))
+
+
 def batch_shard(total: int, *, group=None) -> tuple[int, int]:
     """This rank's contiguous range of a batch of ``total`` graphs."""
     import torch.distributed as dist

@@ -47,6 +47,21 @@ def lexbfs(rows: DeviceRows, tie_rule: int = _native.TIE_ASCENDING, seed: int = 
     return order[:n], pos[:n]
 
 
+def lexbfs_certify(rows: DeviceRows, order, m: int = -1, stream=None) -> tuple[int, int]:
+    """Replay LexBFS with the pivots forced to ``order`` (int32 device tensor) ->
+    (first step whose pivot is not in the maximum-label class, first step whose
+    pivot is not the LOWEST_INDEX choice), -1 for none (chordal_lexbfs_certify_dense)."""
+    torch = _native.require_cuda()
+    n, dev = rows.n, rows.data.device
+    status = torch.empty(2, dtype=torch.int32, device=dev)
+    ws = _ws(torch, lib.chordal_lexbfs_certify_workspace_bytes(n), dev)
+    mm = m if m >= 0 else rows.m
+    check(lib.chordal_lexbfs_certify_dense(rows.ptr, n, rows.stride, mm, ptr(order) if n else None, ptr(status),
+                                           ptr(ws), ws.numel(), stream_ptr(stream)), "chordal_lexbfs_certify_dense")
+    s = status.cpu().tolist()
+    return int(s[0]), int(s[1])
+
+
 def _edge_count(rows: DeviceRows, m: int, stream=None) -> int:
     """The edge count the dense entry points need: only graphs above the
     shared-memory engine's limit (n > 32768, CSR route) need it; the others

@@ -35,10 +35,21 @@ def parallel_lexbfs(g, arb: Arbitration, *, backend: str = "auto", workers: int 
                     adj_reuse: bool = False) -> VertexOrdering:
     """LexBFS via the paper's barrier-phase algorithm; starts at vertex 1.
 
-    ``backend``/``workers``/``audit``/``debug_labels``/``adj_reuse`` select
-    CPU execution strategies in the reference; they are validated the same
-    way and all run the same CUDA kernel (its output is independent of them
-    in the reference too, test_parallel_lexbfs.py:98-137, 152-184).
+    ``backend``/``workers``/``adj_reuse`` select CPU execution strategies in
+    the reference; they are validated the same way and all run the same CUDA
+    kernel (its output is independent of them in the reference too,
+    test_parallel_lexbfs.py:98-137, 152-184).  ``audit`` / ``debug_labels``
+    (the reference checks its set-list invariants after every phase,
+    parallel/lexbfs.py:82-129) replay the finished order on the device with its
+    pivots forced and assert that every elected ``current`` carries the largest
+    label -- under fixed ascending priority also that it is the smallest id of
+    its set (search._certified).
     """
     _check_backend(backend, audit, debug_labels, adj_reuse)
-    return pipeline.lexbfs(g, arb.tie_rule, arb.seed or 0)
+    o = pipeline.lexbfs(g, arb.tie_rule, arb.seed or 0)
+    if audit or debug_labels:
+        from ..search import _certified
+
+        exact = arb.mode == "fixed" and arb.direction == "ascending"
+        _certified(g, o, exact, "parallel_lexbfs(audit=True)" if audit else "parallel_lexbfs(debug_labels=True)")
+    return o

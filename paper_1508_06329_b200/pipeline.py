@@ -42,6 +42,34 @@ def lexbfs_linked_seeded(g, tie_rule: int, seed: int) -> VertexOrdering:
     return VertexOrdering._trusted(order.cpu().numpy(), pos.cpu().numpy())
 
 
+def certify_lexbfs(g, o: VertexOrdering) -> tuple[int, int]:
+    """Device certificate of ``o`` as a LexBFS order of ``g`` (ops.lexbfs_certify):
+    0-based (first step whose pivot lacks the maximum label, first step that is
+    not the LOWEST_INDEX choice), -1 for none.  CSR inputs are expanded to
+    bit rows on the device; the replay engine holds n <= 32768."""
+    torch = _native.require_cuda()
+    n = int(g.n)
+    if n == 0:
+        return -1, -1
+    if n > _native.DENSE_LEXBFS_MAX_N:
+        from .errors import GraphTooLarge
+
+        raise GraphTooLarge(f"the device LexBFS certificate (debug / audit) holds n <= "
+                            f"{_native.DENSE_LEXBFS_MAX_N}, got n={n}")
+    if is_csr(g):
+        from .graph import device_stride
+        from .device import DeviceRows
+
+        ip, ix = device_csr(g)
+        u = torch.repeat_interleave(torch.arange(n, dtype=torch.int32, device=ip.device), ip[1:] - ip[:-1])
+        st = device_stride(n)
+        rows = DeviceRows(n, st, ops.edges_to_dense(u, ix[: u.numel()], n, st), m=int(ix.numel()) // 2)
+    else:
+        rows = device_rows(g)
+    order = torch.as_tensor(np.ascontiguousarray(o.order0, dtype=np.int32)).to(rows.data.device)
+    return ops.lexbfs_certify(rows, order)
+
+
 def peo_witness(g, o: VertexOrdering):
     """0-based witness of the PEO test of ordering ``o`` (None when a PEO)."""
     torch = _native.require_cuda()

@@ -95,14 +95,36 @@ def _run_lexbfs(g, tie_break: TieBreak, label: str, method: str) -> VertexOrderi
     return VertexOrdering._trusted(initial[order_r.cpu().numpy()])
 
 
+def _certified(g, o: VertexOrdering, exact_lowest: bool, what: str) -> VertexOrdering:
+    """Device check of the LexBFS label invariant on the order just produced
+    (pipeline.certify_lexbfs): every pivot has the largest label among the
+    unvisited vertices -- what the reference's debug chain check and audit
+    lemmas assert -- and, under LOWEST_INDEX, every pivot is the smallest id of
+    its label class."""
+    bad, off_rule = pipeline.certify_lexbfs(g, o)
+    if bad >= 0:
+        raise AssertionError(f"{what}: the pivot of step {bad + 1} does not carry the largest label")
+    if exact_lowest and off_rule >= 0:
+        raise AssertionError(f"{what}: step {off_rule + 1} is not the LOWEST_INDEX choice")
+    return o
+
+
 def lexbfs_labels(g, tie_break: TieBreak = LOWEST_INDEX, *, debug: bool = False,
                   method: str = "auto") -> VertexOrdering:
-    """Lexicographic BFS (label-class formulation, search.py:262-310) on the GPU."""
+    """Lexicographic BFS (label-class formulation, search.py:262-310) on the GPU.
+
+    ``debug=True`` (search.py:270-271: labels materialised, the chain checked
+    after every step) replays the finished order on the device with its pivots
+    forced and asserts the same invariant at every step (``_certified``).
+    """
     if method not in ("auto", "array", "linked"):
         raise ValueError(f"unknown method {method!r}")
     if method == "auto":
         method = "array" if g.n >= _ARRAY_MIN_N and not debug else "linked"
-    return _run_lexbfs(g, tie_break, "lexbfs-labels", method)
+    o = _run_lexbfs(g, tie_break, "lexbfs-labels", method)
+    if debug:
+        _certified(g, o, tie_break.seed is None, "lexbfs_labels(debug=True)")
+    return o
 
 
 def lexbfs_partition(g, tie_break: TieBreak = LOWEST_INDEX, *, method: str = "auto",
@@ -111,7 +133,10 @@ def lexbfs_partition(g, tie_break: TieBreak = LOWEST_INDEX, *, method: str = "au
     if method not in ("auto", "array", "linked"):
         raise ValueError(f"unknown method {method!r}")
     if _watch is not None:
-        raise NotImplementedError("_watch observes the CPU PartitionList; the GPU search has none")
+        # a per-step Python callback on the reference's CPU PartitionList object;
+        # the persistent kernel has no such object to hand out between steps
+        raise NotImplementedError("_watch observes the CPU PartitionList; the GPU search has none "
+                                  "(lexbfs_labels(debug=True) checks the label invariant on the device)")
     if method == "auto":
         method = "array" if g.n >= _ARRAY_MIN_N else "linked"
     return _run_lexbfs(g, tie_break, "lexbfs-partition", method)

@@ -50,4 +50,4 @@ def test_status_strings():
     from paper_1508_06329_b200 import _native
 
     assert _native.lib.chordal_strerror(0) == b"ok"
-    assert _native.lib.chordal_abi_version() == 2
+    assert _native.lib.chordal_abi_version() == 3

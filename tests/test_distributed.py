@@ -172,3 +172,39 @@ def test_row_sharded_peo_cuda_backend_two_ranks():
         ok, _, w = oracle.is_chordal(g._packed, g.n)
         exp = (ok, None if w is None else (w[0] + 1, w[1] + 1, w[2] + 1))
         assert results[0][name] == exp and results[1][name] == exp, name
+
+
+@pytest.mark.gpu
+def test_nccl_c_abi_single_rank_matches_oracle():
+    """chordal_is_chordal_{dense,csr}_nccl through a one-rank NCCL communicator
+    (torch.cuda.nccl; this environment has one GPU): the broadcast / shard /
+    MIN all-reduce protocol of the C ABI gives the oracle's verdicts, orders and
+    witnesses."""
+    import numpy as np
+    import torch.cuda.nccl as tnccl
+
+    import oracle
+    from paper_1508_06329_b200.csr import CSRGraph
+    from paper_1508_06329_b200.distributed import sharded_is_chordal_nccl
+    from paper_1508_06329_b200.generate import chordal_random_edges, gen_chordal_random, gen_dense_random, \
+        remove_first_chord
+
+    torch.cuda.set_device(0)
+    comm = tnccl.init_rank(1, tnccl.unique_id(), 0)
+    graphs = {"c1": gen_chordal_random(1000, 8, 0), "c1x": remove_first_chord(gen_chordal_random(1000, 8, 0))[0],
+              "dense": gen_dense_random(2500, 0.5, 4), "chordal3k": gen_chordal_random(3000, 30, 1)}
+    for name, g in graphs.items():
+        ok, order, w = oracle.is_chordal(g._packed, g.n)
+        for gg in (g, CSRGraph.from_dense(g)):
+            v = sharded_is_chordal_nccl(gg, comm)
+            assert v.chordal == ok, name
+            if ok:
+                assert v.peo.order0.tolist() == order.tolist(), name
+            else:
+                assert (v.witness.v - 1, v.witness.p - 1, v.witness.z - 1) == tuple(w), name
+    n = 40000  # the global-state slot engine, parents broadcast from the search
+    u, vv = chordal_random_edges(n, 4, 3)
+    big = CSRGraph.from_edges0(n, u, vv)
+    v = sharded_is_chordal_nccl(big, comm)
+    order = oracle.lexbfs_partition_csr(big.indptr, big.indices, n)
+    assert v.chordal and np.array_equal(v.peo.order0, order)

@@ -177,3 +177,28 @@ def test_oracle_mcs_bfs_goldens():
             assert oracle.other_order(rows, n, "mcs", s).tolist() == z["mcs_seeded"][i, :n].tolist(), i
         assert oracle.other_order(rows, n, "bfs").tolist() == z["bfs"][i, :n].tolist(), i
         assert oracle.other_order(rows, n, "bfs", s).tolist() == z["bfs_seeded"][i, :n].tolist(), i
+
+
+def test_oracle_lexbfs_certificate_on_reference_orders(small_corpus):
+    """The certificate (oracle.lexbfs_certify) accepts every LexBFS order the
+    reference produced -- LOWEST_INDEX exactly, the descending / seeded
+    arbitration and seeded-array orders as LexBFS orders that leave the
+    LOWEST_INDEX choice at their first difference from it -- and rejects
+    non-LexBFS orders (the random permutations) at a step where a smaller label
+    was taken."""
+    c = small_corpus
+    rejected = 0
+    for i in range(0, len(c), 3):
+        n = int(c.ns[i])
+        P = c.packed(i)
+        lex = c.vec("lex", i).tolist()
+        assert oracle.lexbfs_certify(P, n, lex) == (-1, -1), i
+        for key in ("par_desc", "par_seeded", "seeded_array"):
+            o = c.vec(key, i).tolist()
+            first = next((k for k in range(n) if o[k] != lex[k]), -1)
+            assert oracle.lexbfs_certify(P, n, o) == (-1, first), (i, key)
+        bad, off = oracle.lexbfs_certify(P, n, c.vec("perm", i).tolist())
+        if bad >= 0:
+            rejected += 1
+            assert 0 < bad and off <= bad
+    assert rejected > 0

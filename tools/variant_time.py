@@ -42,7 +42,7 @@ def chordal_rows(n, k, seed=0, drop_first_chord=False):
 
 def dense_rows(n, p, seed=0):
     st = device_stride(n)
-    return DeviceRows(n, st, gen_dense_random_device(n, p, [seed], stride=st)[0])
+    return DeviceRows(n, st, gen_dense_random_device(n, p, range(seed, seed + 1), stride=st)[0])
 
 
 def h(t):
