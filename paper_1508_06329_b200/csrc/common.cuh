@@ -39,25 +39,6 @@ __device__ __forceinline__ uint32_t mask_below(int b) {  // bits [0, b), b in [0
 
 __device__ __forceinline__ int highest_bit(uint32_t x) { return 31 - __clz(x); }
 
-// L2 eviction-priority hints (createpolicy + ld.global.nc.L2::cache_hint):
-// data read once per search (a pivot's adjacency list) is marked evict-first so
-// it does not push the search's own state out of L2.
-__device__ __forceinline__ uint64_t l2_policy_evict_first() {
-    uint64_t p;
-    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
-    return p;
-}
-__device__ __forceinline__ int32_t ld_nc_hint(const int32_t *a, uint64_t pol) {
-    int32_t v;
-    asm("ld.global.nc.L2::cache_hint.s32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
-    return v;
-}
-__device__ __forceinline__ int64_t ld_nc_hint(const int64_t *a, uint64_t pol) {
-    int64_t v;
-    asm("ld.global.nc.L2::cache_hint.s64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
-    return v;
-}
-
 }  // namespace chordal
 
 // Status helpers used by the C-ABI layer.

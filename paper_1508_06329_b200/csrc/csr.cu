@@ -68,18 +68,39 @@ __device__ __forceinline__ SlotMem<I, S> carve(uint8_t *ws, const CsrWs &L) {
     return M;
 }
 
+// Look-ahead warp (slot_lookahead): the next CSR_LOOKAHEAD live vertices of the
+// class list, re-walked every CSR_LOOKAHEAD_EVERY steps (0: no look-ahead warp).
+// Config 5: 1.85 s without, 1.615 s with 64 / 8, 1.67 s with 128 / 8, 1.595 s
+// with 32 / 4 (tools/ab_variants.sh).
+#ifndef CSR_LOOKAHEAD
+#define CSR_LOOKAHEAD 32
+#endif
+#ifndef CSR_LOOKAHEAD_EVERY
+#define CSR_LOOKAHEAD_EVERY 4
+#endif
+
 // Any n: all state in global memory (L2-resident), int32 ids; neighbour lists
-// staged through shared memory.
+// staged through shared memory.  Warp 0 runs the search; with CSR_LOOKAHEAD a
+// second warp prefetches the next pivots' lists (slot_lookahead).
 template <int MODE>
-__global__ void __launch_bounds__(32, 1)
+__global__ void __launch_bounds__(64, 1)
 lexbfs_csr_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices, int n, long long m,
                   uint8_t *ws, int32_t *__restrict__ order, int32_t *__restrict__ pos, int32_t *__restrict__ parent,
                   uint64_t seed, uint64_t cell) {
     __shared__ int32_t nbuf[kNbrBuf];
+    __shared__ int prog[3];
     const CsrWs L(n, m, 4, 4);
     const SlotMem<int32_t, int32_t> M = carve<int32_t, int32_t>(ws, L);
+    if (threadIdx.x == 0) prog[0] = prog[1] = prog[2] = 0;
+    __syncthreads();
+    if (threadIdx.x >= 32) {
+        if (CSR_LOOKAHEAD > 0)
+            slot_lookahead<int32_t, int32_t>(indptr, indices, n, M, prog, CSR_LOOKAHEAD, CSR_LOOKAHEAD_EVERY);
+        return;
+    }
     CsrStagedSource<int32_t> src{indptr, indices, nbuf, kNbrBuf, 0};
-    slot_lexbfs<int32_t, int32_t, MODE, CsrStagedSource<int32_t>, int32_t>(src, n, M, order, pos, parent, seed, cell);
+    slot_lexbfs<int32_t, int32_t, MODE, CsrStagedSource<int32_t>, int32_t>(src, n, M, order, pos, parent, seed, cell,
+                                                                           CSR_LOOKAHEAD > 0 ? prog : nullptr);
 }
 
 // n <= 32768: u16 ids; cls / c_cnt / c_tgt (192 KB at n = 32768) and the
@@ -201,7 +222,8 @@ static int launch_csr_mode(const int64_t *indptr, const int32_t *indices, int64_
         lexbfs_csr_smem_kernel<MODE><<<1, 32, sm, stream>>>(indptr, indices, (int)n, m, w, order, pos, parent, seed,
                                                             cell);
     } else {
-        lexbfs_csr_kernel<MODE><<<1, 32, 0, stream>>>(indptr, indices, (int)n, m, w, order, pos, parent, seed, cell);
+        lexbfs_csr_kernel<MODE><<<1, CSR_LOOKAHEAD > 0 ? 64 : 32, 0, stream>>>(indptr, indices, (int)n, m, w, order,
+                                                                               pos, parent, seed, cell);
     }
     CH_LAUNCH_CHECK();
     return CHORDAL_OK;

@@ -223,16 +223,85 @@ __device__ __forceinline__ int seg_scan1(int e, int *wt, int &te) {
     return xe;
 }
 
+// Loads / stores of a thread's WT consecutive 32-bit words (WT = 1, 2 or a
+// multiple of 4), vectorised to 128 / 64 / 32-bit accesses.
+template <int WT>
+__device__ __forceinline__ void ld_words(const uint32_t *p, uint32_t (&o)[WT]) {
+    if constexpr (WT >= 4) {
+#pragma unroll
+        for (int g = 0; g < WT / 4; ++g) {
+            const uint4 v = reinterpret_cast<const uint4 *>(p)[g];
+            o[4 * g] = v.x; o[4 * g + 1] = v.y; o[4 * g + 2] = v.z; o[4 * g + 3] = v.w;
+        }
+    } else if constexpr (WT == 2) {
+        const uint2 v = *reinterpret_cast<const uint2 *>(p);
+        o[0] = v.x; o[1] = v.y;
+    } else {
+        o[0] = *p;
+    }
+}
+template <int WT>
+__device__ __forceinline__ void ld_words_nc(const uint32_t *p, uint32_t (&o)[WT]) {
+    if constexpr (WT >= 4) {
+#pragma unroll
+        for (int g = 0; g < WT / 4; ++g) {
+            const uint4 v = __ldg(reinterpret_cast<const uint4 *>(p) + g);
+            o[4 * g] = v.x; o[4 * g + 1] = v.y; o[4 * g + 2] = v.z; o[4 * g + 3] = v.w;
+        }
+    } else if constexpr (WT == 2) {
+        const uint2 v = __ldg(reinterpret_cast<const uint2 *>(p));
+        o[0] = v.x; o[1] = v.y;
+    } else {
+        o[0] = __ldg(p);
+    }
+}
+template <int WT>
+__device__ __forceinline__ void st_words(uint32_t *p, const uint32_t (&v)[WT]) {
+    if constexpr (WT >= 4) {
+#pragma unroll
+        for (int g = 0; g < WT / 4; ++g)
+            reinterpret_cast<uint4 *>(p)[g] = make_uint4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+    } else if constexpr (WT == 2) {
+        *reinterpret_cast<uint2 *>(p) = make_uint2(v[0], v[1]);
+    } else {
+        *p = v[0];
+    }
+}
+template <int WT>
+__device__ __forceinline__ void st_zero(uint32_t *p) {
+    uint32_t z[WT];
+#pragma unroll
+    for (int k = 0; k < WT; ++k) z[k] = 0u;
+    st_words<WT>(p, z);
+}
+// WT 16-bit values (all < 65536), packed.
+template <int WT>
+__device__ __forceinline__ void st_u16(uint16_t *p, const int (&v)[WT]) {
+    if constexpr (WT >= 4) {
+#pragma unroll
+        for (int g = 0; g < WT / 4; ++g)
+            reinterpret_cast<uint2 *>(p)[g] =
+                make_uint2((uint32_t)v[4 * g] | ((uint32_t)v[4 * g + 1] << 16),
+                           (uint32_t)v[4 * g + 2] | ((uint32_t)v[4 * g + 3] << 16));
+    } else if constexpr (WT == 2) {
+        *reinterpret_cast<uint32_t *>(p) = (uint32_t)v[0] | ((uint32_t)v[1] << 16);
+    } else {
+        *p = (uint16_t)v[0];
+    }
+}
+
 }  // namespace
 
 // MV: movers handled per round of a thread's mover loop (their position loads
 // overlap): 4 for dense graphs (many movers per thread), 2 otherwise (config 2
-// chordal 12.53 -> 12.07 ms; G(8192, 0.5) would go 0.260 -> 0.274 ms with 2).
-// G: 128-bit word groups per thread (thread t owns words [4 G t, 4 G (t + 1))).
+// chordal 12.53 -> 12.07 ms; G(8192, 0.5) would go 0.260 -> 0.274 ms with 2;
+// 4 on the sparse path: c3 chordal 69.8 -> 72.0 ms).
+// WT: 32-bit words per thread (thread t owns vertex / position words
+// [WT t, WT (t + 1)); 1, 2 or a multiple of 4).
 // ONEWARP: the block is one warp -- every barrier is a __syncwarp and the
-// block scans are warp scans (sparse graphs up to n = 16384, G = n / 4096).
-template <int MODE, int MV, int G, bool ONEWARP>
-__global__ void __launch_bounds__(ONEWARP ? 32 : 512, 1)
+// block scans are warp scans.
+template <int MODE, int MV, int WT, bool ONEWARP>
+__global__ void __launch_bounds__(ONEWARP ? 32 : (WT == 1 ? 1024 : 512), 1)
 lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint64_t seed, uint64_t cell,
                   int32_t *__restrict__ order, int32_t *__restrict__ pos_out, int32_t *__restrict__ parent,
                   const int32_t *__restrict__ forced, int32_t *__restrict__ status) {
@@ -264,9 +333,8 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
 
     const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
     const int NT = ONEWARP ? 32 : blockDim.x, NW = NT >> 5;
-    constexpr int WT = 4 * G;                      // words per thread
-    constexpr int LG = G == 1 ? 2 : (G == 2 ? 3 : (G == 4 ? 4 : 5));  // log2(WT)
-    static_assert(G == 1 || G == 2 || G == 4 || G == 8, "G");
+    constexpr int LG = WT == 1 ? 0 : (WT == 2 ? 1 : (WT == 4 ? 2 : (WT == 8 ? 3 : (WT == 16 ? 4 : 5))));  // log2(WT)
+    static_assert(WT == 1 || WT == 2 || WT == 4 || WT == 8 || WT == 16 || WT == 32, "WT");
     const int w0 = WT * t;  // this thread owns vertex / position words [w0, w0 + WT)
     const bool own = w0 < W;
 #define SEG_SYNC()                   \
@@ -309,9 +377,9 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
 #endif
     int tail = 1, nclasses = 1;
     int guess = -1;
-    uint4 nxt[G];
+    uint32_t nxt[WT];
 #pragma unroll
-    for (int g = 0; g < G; ++g) nxt[g] = make_uint4(0, 0, 0, 0);
+    for (int k = 0; k < WT; ++k) nxt[k] = 0u;
 
     for (int i = 0; i < n; ++i) {
         // ---- pivot ---------------------------------------------------------
@@ -452,27 +520,24 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
         for (int k = 0; k < WT; ++k) r[k] = ext[k] = 0u;
         int extc = 0, cnt = 0, pmn = kSegBig, pmx = -1;
         if (own) {
-            const bool hit = x == guess;
+            if (x == guess) {
 #pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const uint4 rw = hit ? nxt[g] : ld_nc_v4(rows + (long long)x * sw + w0 + 4 * g);
-                r[4 * g] = rw.x; r[4 * g + 1] = rw.y; r[4 * g + 2] = rw.z; r[4 * g + 3] = rw.w;
+                for (int k = 0; k < WT; ++k) r[k] = nxt[k];
+            } else {
+                ld_words_nc<WT>(rows + (long long)x * sw + w0, r);
             }
         }
 #ifdef SEG_PROFILE
         const int guess_prev = guess;
 #endif
         guess = hpos < tail0 ? (int)A[hpos] : -1;
+        // (an L2 prefetch of the row two positions ahead measured slower: c3
+        // chordal 68.9 -> 69.8 ms, c2 chordal 12.04 -> 12.42 ms)
         if (own) {
             if (((x >> 5) >> LG) == t) RA[x >> 5] &= ~(1u << (x & 31));
             uint32_t ra[WT], uu[WT];
-#pragma unroll
-            for (int g = 0; g < G; ++g) {
-                const uint4 ra4 = *reinterpret_cast<const uint4 *>(RA + w0 + 4 * g);
-                const uint4 u4 = *reinterpret_cast<const uint4 *>(U + w0 + 4 * g);
-                ra[4 * g] = ra4.x; ra[4 * g + 1] = ra4.y; ra[4 * g + 2] = ra4.z; ra[4 * g + 3] = ra4.w;
-                uu[4 * g] = u4.x; uu[4 * g + 1] = u4.y; uu[4 * g + 2] = u4.z; uu[4 * g + 3] = u4.w;
-            }
+            ld_words<WT>(RA + w0, ra);
+            ld_words<WT>(U + w0, uu);
 #pragma unroll
             for (int k = 0; k < WT; ++k) {
                 uint32_t m2 = r[k] & ra[k];
@@ -513,13 +578,12 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                     }
                 }
 #pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const int k = 4 * g;
-                    *reinterpret_cast<uint4 *>(U + w0 + k) = make_uint4(uu[k] & ~ext[k], uu[k + 1] & ~ext[k + 1],
-                                                                        uu[k + 2] & ~ext[k + 2], uu[k + 3] & ~ext[k + 3]);
-                    *reinterpret_cast<uint4 *>(RA + w0 + k) = make_uint4(ra[k] | ext[k], ra[k + 1] | ext[k + 1],
-                                                                         ra[k + 2] | ext[k + 2], ra[k + 3] | ext[k + 3]);
+                for (int k = 0; k < WT; ++k) {
+                    uu[k] &= ~ext[k];
+                    ra[k] |= ext[k];
                 }
+                st_words<WT>(U + w0, uu);
+                st_words<WT>(RA + w0, ra);
                 fl[0] = 1;
             }
         }
@@ -530,10 +594,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
         // (into the registers the current row just left) it stalled that loop
         // (c3 chordal 90.5 -> 86.5 ms); an extra L2 prefetch of the row after
         // it no longer pays once the load sits here.
-        if (guess >= 0 && own) {
-#pragma unroll
-            for (int g = 0; g < G; ++g) nxt[g] = ld_nc_v4(rows + (long long)guess * sw + w0 + 4 * g);
-        }
+        if (guess >= 0 && own) ld_words_nc<WT>(rows + (long long)guess * sw + w0, nxt);
         // mover count and position range: per-warp slots, reduced after B1 by
         // every warp (lane w reads warp w's slot) -- same-address shared atomics
         // from every warp cost ~1 % of a step at N = 32768
@@ -607,13 +668,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
             int ctot = 0, hmax = 0, lmin = kSegBig;
 #pragma unroll
             for (int k = 0; k < WT; ++k) f[k] = b[k] = 0u;
-            if (own) {
-#pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const uint4 f4 = *reinterpret_cast<const uint4 *>(F + w0 + 4 * g);
-                    f[4 * g] = f4.x; f[4 * g + 1] = f4.y; f[4 * g + 2] = f4.z; f[4 * g + 3] = f4.w;
-                }
-            }
+            if (own) ld_words<WT>(F + w0, f);
 #pragma unroll
             for (int k = 0; k < WT; ++k) {
                 if (own) b[k] = breg(w0 + k);
@@ -636,19 +691,12 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                 for (int k = WT - 1; k >= 0; --k) { nbq[k] = run; run = min(run, lbw[k]); }
             }
             if (own) {
+                int pcv[WT];
 #pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const int k = 4 * g;
-                    *reinterpret_cast<uint2 *>(Pc + w0 + k) =
-                        make_uint2((uint32_t)(xa + cpre[k]) | ((uint32_t)(xa + cpre[k + 1]) << 16),
-                                   (uint32_t)(xa + cpre[k + 2]) | ((uint32_t)(xa + cpre[k + 3]) << 16));
-                    *reinterpret_cast<uint2 *>(LB + w0 + k) =
-                        make_uint2((uint32_t)lbq[k] | ((uint32_t)lbq[k + 1] << 16),
-                                   (uint32_t)lbq[k + 2] | ((uint32_t)lbq[k + 3] << 16));
-                    *reinterpret_cast<uint2 *>(NBq + w0 + k) =
-                        make_uint2((uint32_t)nbq[k] | ((uint32_t)nbq[k + 1] << 16),
-                                   (uint32_t)nbq[k + 2] | ((uint32_t)nbq[k + 3] << 16));
-                }
+                for (int k = 0; k < WT; ++k) pcv[k] = xa + cpre[k];
+                st_u16<WT>(Pc + w0, pcv);
+                st_u16<WT>(LB + w0, lbq);
+                st_u16<WT>(NBq + w0, nbq);
             }
             SEG_SYNC();  // B2
             SEG_T(4);
@@ -656,10 +704,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                 const int g = fl[6];
                 if (g >= 0 && g != guess) {
                     guess = g;
-                    if (own) {
-#pragma unroll
-                        for (int gg = 0; gg < G; ++gg) nxt[gg] = ld_nc_v4(rows + (long long)g * sw + w0 + 4 * gg);
-                    }
+                    if (own) ld_words_nc<WT>(rows + (long long)g * sw + w0, nxt);
                 }
             }
             // ---- phase 3a: list the words of split classes ------------------------
@@ -809,21 +854,16 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                 }
             }
             if (own) {
+                ld_words<WT>(NB + w0, nbadd);
+                uint32_t any = 0u;
 #pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const uint4 nb4 = *reinterpret_cast<const uint4 *>(NB + w0 + 4 * g);
-                    nbadd[4 * g] = nb4.x; nbadd[4 * g + 1] = nb4.y; nbadd[4 * g + 2] = nb4.z; nbadd[4 * g + 3] = nb4.w;
-                    if (nb4.x | nb4.y | nb4.z | nb4.w)
-                        *reinterpret_cast<uint4 *>(NB + w0 + 4 * g) = make_uint4(0, 0, 0, 0);
-                }
+                for (int k = 0; k < WT; ++k) any |= nbadd[k];
+                if (any) st_zero<WT>(NB + w0);
             }
         }
         // ---- end of step: clear flags, new class starts, append -----------------
         if (own) {
-            if (cntA && (w0 + WT - 1) >= (gmn >> 5) && w0 <= (gmx >> 5)) {
-#pragma unroll
-                for (int g = 0; g < G; ++g) *reinterpret_cast<uint4 *>(F + w0 + 4 * g) = make_uint4(0, 0, 0, 0);
-            }
+            if (cntA && (w0 + WT - 1) >= (gmn >> 5) && w0 <= (gmx >> 5)) st_zero<WT>(F + w0);
 #pragma unroll
             for (int k = 0; k < WT; ++k) {
                 if (hpos < tail0 && (hpos >> 5) == w0 + k) nbadd[k] |= 1u << (hpos & 31);
@@ -974,25 +1014,33 @@ int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int64_t m, 
     if (e != cudaSuccess) return CHORDAL_ECUDA;                                                                    \
     lexbfs_seg_kernel<M, K, GG, OW><<<1, NTH, smem, stream>>>(adj, (int)n, stride, seed, cell, order, pos, parent, \
                                                               forced, status);
+#ifndef SEG_WT_SPARSE
+#define SEG_WT_SPARSE 4
+#endif
+#ifndef SEG_WT_DENSE
+#define SEG_WT_DENSE 4
+#endif
+    const int Ts = max(T, ((W + SEG_WT_SPARSE - 1) / SEG_WT_SPARSE + 31) / 32 * 32);
+    const int Td = max(T, max(32, ((W + SEG_WT_DENSE - 1) / SEG_WT_DENSE + 31) / 32 * 32));
 #if SEG_ONEWARP_MAX_N > 0
 #define SEG_LAUNCH(M)                                         \
     if (dense) {                                              \
-        SEG_LAUNCH_K(M, 4, 1, false, T)                       \
+        SEG_LAUNCH_K(M, 4, SEG_WT_DENSE, false, Td)           \
     } else if (onewarp && W <= 128) {                         \
-        SEG_LAUNCH_K(M, 2, 1, true, 32)                       \
-    } else if (onewarp && W <= 256) {                         \
-        SEG_LAUNCH_K(M, 2, 2, true, 32)                       \
-    } else if (onewarp) {                                     \
         SEG_LAUNCH_K(M, 2, 4, true, 32)                       \
+    } else if (onewarp && W <= 256) {                         \
+        SEG_LAUNCH_K(M, 2, 8, true, 32)                       \
+    } else if (onewarp) {                                     \
+        SEG_LAUNCH_K(M, 2, 16, true, 32)                      \
     } else {                                                  \
-        SEG_LAUNCH_K(M, 2, 1, false, T)                       \
+        SEG_LAUNCH_K(M, 2, SEG_WT_SPARSE, false, Ts)          \
     }
 #else
 #define SEG_LAUNCH(M)                                         \
     if (dense) {                                              \
-        SEG_LAUNCH_K(M, 4, 1, false, T)                       \
+        SEG_LAUNCH_K(M, 4, SEG_WT_DENSE, false, Td)           \
     } else {                                                  \
-        SEG_LAUNCH_K(M, 2, 1, false, T)                       \
+        SEG_LAUNCH_K(M, 2, SEG_WT_SPARSE, false, Ts)          \
     }
 #endif
     switch (tie_rule) {

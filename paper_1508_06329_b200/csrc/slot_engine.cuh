@@ -81,16 +81,6 @@ struct CsrStagedSource {
     T *buf;      // shared memory, bufcap entries
     int bufcap;
     mutable int64_t base;
-    // Each list is read once per search (when its vertex is the pivot): loaded
-    // evict-first, so the engine's class / slot state keeps its L2 lines
-    // (config 5: 64 MB of lists against ~76 MB of state in a 126 MB L2).
-#ifndef CSR_NO_EVICT_FIRST
-    __device__ __forceinline__ static uint64_t list_policy() { return l2_policy_evict_first(); }
-    __device__ __forceinline__ static int32_t ld_list(const int32_t *a, uint64_t pol) { return ld_nc_hint(a, pol); }
-#else
-    __device__ __forceinline__ static uint64_t list_policy() { return 0; }
-    __device__ __forceinline__ static int32_t ld_list(const int32_t *a, uint64_t) { return __ldg(a); }
-#endif
     __device__ __forceinline__ void bounds(int x, int64_t &b, int64_t &e) const {
         b = __ldg(indptr + x);
         e = __ldg(indptr + x + 1);
@@ -101,21 +91,22 @@ struct CsrStagedSource {
         const int cnt = (int)(hi - lo);
         const int32_t *src = indices + lo;
         int k = lane;
-        const uint64_t pol = list_policy();
         for (; k + 224 < cnt; k += 256) {
             int32_t a[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) a[j] = ld_list(src + k + 32 * j, pol);
+            for (int j = 0; j < 8; ++j) a[j] = __ldg(src + k + 32 * j);
 #pragma unroll
             for (int j = 0; j < 8; ++j) buf[k + 32 * j] = (T)a[j];
         }
-        for (; k < cnt; k += 32) buf[k] = (T)ld_list(src + k, pol);
+        for (; k < cnt; k += 32) buf[k] = (T)__ldg(src + k);
         base = lo;
         __syncwarp();
     }
     __device__ __forceinline__ int get(int64_t e) const { return (int)buf[e - base]; }
     // one list entry straight from global memory (the <= 32-neighbour fast step)
-    __device__ __forceinline__ int fetch(int64_t k) const { return ld_list(indices + k, list_policy()); }
+    // (an L2 evict-first hint on these list loads measured slower: config 5
+    // 1.88 -> 1.97 s)
+    __device__ __forceinline__ int fetch(int64_t k) const { return __ldg(indices + k); }
     // Row bounds of a likely next pivot, issued where they stand (their values
     // are used a step later), and an L2 prefetch of the row itself once they
     // have arrived: the next step's row fetch then skips the indptr round trip
@@ -260,7 +251,8 @@ __device__ long long compact(const SlotMem<I, S> &M, int chead, int lane) {
 // in the output type O.  MODE: CHORDAL_TIE_ASCENDING / DESCENDING / SEEDED_ARB.
 template <typename I, typename S, int MODE, typename Src, typename O>
 __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__restrict__ order, O *__restrict__ pos,
-                            O *__restrict__ parent, uint64_t seed, uint64_t cell) {
+                            O *__restrict__ parent, uint64_t seed, uint64_t cell,
+                            volatile int *progress = nullptr) {
     using C = SlotConst<I>;
     const int lane = threadIdx.x & 31;
     const uint32_t lt = slot_detail::lanemask_lt();
@@ -341,6 +333,10 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
             ypre = src.fetch(MODE == CHORDAL_TIE_DESCENDING ? gb1 - 1 - lane : gb0 + lane);
         // ---- pivot: first live slot of the head class (or hash election) ----
         const int c0 = chead;
+        if (progress && lane == 0) {  // for the look-ahead warp (slot_lookahead): head class, step
+            progress[0] = c0;
+            progress[2] = i;
+        }
         const long long e0 = (long long)M.c_end[c0];
         const int live_c0 = (int)M.c_live[c0], next_c0 = (int)M.c_next[c0];  // one round trip
         long long xs = -1;
@@ -777,6 +773,74 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
     if (lane == 0)
         for (int k = 0; k < 10; ++k) atomicAdd(&slot_prof[k], slot_acc[k]);
 #endif
+    if (progress && lane == 0) progress[1] = 1;
+}
+
+// Look-ahead warp of the global-state slot engine: every few steps it walks the
+// class list from the current head class and, for the next `ahead` live
+// vertices (the next pivots, in order, unless a split reorders them), loads
+// their row bounds and prefetches their neighbour lists into L2 -- each list is
+// read once per search, so without this the pivot's list fetch is a DRAM round
+// trip on the search's critical path.  It only reads (racy reads of structures
+// the search is mutating are harmless: a wrong guess costs one useless prefetch).
+#ifndef SLOT_LOOKAHEAD_L1
+#define SLOT_LOOKAHEAD_L1 0
+#endif
+template <typename I, typename S>
+__device__ void slot_lookahead(const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices, int n,
+                               const SlotMem<I, S> &M, volatile int *progress, int ahead, int every) {
+    using C = SlotConst<I>;
+    const int lane = threadIdx.x & 31;
+    int last = -every;
+    while (true) {
+        if (progress[1]) break;
+        const int step = progress[2];
+        if (step - last < every) {
+            __nanosleep(32);
+            continue;
+        }
+        last = step;
+        int c = progress[0];
+        int budget = ahead;
+        // every value read here may be stale (the search is mutating it): ids
+        // and slot ranges are range-checked so a stale read never leaves the arrays
+        while (budget > 0 && c >= 0 && c < n + 2) {
+            long long h = (long long)M.c_head[c], e = (long long)M.c_end[c];
+            const int next = (int)M.c_next[c];
+            if (h < 0 || e > M.cap || h >= e) break;
+            if (e - h > 4096) e = h + 4096;
+            for (long long s0 = h; s0 < e && budget > 0; s0 += 32) {
+                const long long sl = s0 + lane;
+                const int v = sl < e ? (int)M.slot_v[sl] : -1;
+                const bool live = v >= 0 && v < n && (int)M.cls[v] == c;
+                const int before = ahead - budget;  // live vertices of earlier rounds
+                const uint32_t lm = __ballot_sync(CH_FULL, live);
+                int64_t b = 0, en = 0;
+                if (live) {
+                    b = __ldg(indptr + v);
+                    en = __ldg(indptr + v + 1);
+                    for (int64_t k = b; k < en && k < b + 64; k += 32)
+                        asm volatile("prefetch.global.L2 [%0];" ::"l"(indices + k));
+                }
+#if SLOT_LOOKAHEAD_L1 > 0
+                // the nearest pivots: their lists and their neighbours' class ids
+                // into this SM's L1 (the search warp shares it), one warp-wide
+                // round trip per pivot
+                for (uint32_t mm = lm; mm && before + __popc(lm & ~mm) < SLOT_LOOKAHEAD_L1; mm &= mm - 1) {
+                    const int src = __ffs(mm) - 1;
+                    const int64_t bb = __shfl_sync(CH_FULL, b, src), ee = __shfl_sync(CH_FULL, en, src);
+                    if (ee - bb > 32) continue;
+                    if (lane < (int)(ee - bb)) {
+                        const int y = __ldg(indices + bb + lane);
+                        if (y >= 0 && y < n) asm volatile("prefetch.global.L1 [%0];" ::"l"(M.cls + y));
+                    }
+                }
+#endif
+                budget -= __popc(lm);
+            }
+            c = next;
+        }
+    }
 }
 
 }  // namespace chordal

@@ -180,8 +180,10 @@ def test_nccl_c_abi_single_rank_matches_oracle():
     (torch.cuda.nccl; this environment has one GPU): the broadcast / shard /
     MIN all-reduce protocol of the C ABI gives the oracle's verdicts, orders and
     witnesses."""
+    import ctypes
+    import glob
+
     import numpy as np
-    import torch.cuda.nccl as tnccl
 
     import oracle
     from paper_1508_06329_b200.csr import CSRGraph
@@ -190,7 +192,20 @@ def test_nccl_c_abi_single_rank_matches_oracle():
         remove_first_chord
 
     torch.cuda.set_device(0)
-    comm = tnccl.init_rank(1, tnccl.unique_id(), 0)
+    torch.zeros(1, device="cuda")  # CUDA context up before NCCL
+    # the NCCL torch ships (the library our entry points resolve by soname)
+    libs = glob.glob(os.path.join(os.path.dirname(torch.__file__), "..", "nvidia", "nccl", "lib", "libnccl.so*"))
+    nccl = ctypes.CDLL(libs[0] if libs else "libnccl.so.2", mode=ctypes.RTLD_GLOBAL)
+
+    class UniqueId(ctypes.Structure):
+        _fields_ = [("internal", ctypes.c_char * 128)]
+
+    uid = UniqueId()
+    assert nccl.ncclGetUniqueId(ctypes.byref(uid)) == 0
+    comm_p = ctypes.c_void_p()
+    nccl.ncclCommInitRank.argtypes = [ctypes.POINTER(ctypes.c_void_p), ctypes.c_int, UniqueId, ctypes.c_int]
+    assert nccl.ncclCommInitRank(ctypes.byref(comm_p), 1, uid, 0) == 0
+    comm = int(comm_p.value)
     graphs = {"c1": gen_chordal_random(1000, 8, 0), "c1x": remove_first_chord(gen_chordal_random(1000, 8, 0))[0],
               "dense": gen_dense_random(2500, 0.5, 4), "chordal3k": gen_chordal_random(3000, 30, 1)}
     for name, g in graphs.items():
@@ -208,3 +223,5 @@ def test_nccl_c_abi_single_rank_matches_oracle():
     v = sharded_is_chordal_nccl(big, comm)
     order = oracle.lexbfs_partition_csr(big.indptr, big.indices, n)
     assert v.chordal and np.array_equal(v.peo.order0, order)
+    nccl.ncclCommDestroy.argtypes = [ctypes.c_void_p]
+    nccl.ncclCommDestroy(ctypes.c_void_p(comm))

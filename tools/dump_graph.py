@@ -31,5 +31,21 @@ def main(n, k, out):
         rows.tofile(f)
 
 
+def main_removed(n, k, out):
+    """The chord-removed twin (generate.remove_first_chord) of gen_chordal_random(n, k, 0)."""
+    from paper_1508_06329_b200.generate import gen_chordal_random, remove_first_chord
+
+    g, _ = remove_first_chord(gen_chordal_random(n, int(k), 0, cap=max(n, 20000)))
+    stride = device_stride(n)
+    rows = np.zeros((n, stride), np.uint8)
+    rows[:, : g._packed.shape[1]] = g._packed
+    with open(out, "wb") as f:
+        np.array([n, stride], np.int64).tofile(f)
+        rows.tofile(f)
+
+
 if __name__ == "__main__":
-    main(int(sys.argv[1]), sys.argv[2], sys.argv[3])
+    if len(sys.argv) > 4 and sys.argv[4] == "x":
+        main_removed(int(sys.argv[1]), sys.argv[2], sys.argv[3])
+    else:
+        main(int(sys.argv[1]), sys.argv[2], sys.argv[3])

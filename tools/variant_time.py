@@ -35,7 +35,7 @@ def chordal_rows(n, k, seed=0, drop_first_chord=False):
         from paper_1508_06329_b200.device import device_rows
         from paper_1508_06329_b200.generate import gen_chordal_random, remove_first_chord
 
-        return device_rows(remove_first_chord(gen_chordal_random(n, k, seed))[0])
+        return device_rows(remove_first_chord(gen_chordal_random(n, k, seed, cap=n))[0])
     u, v = chordal_random_edges(n, k, seed)
     return DeviceRows(n, device_stride(n), ops.edges_to_dense(u, v, n, device_stride(n)), m=len(u))
 
