@@ -300,8 +300,9 @@ __device__ __forceinline__ void st_u16(uint16_t *p, const int (&v)[WT]) {
 // [WT t, WT (t + 1)); 1, 2 or a multiple of 4).
 // ONEWARP: the block is one warp -- every barrier is a __syncwarp and the
 // block scans are warp scans.
-template <int MODE, int MV, int WT, bool ONEWARP>
-__global__ void __launch_bounds__(ONEWARP ? 32 : (WT == 1 ? 1024 : 512), 1)
+// MAXT: the largest block the instance is launched with (register budget).
+template <int MODE, int MV, int WT, bool ONEWARP, int MAXT>
+__global__ void __launch_bounds__(ONEWARP ? 32 : MAXT, 1)
 lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint64_t seed, uint64_t cell,
                   int32_t *__restrict__ order, int32_t *__restrict__ pos_out, int32_t *__restrict__ parent,
                   const int32_t *__restrict__ forced, int32_t *__restrict__ status) {
@@ -970,6 +971,8 @@ int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int64_t m, 
     if (n <= 0) return CHORDAL_OK;
     if (n > CHORDAL_DENSE_LEXBFS_MAX_N) return CHORDAL_ETOOLARGE;
     if (tie_rule == kTieCertify && (!forced || !status)) return CHORDAL_EINVAL;
+    // (the CTA engine below with one word per thread takes 0.99-1.16 ms for
+    // config 1's LexBFS on 32-512 threads; the one-warp engine 0.51 ms)
     if (n <= 1024 && tie_rule != CHORDAL_TIE_SEEDED_ARB && tie_rule != kTieCertify) {
         const size_t state = (size_t((n + 31) >> 5) * 32 * 2 * 4 + 256 + 15) & ~size_t(15);
         const size_t rows = (size_t)n * stride;
@@ -990,59 +993,61 @@ int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int64_t m, 
         return CHORDAL_OK;
     }
     const int W = (int)((n + 31) >> 5);
-    // One thread per four row words; dense graphs (m known, 2m >= n^2 / 8:
-    // G(n, 0.5) splits classes of thousands of vertices in each of its few
-    // steps) run their partition phases (3b / 3c, one warp per four split-class
-    // words) on 512 threads: G(32768, 0.5) 0.68 -> 0.60 ms, while the sparser
-    // configuration-3 chordal graph (average degree 1005) is faster on 256
-    // (69.8 vs 71.6 ms, tools/seg_time.cu).  Sparse graphs (m known, below that
-    // density) with n <= kOneWarpMaxN run on one warp with 4 G words per lane:
-    // no block barriers, warp scans only.
-    int T = max(32, ((W + 3) / 4 + 31) / 32 * 32);
+    // Words per thread (WT) and threads (T).  Every phase of a step has a
+    // per-thread loop over the thread's words and ends at a block barrier, so
+    // the step's latency follows the per-thread work: fewer words per thread
+    // until the block barrier / register budget bites (config 3 chordal, sparse:
+    // WT = 4 on 256 threads 68.2 ms, WT = 2 on 512 63.0 ms, WT = 1 on 1024 99 ms
+    // (64 registers, spills); config 2 chordal: WT 4 / 2 / 1 11.9 / 9.07 / 8.20
+    // ms; G(8192, 0.5): 0.452 / 0.250 / 0.176 ms; G(32768, 0.5): WT 4 / 2 / 1
+    // 0.68 / 0.556 / 0.616 ms; WT = 8 / 16 (fewer warps) 103 / 180 ms on
+    // config 3 chordal).  Dense graphs (m known, 2m >= n^2 / 8: G(n, 0.5) splits
+    // classes of thousands of vertices in each of its few steps) keep at least
+    // 512 threads for their partition phases (3b / 3c, one warp per four
+    // split-class words); extra threads for sparse graphs do not pay (config 2
+    // chordal on 512 threads: 8.20 -> 9.20 ms).
     const bool dense = m >= 0 && n > 1024 && 2 * m * kSegDenseFrac >= n * n;
     const bool onewarp = m > 0 && !dense && n <= kOneWarpMaxN;
-    if (dense) T = max(T, 512);
+    int T1 = max(32, (W + 31) / 32 * 32), T2 = max(32, ((W + 1) / 2 + 31) / 32 * 32);
+    if (dense) {
+        T1 = max(T1, 512);
+        T2 = max(T2, 512);
+    }
 #ifdef SEG_THREADS_ENV
-    if (const char *ev = getenv("SEG_THREADS")) T = max(max(32, ((W + 3) / 4 + 31) / 32 * 32), atoi(ev));
-    if (const char *ev = getenv("SEG_THREADS_DENSE")) if (dense) T = atoi(ev);
+    if (const char *ev = getenv("SEG_THREADS")) T2 = max(T2, atoi(ev));
 #endif
+    const bool wt1 = W <= (dense ? 512 : 256);  // one word per thread within a 512-thread register budget
     const size_t smem = seg_smem_bytes(n);
     cudaError_t e;
-#define SEG_LAUNCH_K(M, K, GG, OW, NTH)                                                                           \
-    e = cudaFuncSetAttribute(lexbfs_seg_kernel<M, K, GG, OW>, cudaFuncAttributeMaxDynamicSharedMemorySize,         \
-                             (int)smem);                                                                           \
-    if (e != cudaSuccess) return CHORDAL_ECUDA;                                                                    \
-    lexbfs_seg_kernel<M, K, GG, OW><<<1, NTH, smem, stream>>>(adj, (int)n, stride, seed, cell, order, pos, parent, \
-                                                              forced, status);
-#ifndef SEG_WT_SPARSE
-#define SEG_WT_SPARSE 4
-#endif
-#ifndef SEG_WT_DENSE
-#define SEG_WT_DENSE 4
-#endif
-    const int Ts = max(T, ((W + SEG_WT_SPARSE - 1) / SEG_WT_SPARSE + 31) / 32 * 32);
-    const int Td = max(T, max(32, ((W + SEG_WT_DENSE - 1) / SEG_WT_DENSE + 31) / 32 * 32));
+#define SEG_LAUNCH_K(M, K, WTN, OW, NTH, MT)                                                                     \
+    e = cudaFuncSetAttribute(lexbfs_seg_kernel<M, K, WTN, OW, MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,   \
+                             (int)smem);                                                                         \
+    if (e != cudaSuccess) return CHORDAL_ECUDA;                                                                  \
+    lexbfs_seg_kernel<M, K, WTN, OW, MT><<<1, NTH, smem, stream>>>(adj, (int)n, stride, seed, cell, order, pos,  \
+                                                                   parent, forced, status);
 #if SEG_ONEWARP_MAX_N > 0
-#define SEG_LAUNCH(M)                                         \
-    if (dense) {                                              \
-        SEG_LAUNCH_K(M, 4, SEG_WT_DENSE, false, Td)           \
-    } else if (onewarp && W <= 128) {                         \
-        SEG_LAUNCH_K(M, 2, 4, true, 32)                       \
-    } else if (onewarp && W <= 256) {                         \
-        SEG_LAUNCH_K(M, 2, 8, true, 32)                       \
-    } else if (onewarp) {                                     \
-        SEG_LAUNCH_K(M, 2, 16, true, 32)                      \
-    } else {                                                  \
-        SEG_LAUNCH_K(M, 2, SEG_WT_SPARSE, false, Ts)          \
-    }
+#define SEG_LAUNCH_OW(M)                               \
+    if (onewarp && W <= 128) {                         \
+        SEG_LAUNCH_K(M, 2, 4, true, 32, 32)            \
+    } else if (onewarp && W <= 256) {                  \
+        SEG_LAUNCH_K(M, 2, 8, true, 32, 32)            \
+    } else if (onewarp) {                              \
+        SEG_LAUNCH_K(M, 2, 16, true, 32, 32)           \
+    } else
 #else
-#define SEG_LAUNCH(M)                                         \
-    if (dense) {                                              \
-        SEG_LAUNCH_K(M, 4, SEG_WT_DENSE, false, Td)           \
-    } else {                                                  \
-        SEG_LAUNCH_K(M, 2, SEG_WT_SPARSE, false, Ts)          \
-    }
+#define SEG_LAUNCH_OW(M)
 #endif
+#define SEG_LAUNCH(M)                                   \
+    SEG_LAUNCH_OW(M)                                    \
+    if (dense && wt1) {                                 \
+        SEG_LAUNCH_K(M, 4, 1, false, T1, 512)           \
+    } else if (dense) {                                 \
+        SEG_LAUNCH_K(M, 4, 2, false, T2, 512)           \
+    } else if (wt1) {                                   \
+        SEG_LAUNCH_K(M, 2, 1, false, T1, 512)           \
+    } else {                                            \
+        SEG_LAUNCH_K(M, 2, 2, false, T2, 512)           \
+    }
     switch (tie_rule) {
         case CHORDAL_TIE_ASCENDING: SEG_LAUNCH(CHORDAL_TIE_ASCENDING); break;
         case CHORDAL_TIE_DESCENDING: SEG_LAUNCH(CHORDAL_TIE_DESCENDING); break;
@@ -1051,6 +1056,7 @@ int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int64_t m, 
         default: return CHORDAL_EINVAL;
     }
 #undef SEG_LAUNCH
+#undef SEG_LAUNCH_OW
 #undef SEG_LAUNCH_K
     CH_LAUNCH_CHECK();
     return CHORDAL_OK;
