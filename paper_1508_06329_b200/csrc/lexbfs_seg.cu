@@ -69,6 +69,19 @@ constexpr int kSegBig = 0x7FFFFFFF;
 // search.py:270-271 / 313-322, parallel/lexbfs.py:82-129) and the first step
 // whose pivot differs from the LOWEST_INDEX choice.
 constexpr int kTieCertify = 5;
+#ifndef SEG_SPARSE_SPLIT
+#define SEG_SPARSE_SPLIT 1
+#endif
+constexpr bool kSparseSplit = SEG_SPARSE_SPLIT;
+#ifndef SEG_SPARSE_WT
+#define SEG_SPARSE_WT 2     // only the two-word form (0: any)
+#endif
+#ifndef SEG_SPARSE_MAXMOV
+#define SEG_SPARSE_MAXMOV 32
+#endif
+#ifndef SEG_SPARSE_SPAN
+#define SEG_SPARSE_SPAN 32  // words
+#endif
 constexpr int kSegDenseFrac = 8;  // edge density (2m / n^2) from which the kernel runs 512 threads: 1 / 8
 // The one-warp form (ONEWARP, 4 G words per lane) for sparse graphs up to this
 // n: no block barriers, but measured slower -- config 2 chordal 11.9 -> 18.4 ms
@@ -288,6 +301,103 @@ __device__ __forceinline__ void st_u16(uint16_t *p, const int (&v)[WT]) {
     } else {
         *p = (uint16_t)v[0];
     }
+}
+
+// Sparse split (one warp): stably partition, movers first, every split class
+// inside the position span [S, E) -- S and E class bounds, at most 32 words --
+// the one-warp engine's split (warp_seg.cuh) on a window of position words:
+// lane l owns word (S >> 5) + l.  New class starts go to NB; returns the
+// number of new classes (warp-uniform).  Used when a step's movers are few
+// (<= 32) and their classes are short, so the block-wide scans and the two
+// extra barriers of the general split path are not needed.
+__device__ __forceinline__ int span_split_warp(int S, int E, const uint32_t *__restrict__ F,
+                                               const uint32_t *__restrict__ bnd, uint16_t *A, uint16_t *An,
+                                               uint16_t *P, uint32_t *NB) {
+    const int l = threadIdx.x & 31;
+    const uint32_t ltm = wseg::lanemask_lt();
+    const int q0 = S >> 5, nwd = ((E - 1) >> 5) - q0 + 1;
+    const int q = q0 + l;
+    const int lo = max(32 * q, S), hi = min(32 * q + 32, E);
+    const bool inr = l < nwd && lo < hi;
+    const int lob = inr ? lo - 32 * q : 0, hib = inr ? hi - 32 * q : 0;
+    const uint32_t vm = inr ? (mask_below(hib) & ~mask_below(lob)) : 0u;
+    const uint32_t Fl = inr ? (F[q] & vm) : 0u;
+    uint32_t b = inr ? (bnd[q] & vm) : 0u;
+    if (l == 0) b |= 1u << (S & 31);  // S starts a class (hpos's bit is only set at the step's end)
+    int tot;
+    const int Pc = wseg::excl_prefix6(__popc(Fl), ltm, tot);
+    const int hb = b ? 32 * q + highest_bit(b) : 0;
+    const int lb = b ? 32 * q + __ffs(b) - 1 : kSegBig;
+    const uint32_t bw = __ballot_sync(CH_FULL, b != 0);
+    const uint32_t below = bw & ltm, above = bw & ~ltm & ~(1u << l);
+    int LBr = __shfl_sync(CH_FULL, hb, below ? highest_bit(below) : 0);
+    int NBr = __shfl_sync(CH_FULL, lb, above ? __ffs(above) - 1 : 0);
+    if (!below) LBr = S;
+    if (!above) NBr = E;
+    NBr = min(NBr, E);
+    // movers at positions in [S, pp) (all lanes must call: shuffles)
+    auto cntb = [&](int pp) -> int {
+        const int qq = (pp >> 5) - q0;
+        const int pcq = __shfl_sync(CH_FULL, Pc, qq & 31);
+        const uint32_t fq = __shfl_sync(CH_FULL, Fl, qq & 31);
+        return qq >= nwd ? tot : pcq + __popc(fq & mask_below(pp & 31));
+    };
+    // words of split classes (the touched-word test of warp_seg.cuh)
+    bool touched = (((Fl ^ (Fl >> 1)) & ~(b >> 1)) & vm & (vm >> 1)) != 0;
+    const int s_in = LBr, e_in = b ? 32 * q + __ffs(b) - 1 : NBr;
+    const int s_out = b ? 32 * q + highest_bit(b) : 0, e_out = NBr;
+    const int c1 = cntb(s_in), c4 = cntb(e_out);
+    const int c2 = b ? Pc + __popc(Fl & mask_below(e_in & 31)) : c4;
+    const int c3 = Pc + __popc(Fl & mask_below(s_out & 31));
+    if (inr && !touched && !((b >> lob) & 1u)) {
+        const int T = c2 - c1;
+        touched = T > 0 && T < e_in - s_in;
+    }
+    if (inr && !touched && hib == 32 && NBr > 32 * q + 32 && b) {
+        const int T = c4 - c3;
+        touched = T > 0 && T < e_out - s_out;
+    }
+    const uint32_t pkb = (uint32_t)LBr | ((uint32_t)NBr << 16);
+    const uint32_t pkc = (uint32_t)c1 | ((uint32_t)c4 << 16);
+    const uint32_t tmask = __ballot_sync(CH_FULL, touched);
+    int nsp = 0;
+    for (uint32_t tm = tmask; tm; tm &= tm - 1) {
+        const int qq = __ffs(tm) - 1;
+        const uint32_t bq = __shfl_sync(CH_FULL, b, qq), fq = __shfl_sync(CH_FULL, Fl, qq);
+        const uint32_t pbq = __shfl_sync(CH_FULL, pkb, qq), pcq2 = __shfl_sync(CH_FULL, pkc, qq);
+        const int pcq = __shfl_sync(CH_FULL, Pc, qq);
+        const int wq = q0 + qq;
+        const int p = 32 * wq + l;
+        const bool ok = p >= S && p < E;
+        const uint32_t bl = bq & mask_below(l + 1), ab = bq & ~mask_below(l + 1);
+        const int s = bl ? 32 * wq + highest_bit(bl) : (int)(pbq & 0xFFFFu);
+        const int e = ab ? 32 * wq + __ffs(ab) - 1 : (int)(pbq >> 16);
+        const int cs = bl ? pcq + __popc(fq & mask_below(s & 31)) : (int)(pcq2 & 0xFFFFu);
+        const int T = (ab ? pcq + __popc(fq & mask_below(e & 31)) : (int)(pcq2 >> 16)) - cs;
+        if (ok) {
+            const int v = A[p];
+            int dst = p;
+            if (T > 0 && T < e - s) {
+                const int fb = pcq + __popc(fq & mask_below(l)) - cs;
+                dst = ((fq >> l) & 1u) ? s + fb : s + T + (p - s - fb);
+                if (p == s) {
+                    atomicOr(&NB[(s + T) >> 5], 1u << ((s + T) & 31));
+                    ++nsp;
+                }
+            }
+            An[dst] = (uint16_t)v;
+        }
+    }
+    __syncwarp();
+    for (uint32_t tm = tmask; tm; tm &= tm - 1) {
+        const int p = 32 * (q0 + __ffs(tm) - 1) + l;
+        if (p >= S && p < E) {
+            const int v = An[p];
+            A[p] = (uint16_t)v;
+            P[v] = (uint16_t)p;
+        }
+    }
+    return __reduce_add_sync(CH_FULL, nsp);
 }
 
 }  // namespace
@@ -634,9 +744,100 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
         uint32_t nbadd[WT];
 #pragma unroll
         for (int k = 0; k < WT; ++k) nbadd[k] = 0u;
+        // Region class starts of position word q: bnd bits in [hpos, tail0)
+        // with hpos forced.
+        auto breg = [&](int q) -> uint32_t {
+            uint32_t b = bnd[q];
+            const int lo = hpos - 32 * q;
+            if (lo > 0) b = lo >= 32 ? 0u : (b & ~mask_below(lo));
+            if (lo >= 0 && lo < 32) b |= 1u << lo;
+            return b;
+        };
+        // Sparse split: few movers (<= 32) whose classes span at most 32 words
+        // [S, E) -- one warp partitions them (span_split_warp) while the others
+        // wait at one barrier, instead of the block scans and three barriers of
+        // the general path.  Every warp finds S and E itself (same loads).
+        // Measured: c3 chordal 63.0 -> 58.9 ms, chord-removed 80.4 -> 81.3 ms;
+        // with one word per thread (8 warps) it does not pay (config 2 chordal
+        // 8.20 -> 8.27 ms), hence two-word form only; mover caps 16 / 128 / 1024
+        // and an 8-word span: within 1 %.
+        bool sparse = false;
+        int spS = -1, spE = -1;
+        if (kSparseSplit && (SEG_SPARSE_WT == 0 || WT == SEG_SPARSE_WT) && full && cntA <= SEG_SPARSE_MAXMOV &&
+            (gmx >> 5) - (gmn >> 5) < SEG_SPARSE_SPAN) {
+            for (int r = 0, qb = gmn >> 5; r < 2 && spS < 0 && qb >= (hpos >> 5); ++r, qb -= 32) {
+                const int q = qb - lane;
+                uint32_t bw = 0u;
+                if (q >= (hpos >> 5)) {
+                    bw = breg(q);
+                    if (q == (gmn >> 5)) bw &= mask_below((gmn & 31) + 1);
+                }
+                const uint32_t any = __ballot_sync(CH_FULL, bw != 0u);
+                if (any) {
+                    const int src = __ffs(any) - 1;
+                    spS = 32 * (qb - src) + highest_bit(__shfl_sync(CH_FULL, bw, src));
+                }
+            }
+            const int q1 = (gmx + 1) >> 5;
+            if (gmx + 1 >= tail0) spE = tail0;
+            for (int r = 0, qb = q1; r < 2 && spE < 0; ++r, qb += 32) {
+                if (32 * qb >= tail0) {
+                    spE = tail0;
+                    break;
+                }
+                const int q = qb + lane;
+                uint32_t bw = 0u;
+                if (32 * q < tail0) {
+                    bw = breg(q);
+                    if (q == q1) bw &= ~mask_below((gmx + 1) & 31);
+                }
+                const uint32_t any = __ballot_sync(CH_FULL, bw != 0u);
+                if (any) {
+                    const int src = __ffs(any) - 1;
+                    spE = min(tail0, 32 * (qb + src) + __ffs(__shfl_sync(CH_FULL, bw, src)) - 1);
+                }
+            }
+            sparse = spS >= 0 && spE > spS && ((spE - 1) >> 5) - (spS >> 5) < SEG_SPARSE_SPAN;
+        }
 
         if (!full) {
             if (anyE) xe = seg_scan1<ONEWARP>(extc, wt, ktot);
+        } else if (sparse) {
+            if (t == 0) {  // re-aim the speculative row load (as in the general path below)
+                int g = -1;
+                if (gmn > hpos && (gmn >> 5) - (hpos >> 5) < 4) {
+                    bool inhead = true;
+                    for (int q = hpos >> 5; q <= (gmn >> 5); ++q) {
+                        uint32_t bw = bnd[q];
+                        if (q == (hpos >> 5)) bw &= ~mask_below((hpos & 31) + 1);
+                        if (q == (gmn >> 5)) bw &= mask_below((gmn & 31) + 1);
+                        if (bw) inhead = false;
+                    }
+                    if (inhead) g = A[gmn];
+                }
+                fl[6] = g;
+            }
+            if (anyE) xe = seg_scan1<ONEWARP>(extc, wt, ktot);
+            if (warp == 0) {
+                const int ns = span_split_warp(spS, spE, F, bnd, A, An, P, NB);
+                if (lane == 0) fl[5] = ns;
+            }
+            SEG_SYNC();  // B3'
+            {
+                const int g = fl[6];
+                if (g >= 0 && g != guess) {
+                    guess = g;
+                    if (own) ld_words_nc<WT>(rows + (long long)g * sw + w0, nxt);
+                }
+            }
+            nclasses += fl[5];
+            if (own) {
+                ld_words<WT>(NB + w0, nbadd);
+                uint32_t any = 0u;
+#pragma unroll
+                for (int k = 0; k < WT; ++k) any |= nbadd[k];
+                if (any) st_zero<WT>(NB + w0);
+            }
         } else {
 #ifdef SEG_PROFILE
             seg_acc[1]++;
@@ -659,15 +860,6 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                 fl[6] = g;
             }
             // ---- phase 2: word-level scans over positions -------------------------
-            // Region class starts of position word q: bnd bits in [hpos, tail0)
-            // with hpos forced.
-            auto breg = [&](int q) -> uint32_t {
-                uint32_t b = bnd[q];
-                const int lo = hpos - 32 * q;
-                if (lo > 0) b = lo >= 32 ? 0u : (b & ~mask_below(lo));
-                if (lo >= 0 && lo < 32) b |= 1u << lo;
-                return b;
-            };
             uint32_t f[WT], b[WT];
             int cpre[WT], hb[WT], lbw[WT];
             int ctot = 0, hmax = 0, lmin = kSegBig;

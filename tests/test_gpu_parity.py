@@ -131,7 +131,7 @@ def _random_cases():
     out = []
     for n, kind, seed in [(100, "dense", 1), (257, "chordal", 2), (500, "dense", 3), (1000, "chordal", 4),
                           (1000, "sparse", 5), (2048, "chordal", 6), (3000, "dense", 7), (5000, "chordal", 8),
-                          (8191, "sparse", 9)]:
+                          (8191, "sparse", 9), (12000, "chordal", 10), (16000, "dense", 11), (20000, "sparse", 12)]:
         if kind == "dense":
             g = gen_dense_random(n, 0.5, seed)
         elif kind == "sparse":

@@ -1,3 +1,2 @@
-set -x
-bash tools/ab_variants.sh run "c3c c3r c3d c2c c2d" base fp > gpurun_out/r02_ab_fp.txt 2>&1
-grep -E "^(==|c)" gpurun_out/r02_ab_fp.txt
+bash tools/ab_variants.sh run "c3c c3r" sp_wt2 sp_mov128 sp_mov1k > gpurun_out/r02_ab_sparse3.txt 2>&1
+grep -E "^(==|c)" gpurun_out/r02_ab_sparse3.txt
