@@ -92,7 +92,16 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, long long batch, int n
 
     // ---- write the order ---------------------------------------------------
     int32_t *og = orders + g * n;
-    for (int k = lane; k < n; k += 32) og[k] = ord[k];
+    if ((n & 3) == 0 && (reinterpret_cast<uintptr_t>(og) & 15) == 0) {  // 4 entries per 64-bit load / 128-bit store
+        const uint2 *o2 = reinterpret_cast<const uint2 *>(ord);
+        int4 *g4 = reinterpret_cast<int4 *>(og);
+        for (int k = lane; k < (n >> 2); k += 32) {
+            const uint2 w = o2[k];
+            g4[k] = make_int4((int)(w.x & 0xFFFFu), (int)(w.x >> 16), (int)(w.y & 0xFFFFu), (int)(w.y >> 16));
+        }
+    } else {
+        for (int k = lane; k < n; k += 32) og[k] = ord[k];
+    }
     if (SINGLE && pos_out)
         for (int k = lane; k < n; k += 32) pos_out[k] = pos[k];
 

@@ -251,6 +251,9 @@ int chordal_peo_dense_witness(const uint8_t *adj_dev, int64_t n, int64_t stride,
 int chordal_peo_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, const int32_t *order_dev,
                       const int32_t *pos_dev, const int32_t *parent_dev, uint64_t *key_dev, int32_t *witness_dev,
                       void *stream) {
+    // three launches (key init, key, witness): a fused form whose last CTA resolves
+    // the witness (ticket counter) measured no faster -- G(8192, 0.5) is_chordal
+    // 0.1987 -> 0.2002 ms, config 3 unchanged; queued launches cost ~no gap
     int rc = chordal_key_init(key_dev, stream);
     if (rc) return rc;
     rc = chordal_peo_dense_key(adj_dev, n, stride, order_dev, pos_dev, parent_dev, 0, n, key_dev, stream);

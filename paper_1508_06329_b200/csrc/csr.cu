@@ -18,7 +18,7 @@ namespace {
 // capacity n + m + 64 covers every move of the search (each edge moves at most
 // one endpoint, once), so compaction never runs for single graphs.
 struct CsrWs {
-    size_t cls, slot, c_head, c_end, c_live, c_prev, c_next, c_tgt, c_cnt, freel, touched, scratch, total;
+    size_t cls, slot, c_head, c_end, c_live, c_prev, c_next, c_tgt, c_cnt, freel, touched, scratch, prog, total;
     long long cap;
     __host__ __device__ CsrWs(long long n, long long m, int isz, int ssz) {
         const long long nc = n + 2;
@@ -37,6 +37,7 @@ struct CsrWs {
         freel = take(nc, isz);
         touched = take(nc, isz);
         scratch = take(n, isz);
+        prog = take(4, 4);  // search -> look-ahead warp hand-off (head class, done, step)
         total = o;
     }
 };
@@ -88,8 +89,11 @@ lexbfs_csr_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict_
                   uint8_t *ws, int32_t *__restrict__ order, int32_t *__restrict__ pos, int32_t *__restrict__ parent,
                   uint64_t seed, uint64_t cell) {
     __shared__ int32_t nbuf[kNbrBuf];
-    __shared__ int prog[3];
+    // The hand-off to the look-ahead warp lives in global memory (the
+    // workspace) and is read racily on purpose: the look-ahead only needs a
+    // recent head class / step, and a stale one costs a useless prefetch.
     const CsrWs L(n, m, 4, 4);
+    volatile int *prog = reinterpret_cast<volatile int *>(ws + L.prog);
     const SlotMem<int32_t, int32_t> M = carve<int32_t, int32_t>(ws, L);
     if (threadIdx.x == 0) prog[0] = prog[1] = prog[2] = 0;
     __syncthreads();

@@ -333,7 +333,7 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
             ypre = src.fetch(MODE == CHORDAL_TIE_DESCENDING ? gb1 - 1 - lane : gb0 + lane);
         // ---- pivot: first live slot of the head class (or hash election) ----
         const int c0 = chead;
-        if (progress && lane == 0) {  // for the look-ahead warp (slot_lookahead): head class, step
+        if (progress && lane == 0 && (i & 3) == 0) {  // for the look-ahead warp (slot_lookahead): head class, step
             progress[0] = c0;
             progress[2] = i;
         }
@@ -802,7 +802,7 @@ __device__ void slot_lookahead(const int64_t *__restrict__ indptr, const int32_t
         if (progress[1]) break;
         const int step = progress[2];
         if (step - last < every) {
-            __nanosleep(32);
+            __nanosleep(256);  // the hand-off words live in global memory: poll sparingly
             continue;
         }
         last = step;

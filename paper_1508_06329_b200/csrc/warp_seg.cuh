@@ -84,8 +84,10 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
     uint32_t RAl = 0, Bl = 0;
     M.F[l] = 0;
     M.NB[l] = 0;
-    if (M.par)
-        for (int v = l; v < n; v += 32) M.par[v] = 0xFFFF;
+    if (M.par) {  // 0xFFFF over the whole (16-byte aligned, 32 W entries) array: 128-bit stores
+        uint4 *p4 = reinterpret_cast<uint4 *>(M.par);
+        for (int k = l; k < 4 * W; k += 32) p4[k] = make_uint4(CH_FULL, CH_FULL, CH_FULL, CH_FULL);
+    }
     // every rule starts at vertex 0 (parallel/lexbfs.py:173)
     if (l == 0) {
         M.A[0] = 0;

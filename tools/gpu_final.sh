@@ -1,0 +1,17 @@
+# Final round evidence on one B200: smoke, GPU tests, compute-sanitizer over every
+# kernel family, bench (ours + reference arm), ncu launch list of the bench.
+#   bash tools/gpu_final.sh TAG
+TAG=${1:-r02_final}
+set -x
+nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${TAG}_smoke.txt 2>&1
+timeout 1800 python -m pytest tests -m gpu -q 2>&1 | tail -6 > gpurun_out/${TAG}_pytest_gpu.txt
+cat gpurun_out/${TAG}_pytest_gpu.txt
+timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${TAG}_bench_ref.json 2>gpurun_out/${TAG}_bench_ref.err
+for t in memcheck racecheck synccheck; do
+  timeout 1200 compute-sanitizer --tool $t --print-limit 20 python tools/sanitize_driver.py > gpurun_out/${TAG}_sanitize_${t}.txt 2>&1
+  tail -2 gpurun_out/${TAG}_sanitize_${t}.txt
+done
+[ -n "$NO_NCU" ] || timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 600 --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 2 --warmup 3 --no-cpu > gpurun_out/${TAG}_ncu_bench.log 2>&1
+ls -la gpurun_out

@@ -1,2 +1,2 @@
-bash tools/ab_variants.sh run "c3c c3r" sp_wt2 sp_mov128 sp_mov1k > gpurun_out/r02_ab_sparse3.txt 2>&1
-grep -E "^(==|c)" gpurun_out/r02_ab_sparse3.txt
+bash tools/ab_variants.sh run "c5" laprev glob256 > gpurun_out/r02_ab_glob256.txt 2>&1
+grep -E "^(==|c)|Error" gpurun_out/r02_ab_glob256.txt
