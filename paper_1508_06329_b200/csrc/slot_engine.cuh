@@ -802,7 +802,7 @@ __device__ void slot_lookahead(const int64_t *__restrict__ indptr, const int32_t
         if (progress[1]) break;
         const int step = progress[2];
         if (step - last < every) {
-            __nanosleep(256);  // the hand-off words live in global memory: poll sparingly
+            __nanosleep(32);  // (256 ns: the look-ahead lags, 1.528 -> 1.553 s)
             continue;
         }
         last = step;
