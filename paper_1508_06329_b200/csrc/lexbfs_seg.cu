@@ -73,6 +73,16 @@ constexpr int kTieCertify = 5;
 #define SEG_SPARSE_SPLIT 1
 #endif
 constexpr bool kSparseSplit = SEG_SPARSE_SPLIT;
+// A step that splits no class and reaches no new vertex writes nothing the next
+// step reads except the mover flags and the per-warp slots, which can alternate
+// between two buffers by step parity -- so its closing barrier (B4) could be
+// skipped.  Measured slower (c3 chordal 58.8 -> 60.3 ms, config 2 chordal 8.20
+// -> 9.34 ms: warps that run ahead into the next step's phase 1 lengthen the
+// waits at its B1), so off (-DSEG_ELIDE_B4=1 builds it; correct either way).
+#ifndef SEG_ELIDE_B4
+#define SEG_ELIDE_B4 0
+#endif
+constexpr int kFBufs = SEG_ELIDE_B4 ? 2 : 1;
 #ifndef SEG_SPARSE_WT
 #define SEG_SPARSE_WT 2     // only the two-word form (0: any)
 #endif
@@ -105,7 +115,7 @@ struct SegLayout {
         const size_t WP = size_t(W + 31) & ~size_t(31);  // words rounded up to a thread's word group (<= 32)
         U = o; o = align16(o + WP * 4);
         RA = o; o = align16(o + WP * 4);
-        F = o; o = align16(o + WP * 4);
+        F = o; o = align16(o + WP * 4 * kFBufs);  // mover flags, double-buffered by step parity
         NB = o; o = align16(o + WP * 4);
         bnd = o; o = align16(o + (WP + 4) * 4);
         Pc = o; o = align16(o + WP * 2);
@@ -114,7 +124,7 @@ struct SegLayout {
         TW = o; o = align16(o + WP * 2);
         wt = o; o = align16(o + 4 * 32 * 4);
         misc = o; o = align16(o + 24 * 4);
-        wslot = o; o = align16(o + 3 * 32 * 4);  // per-warp mover count / min / max position
+        wslot = o; o = align16(o + 3 * 32 * 4 * kFBufs);  // per-warp mover count / min / max position (by parity)
         total = o;
     }
 };
@@ -425,7 +435,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
     uint16_t *P = (uint16_t *)(smem + L.P);
     uint32_t *U = (uint32_t *)(smem + L.U);
     uint32_t *RA = (uint32_t *)(smem + L.RA);
-    uint32_t *F = (uint32_t *)(smem + L.F);
+    uint32_t *const F0 = (uint32_t *)(smem + L.F);
     uint32_t *NB = (uint32_t *)(smem + L.NB);
     uint32_t *bnd = (uint32_t *)(smem + L.bnd);
     // (packing F + Pc into one 64-bit word and LB + NBq into one 32-bit word, so
@@ -461,7 +471,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
     for (int w = t; w < WP; w += NT) {
         U[w] = w < W - 1 ? CH_FULL : (w == W - 1 ? ((n & 31) ? mask_below(n & 31) : CH_FULL) : 0u);
         RA[w] = 0;
-        F[w] = 0;
+        for (int b = 0; b < kFBufs; ++b) F0[b * WP + w] = 0;
         NB[w] = 0;
         bnd[w] = 0;
     }
@@ -629,6 +639,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
             pos_out[x] = i;
         }
         int *fl = misc + 8 * (i % 3);
+        uint32_t *const F = F0 + (kFBufs > 1 ? (i & 1) * WP : 0);
         // ---- phase 1: movers and newly reached vertices, 128-bit row loads --
         uint32_t r[WT], ext[WT];
 #pragma unroll
@@ -713,7 +724,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
         // mover count and position range: per-warp slots, reduced after B1 by
         // every warp (lane w reads warp w's slot) -- same-address shared atomics
         // from every warp cost ~1 % of a step at N = 32768
-        int *ws_ = (int *)(smem + L.wslot);
+        int *ws_ = (int *)(smem + L.wslot) + (kFBufs > 1 ? (i & 1) * 96 : 0);
         {
             const int wc = __reduce_add_sync(CH_FULL, cnt);
             const int wmn = (int)__reduce_min_sync(CH_FULL, (unsigned)pmn);
@@ -1063,7 +1074,10 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
             if (cntA && (w0 + WT - 1) >= (gmn >> 5) && w0 <= (gmx >> 5)) st_zero<WT>(F + w0);
 #pragma unroll
             for (int k = 0; k < WT; ++k) {
-                if (hpos < tail0 && (hpos >> 5) == w0 + k) nbadd[k] |= 1u << (hpos & 31);
+                // (the hpos bit is never read again -- later steps force their own
+                // region start -- so elided steps skip it: no shared write then)
+                if (hpos < tail0 && (hpos >> 5) == w0 + k && !(SEG_ELIDE_B4 && !full && ktot == 0))
+                    nbadd[k] |= 1u << (hpos & 31);
                 if (ktot > 0 && (tail0 >> 5) == w0 + k) nbadd[k] |= 1u << (tail0 & 31);
             }
 #pragma unroll
@@ -1089,7 +1103,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
             tail = tail0 + ktot;
             ++nclasses;
         }
-        SEG_SYNC();  // B4
+        if (!(SEG_ELIDE_B4 && !full && ktot == 0)) SEG_SYNC();  // B4
         SEG_T(full ? 7 : 3);
         // ---- early exit: everything reached, every class a singleton ----------
         if (tail == n && nclasses == tail - hpos) {

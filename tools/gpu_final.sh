@@ -9,6 +9,7 @@ timeout 1800 python -m pytest tests -m gpu -q 2>&1 | tail -6 > gpurun_out/${TAG}
 cat gpurun_out/${TAG}_pytest_gpu.txt
 timeout 900 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
 timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${TAG}_bench_ref.json 2>gpurun_out/${TAG}_bench_ref.err
+BENCH_DIST_BACKEND=gloo timeout 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 3 --warmup 3 --no-cpu > gpurun_out/${TAG}_bench_2rank_gloo.json 2> gpurun_out/${TAG}_bench_2rank_gloo.err
 for t in memcheck racecheck synccheck; do
   timeout 1200 compute-sanitizer --tool $t --print-limit 20 python tools/sanitize_driver.py > gpurun_out/${TAG}_sanitize_${t}.txt 2>&1
   tail -2 gpurun_out/${TAG}_sanitize_${t}.txt
