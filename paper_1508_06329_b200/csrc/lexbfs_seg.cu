@@ -371,41 +371,72 @@ __device__ __forceinline__ int span_split_warp(int S, int E, const uint32_t *__r
     const uint32_t pkc = (uint32_t)c1 | ((uint32_t)c4 << 16);
     const uint32_t tmask = __ballot_sync(CH_FULL, touched);
     int nsp = 0;
-    for (uint32_t tm = tmask; tm; tm &= tm - 1) {
-        const int qq = __ffs(tm) - 1;
+#ifndef SEG_SPAN_K
+#define SEG_SPAN_K 2
+#endif
+    // K touched words per round, branch-free up to the stores, so their shuffle /
+    // shared-memory chains overlap (the other warps wait: this is latency-bound,
+    // as in the one-warp engine's single-graph form)
+    constexpr int K = SEG_SPAN_K;
+    auto word = [&](int qq, int &v, int &dst, bool &ok, bool &start, int &ns) {
         const uint32_t bq = __shfl_sync(CH_FULL, b, qq), fq = __shfl_sync(CH_FULL, Fl, qq);
         const uint32_t pbq = __shfl_sync(CH_FULL, pkb, qq), pcq2 = __shfl_sync(CH_FULL, pkc, qq);
         const int pcq = __shfl_sync(CH_FULL, Pc, qq);
         const int wq = q0 + qq;
         const int p = 32 * wq + l;
-        const bool ok = p >= S && p < E;
+        ok = p >= S && p < E;
         const uint32_t bl = bq & mask_below(l + 1), ab = bq & ~mask_below(l + 1);
         const int s = bl ? 32 * wq + highest_bit(bl) : (int)(pbq & 0xFFFFu);
         const int e = ab ? 32 * wq + __ffs(ab) - 1 : (int)(pbq >> 16);
         const int cs = bl ? pcq + __popc(fq & mask_below(s & 31)) : (int)(pcq2 & 0xFFFFu);
         const int T = (ab ? pcq + __popc(fq & mask_below(e & 31)) : (int)(pcq2 >> 16)) - cs;
-        if (ok) {
-            const int v = A[p];
-            int dst = p;
-            if (T > 0 && T < e - s) {
-                const int fb = pcq + __popc(fq & mask_below(l)) - cs;
-                dst = ((fq >> l) & 1u) ? s + fb : s + T + (p - s - fb);
-                if (p == s) {
-                    atomicOr(&NB[(s + T) >> 5], 1u << ((s + T) & 31));
-                    ++nsp;
-                }
-            }
-            An[dst] = (uint16_t)v;
+        v = ok ? (int)A[p] : 0;
+        const bool split = T > 0 && T < e - s;
+        const int fb = pcq + __popc(fq & mask_below(l)) - cs;
+        const int to = ((fq >> l) & 1u) ? s + fb : s + T + (p - s - fb);
+        dst = split ? to : p;
+        start = ok && split && p == s;
+        ns = s + T;
+    };
+    for (uint32_t tm = tmask; tm;) {
+        int qv[K], v[K], dst[K], ns[K];
+        bool has[K], ok[K], st[K];
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+            has[u] = tm != 0;
+            qv[u] = has[u] ? __ffs(tm) - 1 : 0;
+            tm &= tm - 1;
         }
+#pragma unroll
+        for (int u = 0; u < K; ++u) word(qv[u], v[u], dst[u], ok[u], st[u], ns[u]);
+#pragma unroll
+        for (int u = 0; u < K; ++u)
+            if (has[u] && ok[u]) An[dst[u]] = (uint16_t)v[u];
+#pragma unroll
+        for (int u = 0; u < K; ++u)
+            if (has[u] && st[u]) {
+                atomicOr(&NB[ns[u] >> 5], 1u << (ns[u] & 31));
+                ++nsp;
+            }
     }
     __syncwarp();
-    for (uint32_t tm = tmask; tm; tm &= tm - 1) {
-        const int p = 32 * (q0 + __ffs(tm) - 1) + l;
-        if (p >= S && p < E) {
-            const int v = An[p];
-            A[p] = (uint16_t)v;
-            P[v] = (uint16_t)p;
+    for (uint32_t tm = tmask; tm;) {
+        int p[K], v[K];
+        bool ok[K];
+#pragma unroll
+        for (int u = 0; u < K; ++u) {
+            const bool h = tm != 0;
+            p[u] = h ? 32 * (q0 + __ffs(tm) - 1) + l : 32 * q0 + l;
+            tm &= tm - 1;
+            ok[u] = h && p[u] >= S && p[u] < E;
+            v[u] = An[p[u]];
         }
+#pragma unroll
+        for (int u = 0; u < K; ++u)
+            if (ok[u]) {
+                A[p[u]] = (uint16_t)v[u];
+                P[v[u]] = (uint16_t)p[u];
+            }
     }
     return __reduce_add_sync(CH_FULL, nsp);
 }
