@@ -37,20 +37,16 @@ struct BatchLayout {  // shared memory per graph (one warp); the adjacency stays
 
 }  // namespace
 
-// Row loads of the PEO check: read-only path for global rows, plain loads for rows
-// staged in shared memory (the single-graph form).
-template <bool SMEM_ROWS>
-__device__ __forceinline__ uint4 ld_row4(const uint4 *p) {
-    if (SMEM_ROWS) return *p;
-    return __ldg(p);
-}
-
-// SINGLE: one graph (n <= 1024) whose rows are first staged in shared memory; the
-// search uses the shorter-latency scans, and positions are written out as well.
-template <int WPC, int MINB, bool SINGLE = false>
+// (A single-graph form -- rows staged in shared memory, search, PEO check and
+// witness in one launch -- measured slower than the separate one-warp search
+// kernel + the grid-wide dense PEO kernels once the latter record the parents:
+// config 1 is_chordal 0.62 -> 0.52 ms; a single warp checks 1000 vertices
+// serially, and warps parked at a barrier beside the searching warp slow it
+// down by 18 %.  Removed.)
+template <int WPC, int MINB>
 __global__ void __launch_bounds__(32 * WPC, MINB)
 batch_chordal_kernel(const uint8_t *__restrict__ adj_all, long long batch, int n, int stride,
-                     int32_t *__restrict__ orders, int32_t *__restrict__ witness, int32_t *__restrict__ pos_out = nullptr) {
+                     int32_t *__restrict__ orders, int32_t *__restrict__ witness) {
     extern __shared__ __align__(16) uint8_t smem[];
     const BatchLayout L(n);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -61,22 +57,6 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, long long batch, int n
     const int sw = stride >> 2;  // row pitch in 32-bit words
     const uint32_t *A32 = reinterpret_cast<const uint32_t *>(adj_all + g * (long long)n * stride);
     uint8_t *ws = smem + warp * L.total;
-    if (SINGLE) {  // stage the rows after the search state: 16-byte copies, eight in flight per lane
-        uint4 *dst = reinterpret_cast<uint4 *>(smem + L.total);
-        const uint4 *src = reinterpret_cast<const uint4 *>(A32);
-        const int n16 = n * (stride >> 4);
-        int k = lane;
-        for (; k + 7 * 32 < n16; k += 8 * 32) {
-            uint4 t[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) t[j] = __ldg(src + k + 32 * j);
-#pragma unroll
-            for (int j = 0; j < 8; ++j) dst[k + 32 * j] = t[j];
-        }
-        for (; k < n16; k += 32) dst[k] = __ldg(src + k);
-        __syncwarp();
-        A32 = reinterpret_cast<const uint32_t *>(smem + L.total);
-    }
     WarpSegMem M;
     M.A = (uint16_t *)(ws + L.A);
     M.An = (uint16_t *)(ws + L.An);
@@ -87,7 +67,7 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, long long batch, int n
     const uint16_t *ord = M.A, *pos = M.P, *par = M.par;
 
     // ---- LexBFS -------------------------------------------------------------------
-    warp_seg_lexbfs<CHORDAL_TIE_ASCENDING, SINGLE, SINGLE>(A32, sw, n, M);
+    warp_seg_lexbfs<CHORDAL_TIE_ASCENDING, false, false>(A32, sw, n, M);
     const bool have_parent = true;
 
     // ---- write the order ---------------------------------------------------
@@ -102,8 +82,6 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, long long batch, int n
     } else {
         for (int k = lane; k < n; k += 32) og[k] = ord[k];
     }
-    if (SINGLE && pos_out)
-        for (int k = lane; k < n; k += 32) pos_out[k] = pos[k];
 
     // ---- PEO check: lanes stride over vertices -----------------------------------
     unsigned long long best = ~0ULL;
@@ -159,8 +137,8 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, long long batch, int n
             for (int j = 0; j < 4; ++j) {
                 uint4 x = make_uint4(0, 0, 0, 0), y = make_uint4(0, 0, 0, 0);
                 if (w0 + 4 * j < W) {
-                    x = ld_row4<SINGLE>(rv4 + (w0 >> 2) + j);
-                    y = ld_row4<SINGLE>(rp4 + (w0 >> 2) + j);
+                    x = __ldg(rv4 + (w0 >> 2) + j);
+                    y = __ldg(rp4 + (w0 >> 2) + j);
                 }
                 a[4 * j] = x.x; a[4 * j + 1] = x.y; a[4 * j + 2] = x.z; a[4 * j + 3] = x.w;
                 b[4 * j] = y.x; b[4 * j + 1] = y.y; b[4 * j + 2] = y.z; b[4 * j + 3] = y.w;
@@ -226,25 +204,6 @@ static int launch_batch_cfg(const uint8_t *adj, int64_t batch, int64_t n, int64_
     const long long blocks = (batch + WPC - 1) / WPC;
     batch_chordal_kernel<WPC, MINB><<<(unsigned)blocks, 32 * WPC, smem, stream>>>(adj, batch, (int)n, (int)stride,
                                                                                   orders, witness);
-    CH_LAUNCH_CHECK();
-    return CHORDAL_OK;
-}
-
-// is_chordal of ONE graph with n <= 1024 in a single launch: rows staged in shared
-// memory, LexBFS + PEO check + witness by one warp (the dense pipeline's three
-// kernels and their launch gaps otherwise dominate such small graphs).
-bool single_fits(int64_t n, int64_t stride) {
-    return n > 0 && n <= 1024 && BatchLayout((int)n).total + (size_t)n * stride <= 200 * 1024;
-}
-
-int launch_single(const uint8_t *adj, int64_t n, int64_t stride, int32_t *order, int32_t *pos, int32_t *witness,
-                  cudaStream_t stream) {
-    if (!single_fits(n, stride)) return CHORDAL_ETOOLARGE;
-    const size_t smem = BatchLayout((int)n).total + (size_t)n * stride;
-    if (cudaFuncSetAttribute(batch_chordal_kernel<1, 1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)smem) != cudaSuccess)
-        return CHORDAL_ECUDA;
-    batch_chordal_kernel<1, 1, true><<<1, 32, smem, stream>>>(adj, 1, (int)n, (int)stride, order, witness, pos);
     CH_LAUNCH_CHECK();
     return CHORDAL_OK;
 }

@@ -30,8 +30,6 @@ int launch_peo_dense_witness(const uint8_t *, int64_t, int64_t, const int32_t *,
                              int32_t *, cudaStream_t);
 int launch_permute_dense(const uint8_t *, int64_t, int64_t, const int32_t *, uint8_t *, cudaStream_t);
 int launch_batch(const uint8_t *, int64_t, int64_t, int64_t, int32_t *, int32_t *, cudaStream_t);
-bool single_fits(int64_t, int64_t);
-int launch_single(const uint8_t *, int64_t, int64_t, int32_t *, int32_t *, int32_t *, cudaStream_t);
 int launch_mcs_dense(const uint8_t *, int64_t, int64_t, bool, uint64_t, int32_t *, int32_t *, cudaStream_t);
 size_t bfs_csr_workspace_bytes(int64_t);
 int launch_bfs_dense(const uint8_t *, int64_t, int64_t, bool, uint64_t, int32_t *, int32_t *, cudaStream_t);
@@ -273,18 +271,15 @@ int chordal_is_chordal_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, 
     }
     const DenseWs L(n, m < 0 ? 0 : m);
     if (!ws || ws_bytes < L.total) return CHORDAL_EINVAL;
-    if (tie_rule == CHORDAL_TIE_ASCENDING && single_fits(n, stride) && order_dev && pos_dev && witness_dev) {
-        const int rc0 = check_dense(adj_dev, n, stride);
-        if (rc0) return rc0;
-        return launch_single(adj_dev, n, stride, order_dev, pos_dev, witness_dev, s);  // one fused launch
-    }
     uint8_t *w = reinterpret_cast<uint8_t *>(ws);
     uint64_t *key = reinterpret_cast<uint64_t *>(w + L.key);
     // The shared-memory CTA engine would record parents with one global store per
     // unvisited neighbour per step (~6 % of its step time at N = 32768, k = 1024);
     // the PEO kernel finds them in a fraction of a millisecond instead.  The slot
     // engine (n > 32768) keeps recording them.
-    int32_t *parent = use_seg(n) ? nullptr : reinterpret_cast<int32_t *>(w + L.parent);
+    // The one-warp engine (n <= 1024) records them in shared memory and copies
+    // them out with the order.
+    int32_t *parent = (use_seg(n) && n > 1024) ? nullptr : reinterpret_cast<int32_t *>(w + L.parent);
     int rc = chordal_lexbfs_dense(adj_dev, n, stride, m, tie_rule, seed, order_dev, pos_dev, parent, ws, ws_bytes,
                                   stream);
     if (rc) return rc;

@@ -864,7 +864,7 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
                 const int ns = span_split_warp(spS, spE, F, bnd, A, An, P, NB);
                 if (lane == 0) fl[5] = ns;
             }
-            SEG_SYNC();  // B3'
+            SEG_SYNC();  // B3' (polling a flag instead measured slower: c3 chordal 58.1 -> 60.5 ms)
             {
                 const int g = fl[6];
                 if (g >= 0 && g != guess) {
@@ -1168,8 +1168,11 @@ size_t seg_smem_bytes(int64_t n) { return SegLayout((int)((n + 31) >> 5)).total;
 
 // n <= 1024, LOWEST_INDEX / descending ties: the one-warp engine (warp_seg.cuh),
 // bitsets in registers; the arrays are copied out at the end.
+// Launched with kWarpKernelWarps warps: all stage the rows (more loads in
+// flight); warp 0 runs the search and copies the arrays out.
+constexpr int kWarpKernelWarps = 8;
 template <int MODE, bool STAGE>
-__global__ void __launch_bounds__(32, 1)
+__global__ void __launch_bounds__(32 * kWarpKernelWarps, 1)
 lexbfs_warp_kernel(const uint8_t *__restrict__ adj, int n, long long stride, int32_t *__restrict__ order,
                    int32_t *__restrict__ pos_out, int32_t *__restrict__ parent) {
     extern __shared__ __align__(16) uint8_t smem[];
@@ -1182,22 +1185,26 @@ lexbfs_warp_kernel(const uint8_t *__restrict__ adj, int n, long long stride, int
     M.F = (uint32_t *)(M.par + np);
     M.NB = M.F + 32;
     const uint32_t *rows = reinterpret_cast<const uint32_t *>(adj);
-    if (STAGE) {  // rows into shared memory after the state (16-byte aligned), eight copies in flight per lane
+    const int nthr = blockDim.x;
+    if (STAGE) {  // rows into shared memory after the state (16-byte aligned), eight copies in flight per thread
         uint4 *dst = reinterpret_cast<uint4 *>(smem + ((np * 8 + 256 + 15) & ~size_t(15)));
         const uint4 *src = reinterpret_cast<const uint4 *>(adj);
-        const int n16 = n * (int)(stride >> 4), lane = threadIdx.x & 31;
-        int k = lane;
-        for (; k + 7 * 32 < n16; k += 8 * 32) {
+        const int n16 = n * (int)(stride >> 4);
+        int k = threadIdx.x;
+        for (; k + 7 * nthr < n16; k += 8 * nthr) {
             uint4 t[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) t[j] = __ldg(src + k + 32 * j);
+            for (int j = 0; j < 8; ++j) t[j] = __ldg(src + k + nthr * j);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) dst[k + 32 * j] = t[j];
+            for (int j = 0; j < 8; ++j) dst[k + nthr * j] = t[j];
         }
-        for (; k < n16; k += 32) dst[k] = __ldg(src + k);
-        __syncwarp();
+        for (; k < n16; k += nthr) dst[k] = __ldg(src + k);
         rows = reinterpret_cast<const uint32_t *>(dst);
     }
+    __syncthreads();
+    // the staging warps leave: parked at a barrier beside the searching warp they
+    // slow it down (config 1: 0.50 -> 0.59 ms)
+    if (threadIdx.x >= 32) return;
     warp_seg_lexbfs<MODE, true, STAGE>(rows, (int)(stride >> 2), n, M);
     for (int k = threadIdx.x; k < n; k += 32) {
         order[k] = M.A[k];
@@ -1223,7 +1230,7 @@ int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int64_t m, 
     if (cudaFuncSetAttribute(lexbfs_warp_kernel<M, S>, cudaFuncAttributeMaxDynamicSharedMemorySize,           \
                              (int)wsmem) != cudaSuccess)                                                      \
         return CHORDAL_ECUDA;                                                                                 \
-    lexbfs_warp_kernel<M, S><<<1, 32, wsmem, stream>>>(adj, (int)n, stride, order, pos, parent);
+    lexbfs_warp_kernel<M, S><<<1, 32 * kWarpKernelWarps, wsmem, stream>>>(adj, (int)n, stride, order, pos, parent);
         if (tie_rule == CHORDAL_TIE_DESCENDING) {
             if (stage) { WARP_LAUNCH(CHORDAL_TIE_DESCENDING, true) } else { WARP_LAUNCH(CHORDAL_TIE_DESCENDING, false) }
         } else {
