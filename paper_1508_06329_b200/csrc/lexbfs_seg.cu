@@ -1264,6 +1264,12 @@ int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int64_t m, 
 #ifdef SEG_THREADS_ENV
     if (const char *ev = getenv("SEG_THREADS")) T2 = max(T2, atoi(ev));
 #endif
+#ifndef SEG_MV_DENSE
+#define SEG_MV_DENSE 4
+#endif
+#ifndef SEG_MV_SPARSE
+#define SEG_MV_SPARSE 2
+#endif
     const bool wt1 = W <= (dense ? 512 : 256);  // one word per thread within a 512-thread register budget
     const size_t smem = seg_smem_bytes(n);
     cudaError_t e;
@@ -1288,13 +1294,13 @@ int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int64_t m, 
 #define SEG_LAUNCH(M)                                   \
     SEG_LAUNCH_OW(M)                                    \
     if (dense && wt1) {                                 \
-        SEG_LAUNCH_K(M, 4, 1, false, T1, 512)           \
+        SEG_LAUNCH_K(M, SEG_MV_DENSE, 1, false, T1, 512) \
     } else if (dense) {                                 \
-        SEG_LAUNCH_K(M, 4, 2, false, T2, 512)           \
+        SEG_LAUNCH_K(M, SEG_MV_DENSE, 2, false, T2, 512) \
     } else if (wt1) {                                   \
-        SEG_LAUNCH_K(M, 2, 1, false, T1, 512)           \
+        SEG_LAUNCH_K(M, SEG_MV_SPARSE, 1, false, T1, 512) \
     } else {                                            \
-        SEG_LAUNCH_K(M, 2, 2, false, T2, 512)           \
+        SEG_LAUNCH_K(M, SEG_MV_SPARSE, 2, false, T2, 512) \
     }
     switch (tie_rule) {
         case CHORDAL_TIE_ASCENDING: SEG_LAUNCH(CHORDAL_TIE_ASCENDING); break;

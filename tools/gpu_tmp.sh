@@ -1,3 +1,2 @@
-timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
-bash tools/ab_variants.sh run "c1 c3c c3r" cur spoll > gpurun_out/r02_ab_spoll.txt 2>&1
-grep -E "^(==|c)|Error" gpurun_out/r02_ab_spoll.txt
+bash tools/ab_variants.sh run "c3c c3r c3d c2c c2d" mvbase mvd2 mvs1 > gpurun_out/r02_ab_mv.txt 2>&1
+grep -E "^(==|c)|Error" gpurun_out/r02_ab_mv.txt
