@@ -1267,6 +1267,9 @@ int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int64_t m, 
 #ifndef SEG_MV_DENSE
 #define SEG_MV_DENSE 4
 #endif
+// movers per round, sparse graphs: 2 with two words per thread, 1 with one
+// (config 2 chordal 8.20 -> 7.96 ms; c3 chordal with 1: 58.6 -> 59.0 ms);
+// dense graphs: 4 (2: unchanged)
 #ifndef SEG_MV_SPARSE
 #define SEG_MV_SPARSE 2
 #endif
@@ -1298,7 +1301,7 @@ int launch_lexbfs_seg(const uint8_t *adj, int64_t n, int64_t stride, int64_t m, 
     } else if (dense) {                                 \
         SEG_LAUNCH_K(M, SEG_MV_DENSE, 2, false, T2, 512) \
     } else if (wt1) {                                   \
-        SEG_LAUNCH_K(M, SEG_MV_SPARSE, 1, false, T1, 512) \
+        SEG_LAUNCH_K(M, 1, 1, false, T1, 512)           \
     } else {                                            \
         SEG_LAUNCH_K(M, SEG_MV_SPARSE, 2, false, T2, 512) \
     }

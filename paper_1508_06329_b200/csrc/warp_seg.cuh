@@ -126,8 +126,10 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
         }
         const int x = M.A[i];
         const int tail0 = tail, hpos = i + 1;
-        const uint32_t bh = __shfl_sync(CH_FULL, Bl, (hpos >> 5) & 31);
-        if (hpos >= tail0 || ((bh >> (hpos & 31)) & 1u)) --nclasses;  // x's class was {x}
+        if (LATENCY) {  // class count for the early exit (the batch tests the class starts instead)
+            const uint32_t bh = __shfl_sync(CH_FULL, Bl, (hpos >> 5) & 31);
+            if (hpos >= tail0 || ((bh >> (hpos & 31)) & 1u)) --nclasses;  // x's class was {x}
+        }
         // ---- row of x ---------------------------------------------------------
         uint32_t r = 0;
 #ifdef WSEG_PROFILE
@@ -399,7 +401,7 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
                         }
                     }
                 }
-                nclasses += __reduce_add_sync(CH_FULL, nsp);
+                if (LATENCY) nclasses += __reduce_add_sync(CH_FULL, nsp);
                 __syncwarp();
                 Bl |= M.NB[l];
                 M.NB[l] = 0;
@@ -419,16 +421,30 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
                 M.P[y] = (uint16_t)dst;
             }
         }
-        if (hpos < tail0 && l == (hpos >> 5)) Bl |= 1u << (hpos & 31);
+        // The start bit at hpos is never read again (every later step forces its
+        // own region start); the batch skips it (config 4: 6.13 -> 6.01 ms), the
+        // latency form keeps it (dropping it measured 0.504 -> 0.513 ms there).
+        if (LATENCY && hpos < tail0 && l == (hpos >> 5)) Bl |= 1u << (hpos & 31);
         if (ktot > 0 && l == (tail0 >> 5)) Bl |= 1u << (tail0 & 31);
         if (ktot > 0) {
             tail = tail0 + ktot;
-            ++nclasses;
+            if (LATENCY) ++nclasses;
         }
         __syncwarp();
         WSEG_T(5);
         // ---- early exit: everything reached, every class a singleton ---------------
-        if (tail == n && nclasses == tail - hpos) {
+        // batch form: with everything reached, test the class starts of [hpos, n)
+        // directly (cheaper than keeping a class count every step)
+        bool singletons = false;
+        if (LATENCY) {
+            singletons = tail == n && nclasses == tail - hpos;
+        } else if (tail == n) {
+            const int lo = hpos + 1 - 32 * l;  // positions <= hpos count as starts
+            uint32_t m = Bl | (lo <= 0 ? 0u : mask_below(lo > 32 ? 32 : lo));
+            if (32 * l + 32 > n) m |= ~mask_below(n - 32 * l > 0 ? n - 32 * l : 0);
+            singletons = __all_sync(CH_FULL, m == CH_FULL);
+        }
+        if (singletons) {
             if (M.par)
                 for (int p = hpos + l; p < n; p += 32) M.par[M.A[p]] = 0xFFFE;
             break;

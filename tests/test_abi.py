@@ -51,3 +51,26 @@ def test_status_strings():
 
     assert _native.lib.chordal_strerror(0) == b"ok"
     assert _native.lib.chordal_abi_version() == 3
+
+
+def test_round2_entry_points_host_side():
+    """Certificate / NCCL entry points: workspace sizes, argument validation that
+    needs no device (NULL communicator / status), the ENCCL status string, and the
+    communicator-pointer helper."""
+    from paper_1508_06329_b200 import _native
+    from paper_1508_06329_b200.distributed import _comm_ptr
+
+    lib = _native.lib
+    assert lib.chordal_lexbfs_certify_workspace_bytes(0) == 0
+    assert lib.chordal_lexbfs_certify_workspace_bytes(1000) == 8000
+    assert lib.chordal_strerror(_native.ENCCL).startswith(b"NCCL")
+    d1, d2 = lib.chordal_dense_nccl_workspace_bytes(1000, 4000), lib.chordal_dense_nccl_workspace_bytes(2000, 4000)
+    assert 0 < d1 < d2
+    # n > 32768 dense: the CSR route's workspace grows with m
+    assert lib.chordal_dense_nccl_workspace_bytes(40000, 10**6) > lib.chordal_dense_nccl_workspace_bytes(40000, 10**5)
+    assert lib.chordal_csr_nccl_workspace_bytes(10**6, 8 * 10**6) > lib.chordal_csr_nccl_workspace_bytes(10**6, 10**6)
+    # NULL communicator / status: rejected before anything touches a device
+    assert lib.chordal_is_chordal_csr_nccl(None, None, 10, 5, 0, 0, 0, None, None, None, None, None, 0,
+                                           None) == _native.EINVAL
+    assert lib.chordal_lexbfs_certify_dense(None, 10, 16, 0, None, None, None, 0, None) == _native.EINVAL
+    assert _comm_ptr(0x1234) == 0x1234

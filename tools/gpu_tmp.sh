@@ -1,2 +1,3 @@
-bash tools/ab_variants.sh run "c3c c3r c3d c2c c2d" mvbase mvd2 mvs1 > gpurun_out/r02_ab_mv.txt 2>&1
-grep -E "^(==|c)|Error" gpurun_out/r02_ab_mv.txt
+bash tools/ab_variants.sh run "batch c1" hposbase bopt > gpurun_out/r02_ab_bopt.txt 2>&1
+grep -E "^(==|c|b)|Error" gpurun_out/r02_ab_bopt.txt
+timeout 1500 python -m pytest tests -m gpu -q -x 2>&1 | tail -2
