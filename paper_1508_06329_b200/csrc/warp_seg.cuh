@@ -41,7 +41,7 @@ __device__ unsigned long long wseg_ph[8];
 
 struct WarpSegMem {
     uint16_t *A, *An, *P;  // [32 W]
-    uint16_t *par;         // [n] or nullptr; 0xFFFF = no parent, 0xFFFE = left to the PEO check
+    uint16_t *par;         // [32 W] PEO parents (required); 0xFFFF = no parent, 0xFFFE = left to the PEO check
     uint32_t *F, *NB;      // [32]
 };
 
@@ -84,7 +84,7 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
     uint32_t RAl = 0, Bl = 0;
     M.F[l] = 0;
     M.NB[l] = 0;
-    if (M.par) {  // 0xFFFF over the whole (16-byte aligned, 32 W entries) array: 128-bit stores
+    {  // par: 0xFFFF over the whole (16-byte aligned, 32 W entries) array: 128-bit stores
         uint4 *p4 = reinterpret_cast<uint4 *>(M.par);
         for (int k = l; k < 4 * W; k += 32) p4[k] = make_uint4(CH_FULL, CH_FULL, CH_FULL, CH_FULL);
     }
@@ -163,13 +163,13 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
             mv &= mv - 1;
             const int pp = (int)M.P[y];
             atomicOr(&M.F[pp >> 5], 1u << (pp & 31));
-            if (M.par) M.par[y] = (uint16_t)x;
+            M.par[y] = (uint16_t)x;
             pmn = min(pmn, pp);
             pmx = max(pmx, pp);
         }
         WSEG_T(1);
         if (ext) {
-            if (M.par) {
+            {
                 uint32_t m3 = ext;
                 while (m3) {
                     M.par[32 * l + __ffs(m3) - 1] = (uint16_t)x;
@@ -445,8 +445,7 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
             singletons = __all_sync(CH_FULL, m == CH_FULL);
         }
         if (singletons) {
-            if (M.par)
-                for (int p = hpos + l; p < n; p += 32) M.par[M.A[p]] = 0xFFFE;
+            for (int p = hpos + l; p < n; p += 32) M.par[M.A[p]] = 0xFFFE;
             break;
         }
     }
