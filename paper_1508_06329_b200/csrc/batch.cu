@@ -217,7 +217,10 @@ int launch_batch(const uint8_t *adj, int64_t batch, int64_t n, int64_t stride, i
     // 7.56 ms per config-4 batch uncapped (71 registers, 28 warps), 7.12 at 64
     // (<4, 8>), 7.02 here, 7.20 at 48 (<4, 10>), 8.58 at 40; <2, 18> 7.40,
     // <8, 4> 7.25 (tools/ab_multi.sh).
-    return launch_batch_cfg<4, 9>(adj, batch, n, stride, orders, witness, stream);
+#ifndef BATCH_MINB
+#define BATCH_MINB 9  // round 2 re-check: 8 (64 registers) 6.25 ms, 10 (48, spills) 6.29 ms, 9: 5.95 ms
+#endif
+    return launch_batch_cfg<4, BATCH_MINB>(adj, batch, n, stride, orders, witness, stream);
 }
 
 }  // namespace chordal
