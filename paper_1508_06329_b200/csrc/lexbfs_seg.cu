@@ -749,8 +749,9 @@ lexbfs_seg_kernel(const uint8_t *__restrict__ adj, int n, long long stride, uint
 #endif
         // The next pivot's row, issued only now: issued before the mover loop
         // (into the registers the current row just left) it stalled that loop
-        // (c3 chordal 90.5 -> 86.5 ms); an extra L2 prefetch of the row after
-        // it no longer pays once the load sits here.
+        // (c3 chordal 90.5 -> 86.5 ms; re-measured at two words per thread: 58.9
+        // -> 67.3 ms); an extra L2 prefetch of the row after it no longer pays
+        // once the load sits here.
         if (guess >= 0 && own) ld_words_nc<WT>(rows + (long long)guess * sw + w0, nxt);
         // mover count and position range: per-warp slots, reduced after B1 by
         // every warp (lane w reads warp w's slot) -- same-address shared atomics
