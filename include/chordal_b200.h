@@ -94,8 +94,10 @@ size_t chordal_dense_workspace_bytes(int64_t n, int64_t m);
  * every vertex (-1 for none, -2 for "not computed": vertices placed by the
  * early exit once every class is a singleton); the PEO checks accept -2
  * entries and search those parents themselves.
- * Engines: n <= 32768 runs the persistent single-CTA touched-segment kernel
- * (state in shared memory, any density; m is ignored and may be < 0); larger
+ * Engines: n <= 1024 (LOWEST_INDEX / descending) runs the one-warp engine; up to
+ * n <= 32768 the persistent single-CTA touched-segment kernel (state in shared
+ * memory, any density; m, when known, picks its dense or sparse form -- pass
+ * m < 0 or 0 if unknown: the sparse form is then used); larger
  * graphs are converted to CSR on the device and run the O(deg)-per-step slot
  * kernel, which needs the edge count m (Graph.m): pass m < 0 to let the call
  * count the edges, which synchronises `stream` once. */
