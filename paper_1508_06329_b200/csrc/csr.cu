@@ -6,6 +6,8 @@
 // (search.py:500-532) and _is_peo_lists (peo.py:100-149) -- the pair the
 // reference runs on graphs that only expose n, m and adjacency_lists0()
 // (the N = 10^6 configuration).
+#include <cstdlib>
+
 #include "common.cuh"
 #include "slot_engine.cuh"
 
@@ -127,6 +129,75 @@ lexbfs_csr_smem_kernel(const int64_t *__restrict__ indptr, const int32_t *__rest
                                                                               cell);
 }
 
+// Small sparse graphs: the whole engine state -- class bookkeeping and the slot
+// array included -- in shared memory with u16 ids and u16 slot indices, so a
+// step's chain of dependent reads (pivot slot -> neighbour classes -> class
+// fields -> next head slot) costs shared-memory latency instead of L2 round
+// trips.  Only the neighbour lists stay in global memory.  The slot array holds
+// as many slots as fit (>= 2n + 64); when the bump pointer would overflow, the
+// live slots are compacted (slot_detail::compact).
+constexpr int kAllNbrBuf = 1024;
+struct AllSmemLayout {
+    size_t cls, slot, c_head, c_end, c_live, c_prev, c_next, c_tgt, c_cnt, freel, touched, scratch, nbuf, total;
+    long long cap;
+    __host__ __device__ AllSmemLayout(long long n, long long cap_) : cap(cap_) {
+        const long long nc = n + 2;
+        size_t o = 0;
+        auto take = [&](long long elems) { size_t r = o; o += ((size_t)elems * 2 + 15) & ~size_t(15); return r; };
+        cls = take(n);
+        c_head = take(nc);
+        c_end = take(nc);
+        c_live = take(nc);
+        c_prev = take(nc);
+        c_next = take(nc);
+        c_tgt = take(nc);
+        c_cnt = take(nc);
+        freel = take(nc);
+        touched = take(nc);
+        scratch = take(n);
+        nbuf = take(kAllNbrBuf);
+        slot = take(cap + slot_detail::kSlotPad);
+        total = o;
+    }
+};
+constexpr size_t kAllSmemMax = 232448;  // 227 KB of dynamic shared memory per block
+// slot capacity for all-in-shared-memory state, or 0 when it does not fit
+inline long long all_smem_cap(long long n, long long m) {
+    if (n > 8836) return 0;  // 26 n + ~3 KB bytes must fit
+    const AllSmemLayout L0(n, 0);
+    const long long room = ((long long)kAllSmemMax - (long long)L0.total) / 2 - slot_detail::kSlotPad - 8;
+    long long cap = n + m + 64 < room ? n + m + 64 : room;
+    if (cap > 65000) cap = 65000;  // u16 slot indices
+    return cap >= 2 * n + 64 ? cap : 0;
+}
+
+template <int MODE>
+__global__ void __launch_bounds__(32, 1)
+lexbfs_csr_allsmem_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict__ indices, int n,
+                          long long cap, int32_t *__restrict__ order, int32_t *__restrict__ pos,
+                          int32_t *__restrict__ parent, uint64_t seed, uint64_t cell) {
+    extern __shared__ __align__(16) uint8_t smb[];
+    const AllSmemLayout L(n, cap);
+    SlotMem<uint16_t, uint16_t> M;
+    M.cls = reinterpret_cast<uint16_t *>(smb + L.cls);
+    M.slot_v = reinterpret_cast<uint16_t *>(smb + L.slot);
+    M.c_head = reinterpret_cast<uint16_t *>(smb + L.c_head);
+    M.c_end = reinterpret_cast<uint16_t *>(smb + L.c_end);
+    M.c_live = reinterpret_cast<uint16_t *>(smb + L.c_live);
+    M.c_prev = reinterpret_cast<uint16_t *>(smb + L.c_prev);
+    M.c_next = reinterpret_cast<uint16_t *>(smb + L.c_next);
+    M.c_tgt = reinterpret_cast<uint16_t *>(smb + L.c_tgt);
+    M.c_cnt = reinterpret_cast<uint16_t *>(smb + L.c_cnt);
+    M.freel = reinterpret_cast<uint16_t *>(smb + L.freel);
+    M.touched = reinterpret_cast<uint16_t *>(smb + L.touched);
+    M.scratch = reinterpret_cast<uint16_t *>(smb + L.scratch);
+    M.cap = cap;
+    uint16_t *nbuf = reinterpret_cast<uint16_t *>(smb + L.nbuf);
+    CsrStagedSource<uint16_t> src{indptr, indices, nbuf, kAllNbrBuf, 0};
+    slot_lexbfs<uint16_t, uint16_t, MODE, CsrStagedSource<uint16_t>, int32_t>(src, n, M, order, pos, parent, seed,
+                                                                               cell);
+}
+
 // ---------------------------------------------------------------------------
 // bitset rows -> CSR (ascending per row)
 __global__ void row_degrees_kernel(const uint8_t *__restrict__ adj, int n, long long stride,
@@ -218,7 +289,15 @@ static int launch_csr_mode(const int64_t *indptr, const int32_t *indices, int64_
                            uint64_t cell, int32_t *order, int32_t *pos, int32_t *parent, void *ws,
                            cudaStream_t stream) {
     uint8_t *w = reinterpret_cast<uint8_t *>(ws);
-    if (n <= kSmemMaxN) {
+    const long long acap = getenv("CSR_NO_ALLSMEM") ? 0 : all_smem_cap(n, m);
+    if (acap > 0) {
+        const size_t sm = AllSmemLayout(n, acap).total;
+        if (cudaFuncSetAttribute(lexbfs_csr_allsmem_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)sm) != cudaSuccess)
+            return CHORDAL_ECUDA;
+        lexbfs_csr_allsmem_kernel<MODE><<<1, 32, sm, stream>>>(indptr, indices, (int)n, acap, order, pos, parent,
+                                                               seed, cell);
+    } else if (n <= kSmemMaxN) {
         const size_t sm = smem16_bytes(n);
         if (cudaFuncSetAttribute(lexbfs_csr_smem_kernel<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)sm) != cudaSuccess)

@@ -127,7 +127,7 @@ struct CsrStagedSource {
 // [2] bounds + pass 1 [3] allocate [4] pass 2 + restore [5] touched classes
 // [6] steps with the pivot known ahead [7] steps with its row bounds fetched ahead
 // [8] fast steps (<= 32 neighbours) [9] (unused)
-__device__ unsigned long long slot_prof[10];
+__device__ unsigned long long slot_prof[16];
 #define SLOT_T(k)                                           \
     do {                                                    \
         const long long _c = clock64();                     \
@@ -315,7 +315,7 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
     long long nxs = -1;
 
 #ifdef SLOT_PROFILE
-    unsigned long long slot_acc[10] = {0, 0, 0, 0, 0, 0, 0, 0, 0, 0};
+    unsigned long long slot_acc[16] = {0};
     long long slot_t0 = clock64();
 #endif
     for (int i = 0; i < n; ++i) {
@@ -328,6 +328,9 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
         // (config 5: 1.98 -> 1.94 s).
         constexpr bool kFast = MODE == CHORDAL_TIE_ASCENDING || MODE == CHORDAL_TIE_DESCENDING;
         const bool pre = kFast && nx >= 0 && nx == gv && gb1 - gb0 <= 32;
+#ifdef SLOT_PROFILE
+        if (__any_sync(CH_FULL, pre)) slot_acc[9] += clock64() - slot_t0;  // wait for the row bounds
+#endif
         int ypre = 0;
         if (pre && lane < (int)(gb1 - gb0))
             ypre = src.fetch(MODE == CHORDAL_TIE_DESCENDING ? gb1 - 1 - lane : gb0 + lane);
@@ -473,6 +476,9 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
                 const int deg = (int)(nb1 - nb0);
                 const int y = pre ? ypre
                                   : (lane < deg ? src.fetch(MODE == CHORDAL_TIE_DESCENDING ? nb1 - 1 - lane : nb0 + lane) : 0);
+#ifdef SLOT_PROFILE
+                if (__reduce_or_sync(CH_FULL, (unsigned)y) != 0xFFFFFFFFu) slot_acc[10] += clock64() - slot_t0;  // list
+#endif
                 const bool alt = hc != c0 && hc != (int)C::NIL;  // head class after x: not x's class
                 long long hh = 0, he = 0;
                 if (alt) {
@@ -481,6 +487,9 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
                 }
                 const int frl = nfree - 1 - lane >= 0 ? (int)M.freel[nfree - 1 - lane] : 0;
                 const int c = lane < deg ? (int)M.cls[y] : (int)C::VISITED;
+#ifdef SLOT_PROFILE
+                if (__reduce_or_sync(CH_FULL, (unsigned)c) != 0xFFFFFFFEu) slot_acc[11] += clock64() - slot_t0;  // classes
+#endif
                 const long long abase = hh & ~(long long)(V - 1);
                 uint4 araw = make_uint4(0, 0, 0, 0);
                 if (alt) araw = *reinterpret_cast<const uint4 *>(M.slot_v + abase + (long long)lane * V);
@@ -490,11 +499,17 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
                 const uint32_t peers = __match_any_sync(CH_FULL, ok ? c : -1) & vm;
                 const bool leader = ok && (peers & lt) == 0;
                 const int cnt = __popc(peers);
+#ifdef SLOT_PROFILE
+                if (__reduce_or_sync(CH_FULL, (unsigned)(cnt)) != 0xFFFFFFF3u) slot_acc[12] += clock64() - slot_t0;
+#endif
                 int live_c = 0, pold = 0;
                 if (leader) {
                     live_c = (int)M.c_live[c];
                     pold = (int)M.c_prev[c];
                 }
+#ifdef SLOT_PROFILE
+                if (__reduce_or_sync(CH_FULL, (unsigned)(live_c + pold)) != 0xFFFFFFF3u) slot_acc[13] += clock64() - slot_t0;
+#endif
                 int acl[V];
                 {
                     const I *av = reinterpret_cast<const I *>(&araw);
@@ -541,13 +556,31 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
                 const uint32_t sm = __ballot_sync(CH_FULL, split);
                 const int d = __shfl_sync(CH_FULL, frl, __popc(sm & lt));
                 const int kk = split ? cnt : 0;
+#ifndef SLOT_SCAN_SHFL
+                // segment offsets: kk <= 32, so six independent bit-plane ballots
+                // give the exclusive prefix and the total (a shorter chain than a
+                // five-round shuffle scan)
+                int excl = 0, ktot = 0;
+#pragma unroll
+                for (int bit = 0; bit < 6; ++bit) {
+                    const uint32_t bm = __ballot_sync(CH_FULL, (kk >> bit) & 1);
+                    excl += __popc(bm & lt) << bit;
+                    ktot += __popc(bm) << bit;
+                }
+                const int incl = excl + kk;
+#else
                 int incl = kk;
 #pragma unroll
                 for (int dd = 1; dd < 32; dd <<= 1) {
                     const int o = __shfl_up_sync(CH_FULL, incl, dd);
                     if (lane >= dd) incl += o;
                 }
-                const long long start = top + incl - kk;
+                const int ktot = __shfl_sync(CH_FULL, incl, 31);
+#endif
+                const int start = (int)top + incl - kk;
+#ifdef SLOT_PROFILE
+                if (__reduce_or_sync(CH_FULL, (unsigned)(start)) != 0xFFFFFFF3u) slot_acc[14] += clock64() - slot_t0;
+#endif
                 if (split) {
                     M.c_head[d] = (S)start;
                     M.c_end[d] = (S)(start + cnt);
@@ -560,20 +593,23 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
                     M.c_prev[c] = (I)d;
                     if (pold != (int)C::NIL) M.c_next[pold] = (I)d;
                 }
-                long long hstart = -1;
+                int hstart = -1;
                 const uint32_t hb = __ballot_sync(CH_FULL, split && c == hc);
                 if (hb) {  // the head class split: its movers' class is the new head
                     const int src_l = __ffs(hb) - 1;
                     chead = __shfl_sync(CH_FULL, d, src_l);
                     hstart = __shfl_sync(CH_FULL, start, src_l);
                 }
-                top += __shfl_sync(CH_FULL, incl, 31);
+                top += ktot;
                 nfree -= __popc(sm);
+#ifdef SLOT_PROFILE
+                if (__reduce_or_sync(CH_FULL, (unsigned)(top + nfree)) != 0xFFFFFFF3u) slot_acc[15] += clock64() - slot_t0;
+#endif
                 nclasses += __popc(sm);
                 // movers of split classes into their new segment, in lane (tie) order
                 const int ls = ok ? __ffs(peers) - 1 : 0;
                 const int dl = __shfl_sync(CH_FULL, d, ls);
-                const long long stl = __shfl_sync(CH_FULL, start, ls);
+                const int stl = __shfl_sync(CH_FULL, start, ls);
                 __syncwarp();  // the candidate-class reads above precede these writes (racecheck)
                 if (ok && ((sm >> ls) & 1u)) {
                     M.slot_v[stl + __popc(peers & lt)] = (I)y;
@@ -771,7 +807,7 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
     }
 #ifdef SLOT_PROFILE
     if (lane == 0)
-        for (int k = 0; k < 10; ++k) atomicAdd(&slot_prof[k], slot_acc[k]);
+        for (int k = 0; k < 16; ++k) atomicAdd(&slot_prof[k], slot_acc[k]);
 #endif
     if (progress && lane == 0) progress[1] = 1;
 }

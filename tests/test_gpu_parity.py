@@ -640,7 +640,8 @@ def test_new_orderings_edge_cases():
 
 
 @pytest.mark.gpu
-def test_csr_global_engine_tie_rules_and_components():
+@pytest.mark.parametrize("n", [8000, 40000])
+def test_csr_global_engine_tie_rules_and_components(n):
     """The global-memory slot engine (CSR, n > 32768) with its <= 32-neighbour fast
     step: LOWEST_INDEX against the oracle's PartitionList, and the descending rule
     through the relabelling v -> n - v (v >= 1) that turns it into LOWEST_INDEX
@@ -649,13 +650,14 @@ def test_csr_global_engine_tie_rules_and_components():
     from paper_1508_06329_b200.csr import CSRGraph
     from paper_1508_06329_b200.generate import chordal_random_edges
 
+    # n = 8000: the all-in-shared-memory slot kernel (u16 slots, compaction runs:
+    # its slot array holds fewer than n + m slots); n = 40000: the global-memory one
     rng = np.random.default_rng(1508)
-    n = 40000
     cases = []
     u, v = chordal_random_edges(n, 6, 11)
     cases.append(("chordal", u, v))
-    a = rng.integers(0, n, 30000)
-    b = rng.integers(0, n, 30000)
+    a = rng.integers(0, n, 3 * n // 4)
+    b = rng.integers(0, n, 3 * n // 4)
     keep = a != b
     cases.append(("forest-ish", a[keep], b[keep]))
     hub = np.zeros(5000, dtype=np.int64) + 7  # one vertex with > 32 neighbours among small ones
@@ -673,3 +675,9 @@ def test_csr_global_engine_tie_rules_and_components():
         gr = CSRGraph.from_edges0(n, relabel[pairs[:, 0]], relabel[pairs[:, 1]])
         want_desc = relabel[oracle.lexbfs_partition_csr(gr.indptr, gr.indices, n)]  # f is an involution
         assert o0(P.parallel_lexbfs(g, DESC)) == want_desc.tolist(), name
+        if n <= 16384:  # seeded arbitration against the dense oracle
+            packed = np.zeros((n, (n + 7) // 8), dtype=np.uint8)
+            for x, y in ((pairs[:, 0], pairs[:, 1]), (pairs[:, 1], pairs[:, 0])):
+                np.bitwise_or.at(packed, (x, y >> 3), (1 << (y & 7)).astype(np.uint8))
+            want_arb = oracle.lexbfs_arbitrated(packed, n, oracle.ARB_SEEDED, 3).tolist()
+            assert o0(P.parallel_lexbfs(g, Arbitration.seeded(3))) == want_arb, name

@@ -1,2 +1,3 @@
-bash tools/ab_variants.sh run "c3c c3r c3d c2c c2d" noagg aggf > gpurun_out/r02_ab_aggf.txt 2>&1
-grep -E "^(==|c)|Error" gpurun_out/r02_ab_aggf.txt
+timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "csr or seeded or config5" 2>&1 | tail -3
+timeout 300 python tools/sanitize_driver.py slot
+timeout 300 python tools/c5_time.py

@@ -61,6 +61,16 @@ def part_cta():
 
 
 def part_slot():
+    # 3000 / 8000: all state in shared memory (8000: the slot array compacts);
+    # 20000: shared-memory class ids, global bookkeeping; 40000: global state
+    for n in (8000, 20000):
+        from paper_1508_06329_b200.generate import chordal_random_edges
+
+        u, v = chordal_random_edges(n, 6, 7)
+        g = CSRGraph.from_edges0(n, u, v)
+        check_chordal(g)
+        for arb in (P.Arbitration.fixed_priority("descending"), P.Arbitration.seeded(3)):
+            assert sorted(P.parallel_lexbfs(g, arb).order0.tolist()) == list(range(n))
     for n in (3000, 40000):
         g = CSRGraph.from_dense(gen_chordal_random(n, 6, 7)) if n <= 3000 else None
         if g is None:

@@ -32,7 +32,7 @@ int main(int argc, char **argv) {
     void *ws;
     cudaMalloc(&ws, wsb);
     for (int rep = 0; rep < 2; ++rep) {
-        unsigned long long z[10] = {0};
+        unsigned long long z[16] = {0};
         cudaMemcpyToSymbol(chordal::slot_prof, z, sizeof(z));
         cudaEvent_t a, b;
         cudaEventCreate(&a);
@@ -44,12 +44,12 @@ int main(int argc, char **argv) {
         cudaEventSynchronize(b);
         float ms = 0;
         cudaEventElapsedTime(&ms, a, b);
-        unsigned long long p[10];
+        unsigned long long p[16];
         cudaMemcpyFromSymbol(p, chordal::slot_prof, sizeof(p));
         printf("rc=%d n=%lld %.3f ms (%.1f ns/step) err=%s\n", rc, n, ms, ms * 1e6 / n,
                cudaGetErrorString(cudaGetLastError()));
-        const char *const names[] = {"steps", "pivot", "bounds+pass1", "allocate", "pass2+restore", "touched", "pivot-known", "bounds-ahead", "fast", "-"};
-        for (int k = 0; k < 10; ++k)
+        const char *const names[] = {"steps", "pivot", "bounds+pass1", "allocate", "pass2+restore", "touched", "pivot-known", "bounds-ahead", "fast", "bounds-wait", "list-avail", "cls-avail", "match", "fields", "scan", "alloc-done"};
+        for (int k = 0; k < 16; ++k)
             printf("  %-14s %14llu  %8.1f per step\n", names[k], p[k], (double)p[k] / (double)(p[0] ? p[0] : 1));
     }
     return 0;
