@@ -29,6 +29,7 @@ int launch_dense_fill(const uint8_t *, int64_t, int64_t, const int64_t *, int32_
 int launch_peo_dense_witness(const uint8_t *, int64_t, int64_t, const int32_t *, const uint64_t *,
                              int32_t *, cudaStream_t);
 int launch_permute_dense(const uint8_t *, int64_t, int64_t, const int32_t *, uint8_t *, cudaStream_t);
+int launch_spread_rows(const uint8_t *, int64_t, int64_t, int64_t, int64_t, uint8_t *, cudaStream_t);
 int launch_batch(const uint8_t *, int64_t, int64_t, int64_t, int32_t *, int32_t *, cudaStream_t);
 int launch_mcs_dense(const uint8_t *, int64_t, int64_t, bool, uint64_t, int32_t *, int32_t *, cudaStream_t);
 size_t bfs_csr_workspace_bytes(int64_t);
@@ -287,6 +288,29 @@ int chordal_is_chordal_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, 
                              stream);
 }
 
+// Host rows -> device rows of pitch `stride` with zeroed padding.  Equal pitches:
+// one flat copy.  A narrower host pitch (the reference's ceil(n/8)-byte rows):
+// one flat copy into `staging` (>= n * row_bytes bytes) and a kernel that spreads
+// the rows -- a pitched copy from pageable memory is staged row by row by the
+// driver (0.45 ms at n = 1000, tools/host_call_probe.cu).  A wider host pitch:
+// the pitched copy into pre-zeroed rows.
+static int upload_rows(uint8_t *adj, int64_t stride, const uint8_t *adj_host, int64_t row_bytes, int64_t n,
+                       uint8_t *staging, cudaStream_t s) {
+    const int64_t nb = (n + 7) / 8;
+    if (row_bytes == stride && stride == nb)
+        return cudaMemcpyAsync(adj, adj_host, (size_t)n * stride, cudaMemcpyHostToDevice, s) == cudaSuccess
+                   ? CHORDAL_OK : CHORDAL_ECUDA;
+    if (row_bytes <= stride && staging) {
+        if (cudaMemcpyAsync(staging, adj_host, (size_t)n * row_bytes, cudaMemcpyHostToDevice, s) != cudaSuccess)
+            return CHORDAL_ECUDA;
+        return launch_spread_rows(staging, row_bytes, n, nb, stride, adj, s);
+    }
+    if (cudaMemsetAsync(adj, 0, (size_t)n * stride, s) != cudaSuccess ||
+        cudaMemcpy2DAsync(adj, stride, adj_host, row_bytes, nb, n, cudaMemcpyHostToDevice, s) != cudaSuccess)
+        return CHORDAL_ECUDA;
+    return CHORDAL_OK;
+}
+
 int chordal_is_chordal_dense_host(const uint8_t *adj_host, int64_t n, int64_t row_bytes,
                                   int32_t tie_rule, uint64_t seed, int32_t *order_host,
                                   int32_t *witness_host, int32_t *chordal_out) {
@@ -307,15 +331,16 @@ int chordal_is_chordal_dense_host(const uint8_t *adj_host, int64_t n, int64_t ro
     int rc = CHORDAL_OK;
     int64_t m = -1;
     do {
-        if (cudaMallocAsync((void **)&adj, adj_bytes + sizeof(int32_t) * (2 * n + 4), s) != cudaSuccess) {
+        // staging for a narrower host pitch (the rows are spread on the device)
+        const size_t stage_bytes = row_bytes <= stride ? (((size_t)n * row_bytes + 255) & ~size_t(255)) : 0;
+        const size_t ord_bytes = (sizeof(int32_t) * (size_t)(2 * n + 4) + 255) & ~size_t(255);
+        if (cudaMallocAsync((void **)&adj, adj_bytes + ord_bytes + stage_bytes, s) != cudaSuccess) {
             rc = CHORDAL_ENOMEM;
             break;
         }
         order = reinterpret_cast<int32_t *>(adj + adj_bytes);
-        // the copy writes (n+7)/8 bytes per row: the rest of the pitch must be zero
-        if (stride != (n + 7) / 8 && cudaMemsetAsync(adj, 0, adj_bytes, s) != cudaSuccess) { rc = CHORDAL_ECUDA; break; }
-        if (cudaMemcpy2DAsync(adj, stride, adj_host, row_bytes, (n + 7) / 8, n, cudaMemcpyHostToDevice, s) !=
-            cudaSuccess) { rc = CHORDAL_ECUDA; break; }
+        rc = upload_rows(adj, stride, adj_host, row_bytes, n, stage_bytes ? adj + adj_bytes + ord_bytes : nullptr, s);
+        if (rc) break;
         if (n > 1024) {  // the engine choice (CSR route) and its thread count depend on the density
             rc = count_edges_sync(adj, n, stride, s, &m);
             if (rc) break;
@@ -344,7 +369,9 @@ size_t chordal_dense_host_workspace_bytes(int64_t n, int64_t m) {
     const int64_t stride = (((n + 7) / 8) + 15) / 16 * 16;
     const size_t adj_bytes = ((size_t)n * stride + 255) & ~size_t(255);
     const size_t ord_bytes = (sizeof(int32_t) * (size_t)(2 * n + 4) + 255) & ~size_t(255);
-    return adj_bytes + ord_bytes + ((DenseWs(n, m < 0 ? 0 : m).total + 255) & ~size_t(255)) + 256;
+    // + staging for host rows narrower than the device pitch (upload_rows)
+    const size_t stage_bytes = stride != (n + 7) / 8 ? adj_bytes : 0;
+    return adj_bytes + ord_bytes + ((DenseWs(n, m < 0 ? 0 : m).total + 255) & ~size_t(255)) + 256 + stage_bytes;
 }
 
 int chordal_is_chordal_dense_host_ws(const uint8_t *adj_host, int64_t n, int64_t row_bytes, int64_t m,
@@ -372,10 +399,9 @@ int chordal_is_chordal_dense_host_ws(const uint8_t *adj_host, int64_t n, int64_t
     cudaStream_t s = cudaStreamPerThread;
     int rc = CHORDAL_OK;
     do {
-        // the copy writes (n+7)/8 bytes per row: the rest of the pitch must be zero
-        if (stride != (n + 7) / 8 && cudaMemsetAsync(adj, 0, adj_bytes, s) != cudaSuccess) { rc = CHORDAL_ECUDA; break; }
-        if (cudaMemcpy2DAsync(adj, stride, adj_host, row_bytes, (n + 7) / 8, n, cudaMemcpyHostToDevice, s) !=
-            cudaSuccess) { rc = CHORDAL_ECUDA; break; }
+        uint8_t *staging = stride != (n + 7) / 8 ? reinterpret_cast<uint8_t *>(wit) + 256 : nullptr;
+        rc = upload_rows(adj, stride, adj_host, row_bytes, n, staging, s);
+        if (rc) break;
         rc = chordal_is_chordal_dense(adj, n, stride, m, tie_rule, seed, order, order + n, ws, wsb, wit, s);
         if (rc) break;
         if (cudaMemcpyAsync(order_host, order, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, s) != cudaSuccess ||
@@ -545,7 +571,9 @@ int chordal_is_chordal_batch(const uint8_t *adj_dev, int64_t batch, int64_t n, i
 
 static size_t batch_host_set_bytes(int64_t n, int64_t chunk) {
     const int64_t stride = (((n + 7) / 8) + 15) / 16 * 16;
-    return ((size_t)n * stride * chunk + sizeof(int32_t) * (size_t)(n + 3) * chunk + 1023) & ~size_t(255);
+    // + staging for host rows narrower than the device pitch (spread on the device)
+    const size_t stage = stride != (n + 7) / 8 ? (((size_t)n * stride * chunk + 255) & ~size_t(255)) : 0;
+    return ((size_t)n * stride * chunk + sizeof(int32_t) * (size_t)(n + 3) * chunk + 1023 + stage) & ~size_t(255);
 }
 
 size_t chordal_batch_host_workspace_bytes(int64_t n, int64_t chunk) {
@@ -570,6 +598,10 @@ static int batch_host_run(const uint8_t *adj_host, int64_t batch, int64_t n, int
     uint8_t *buf[NB] = {};
     int32_t *ord[NB] = {};
     int32_t *wit[NB] = {};
+    uint8_t *stg[NB] = {};
+    // narrower host rows: one flat copy per chunk and a spread kernel (a pitched
+    // copy from pageable memory is staged row by row by the driver)
+    const bool spread = !flat && row_bytes <= stride && stride != (n + 7) / 8;
     int rc = CHORDAL_OK;
     if (cudaEventCreateWithFlags(&ready, cudaEventDisableTiming) != cudaSuccess ||
         cudaEventRecord(ready, home) != cudaSuccess)
@@ -579,23 +611,27 @@ static int batch_host_run(const uint8_t *adj_host, int64_t batch, int64_t n, int
         buf[k] = base;
         ord[k] = reinterpret_cast<int32_t *>(base + ((gbytes * chunk + 255) & ~size_t(255)));
         wit[k] = ord[k] + (size_t)n * chunk;
+        stg[k] = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(wit[k] + 3 * chunk) + 255) & ~uintptr_t(255));
         if (cudaStreamCreateWithFlags(&st[k], cudaStreamNonBlocking) != cudaSuccess ||
             cudaStreamWaitEvent(st[k], ready, 0) != cudaSuccess) {
             rc = CHORDAL_ECUDA;
             break;
         }
-        if (!flat && cudaMemsetAsync(buf[k], 0, gbytes * chunk, st[k]) != cudaSuccess)
+        if (!flat && !spread && cudaMemsetAsync(buf[k], 0, gbytes * chunk, st[k]) != cudaSuccess)
             rc = CHORDAL_ECUDA;
     }
     for (int64_t b0 = 0, c = 0; b0 < batch && rc == CHORDAL_OK; b0 += chunk, ++c) {
         const int k = (int)(c % NB);
         const int64_t nb = (batch - b0 < chunk) ? batch - b0 : chunk;
         const uint8_t *src = adj_host + b0 * n * row_bytes;
-        cudaError_t e = flat
-                            ? cudaMemcpyAsync(buf[k], src, gbytes * nb, cudaMemcpyHostToDevice, st[k])
-                            : cudaMemcpy2DAsync(buf[k], stride, src, row_bytes, (n + 7) / 8, n * nb,
-                                                cudaMemcpyHostToDevice, st[k]);
+        cudaError_t e = flat     ? cudaMemcpyAsync(buf[k], src, gbytes * nb, cudaMemcpyHostToDevice, st[k])
+                        : spread ? cudaMemcpyAsync(stg[k], src, (size_t)n * nb * row_bytes, cudaMemcpyHostToDevice,
+                                                   st[k])
+                                 : cudaMemcpy2DAsync(buf[k], stride, src, row_bytes, (n + 7) / 8, n * nb,
+                                                     cudaMemcpyHostToDevice, st[k]);
         if (e != cudaSuccess) { rc = CHORDAL_ECUDA; break; }
+        if (spread && (rc = launch_spread_rows(stg[k], row_bytes, n * nb, (n + 7) / 8, stride, buf[k], st[k])))
+            break;
         rc = launch_batch(buf[k], nb, n, stride, ord[k], wit[k], st[k]);
         if (rc) break;
         if (cudaMemcpyAsync(orders_host + b0 * n, ord[k], sizeof(int32_t) * n * nb, cudaMemcpyDeviceToHost,

@@ -27,16 +27,18 @@ def test_dense_host_ws_padded_rows_over_dirty_workspace():
     """row_bytes = 16 for n = 100 (ceil(n/8) = 13, device pitch 16): the pitch
     padding must be zeroed even though row_bytes == pitch; the workspace is
     pre-filled with 0xFF so stale bytes would show up as edges to vertices >= n."""
-    for g in (gen_chordal_random(100, 4, 1), remove_first_chord(gen_chordal_random(100, 4, 1))[0]):
+    cases = [(g, pitch) for g in (gen_chordal_random(100, 4, 1), remove_first_chord(gen_chordal_random(100, 4, 1))[0])
+             for pitch in (16, 40)]  # 16: flat copy + device spread; 40 > device pitch: pitched copy
+    for g, pitch in cases:
         n = g.n
-        host = np.full((n, 16), 0xFF, dtype=np.uint8)  # host pad bytes dirty too: never read
+        host = np.full((n, pitch), 0xFF, dtype=np.uint8)  # host pad bytes dirty too: never read
         host[:, :13] = g._packed
         wsb = int(_native.lib.chordal_dense_host_workspace_bytes(n, g.m))
         ws, wp = _aligned_ws(wsb, 0xFF)
         order = np.empty(n, dtype=np.int32)
         wit = np.empty(3, dtype=np.int32)
         flag = ctypes.c_int32(-1)
-        rc = _native.lib.chordal_is_chordal_dense_host_ws(host.ctypes.data, n, 16, g.m, 0, 0, order.ctypes.data,
+        rc = _native.lib.chordal_is_chordal_dense_host_ws(host.ctypes.data, n, pitch, g.m, 0, 0, order.ctypes.data,
                                                           wit.ctypes.data, ctypes.byref(flag), wp, wsb)
         assert rc == 0
         ok, o, w = oracle.is_chordal(np.ascontiguousarray(g._packed), n)
@@ -45,7 +47,7 @@ def test_dense_host_ws_padded_rows_over_dirty_workspace():
         # the per-call form over pool memory
         order2 = np.empty(n, dtype=np.int32)
         wit2 = np.empty(3, dtype=np.int32)
-        rc = _native.lib.chordal_is_chordal_dense_host(host.ctypes.data, n, 16, 0, 0, order2.ctypes.data,
+        rc = _native.lib.chordal_is_chordal_dense_host(host.ctypes.data, n, pitch, 0, 0, order2.ctypes.data,
                                                        wit2.ctypes.data, ctypes.byref(flag))
         assert rc == 0 and order2.tolist() == o.tolist() and wit2.tolist() == wit.tolist()
 
@@ -55,21 +57,22 @@ def test_batch_host_padded_rows_dirty_host_padding():
     pad bytes, over a dirty workspace: only the vertex bytes are copied."""
     gs = [gen_chordal_random(100, 4, s) if s % 3 else remove_first_chord(gen_chordal_random(100, 4, s))[0]
           for s in range(9)]
-    host = np.full((9, 100, 16), 0xFF, dtype=np.uint8)
-    for b, g in enumerate(gs):
-        host[b, :, :13] = g._packed
-    clean = np.ascontiguousarray(host[:, :, :13])
-    want_v, want_o, want_w = oracle.is_chordal_batch(clean, 100)
-    wsb = int(_native.lib.chordal_batch_host_workspace_bytes(100, 4))
-    ws, wp = _aligned_ws(wsb, 0xFF)
-    orders = np.empty((9, 100), dtype=np.int32)
-    wit = np.empty((9, 3), dtype=np.int32)
-    assert _native.lib.chordal_is_chordal_batch_host_ws(host.ctypes.data, 9, 100, 16, orders.ctypes.data,
-                                                        wit.ctypes.data, 4, wp, wsb) == 0
-    assert (orders == want_o).all() and (wit == want_w).all()
-    assert _native.lib.chordal_is_chordal_batch_host(host.ctypes.data, 9, 100, 16, orders.ctypes.data,
-                                                     wit.ctypes.data, 4) == 0
-    assert (orders == want_o).all() and (wit == want_w).all()
+    for pitch in (13, 16, 40):  # 13 / 16: flat copy + device spread; 40 > device pitch: pitched copy
+        host = np.full((9, 100, pitch), 0xFF, dtype=np.uint8)
+        for b, g in enumerate(gs):
+            host[b, :, :13] = g._packed
+        clean = np.ascontiguousarray(host[:, :, :13])
+        want_v, want_o, want_w = oracle.is_chordal_batch(clean, 100)
+        wsb = int(_native.lib.chordal_batch_host_workspace_bytes(100, 4))
+        ws, wp = _aligned_ws(wsb, 0xFF)
+        orders = np.empty((9, 100), dtype=np.int32)
+        wit = np.empty((9, 3), dtype=np.int32)
+        assert _native.lib.chordal_is_chordal_batch_host_ws(host.ctypes.data, 9, 100, pitch, orders.ctypes.data,
+                                                            wit.ctypes.data, 4, wp, wsb) == 0
+        assert (orders == want_o).all() and (wit == want_w).all()
+        assert _native.lib.chordal_is_chordal_batch_host(host.ctypes.data, 9, 100, pitch, orders.ctypes.data,
+                                                         wit.ctypes.data, 4) == 0
+        assert (orders == want_o).all() and (wit == want_w).all()
 
 
 def test_empty_graphs_in_batches_are_chordal():

@@ -1,3 +1,1 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "csr or seeded or config5" 2>&1 | tail -3
-timeout 300 python tools/sanitize_driver.py slot
-timeout 300 python tools/c5_time.py
+timeout 900 python -m pytest tests/test_gpu_abi_edges.py tests/test_gpu_parity.py -m gpu -q -x -k "host or padded or reference_graph or batch" 2>&1 | tail -3
