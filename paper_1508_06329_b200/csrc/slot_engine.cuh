@@ -452,15 +452,50 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
             src.bounds(x, nb0, nb1);
         }
         const int hc = chead;  // head class before this step's splits
-        int ccl[V];
-        if (kTrack) {
-            const I *cv = reinterpret_cast<const I *>(&cand_raw);
-#pragma unroll
-            for (int j = 0; j < V; ++j) {  // only slots inside x's segment hold valid ids
-                const long long sj = cand_base + (long long)lane * V + j;
-                ccl[j] = (sj > xs && sj < e0) ? (int)M.cls[(int)cv[j]] : -1;
-            }
+        // The next-pivot window: the head class after x's removal -- x's class
+        // (the slots after x, fetched with x) or, when x emptied it, the next
+        // class from its segment start -- and the class ids of its 32 * V slots,
+        // read once for both the fast step and the general path.  Bounds are
+        // lane-relative, so each slot costs 32-bit compares only.
+        const bool alt = hc != c0 && hc != (int)C::NIL;  // head class after x: not x's class
+        long long wb = cand_base, wlo = xs + 1, whi = e0;
+        uint4 wraw = cand_raw;
+        if (kTrack && alt) {
+            wlo = (long long)M.c_head[hc];
+            whi = (long long)M.c_end[hc];
+            wb = wlo & ~(long long)(V - 1);
+            wraw = *reinterpret_cast<const uint4 *>(M.slot_v + wb + (long long)lane * V);
         }
+        int wcl[V];  // class of each window slot inside [wlo, whi), else -1
+        if (kTrack) {
+            const long long l0 = wb + (long long)lane * V;
+            const int rlo = (int)(wlo - l0 < 0 ? 0 : (wlo - l0 > V ? V : wlo - l0));
+            const int rhi = (int)(whi - l0 < 0 ? 0 : (whi - l0 > V ? V : whi - l0));
+            const I *cv = reinterpret_cast<const I *>(&wraw);
+#pragma unroll
+            for (int j = 0; j < V; ++j) wcl[j] = (j >= rlo && j < rhi) ? (int)M.cls[(int)cv[j]] : -1;
+        }
+        // the head class's first live slot in the window (its classes as read
+        // before this step's moves: a head class that loses members to a split
+        // gets a new segment and its first mover is the next pivot instead)
+        auto window_first = [&](int &gv_out, long long &gs_out) {
+            const I *cv = reinterpret_cast<const I *>(&wraw);
+            int fj = V, fv = -1;
+#pragma unroll
+            for (int j = V - 1; j >= 0; --j)
+                if (wcl[j] == hc) {
+                    fj = j;
+                    fv = (int)cv[j];
+                }
+            const uint32_t gm = __ballot_sync(CH_FULL, fj < V);
+            gv_out = -1;
+            gs_out = -1;
+            if (gm) {
+                const int src_l = __ffs(gm) - 1;
+                gv_out = __shfl_sync(CH_FULL, fv, src_l);
+                gs_out = wb + (long long)src_l * V + __shfl_sync(CH_FULL, fj, src_l);
+            }
+        };
         // ---- fast step: at most 32 neighbours (97 % of the configuration-5 steps) --
         // One chunk holds every mover of the step, so a class's group in the
         // chunk is its whole move set: counts come from __match_any_sync, each
@@ -479,21 +514,21 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
 #ifdef SLOT_PROFILE
                 if (__reduce_or_sync(CH_FULL, (unsigned)y) != 0xFFFFFFFFu) slot_acc[10] += clock64() - slot_t0;  // list
 #endif
-                const bool alt = hc != c0 && hc != (int)C::NIL;  // head class after x: not x's class
-                long long hh = 0, he = 0;
-                if (alt) {
-                    hh = (long long)M.c_head[hc];
-                    he = (long long)M.c_end[hc];
-                }
                 const int frl = nfree - 1 - lane >= 0 ? (int)M.freel[nfree - 1 - lane] : 0;
                 const int c = lane < deg ? (int)M.cls[y] : (int)C::VISITED;
 #ifdef SLOT_PROFILE
                 if (__reduce_or_sync(CH_FULL, (unsigned)c) != 0xFFFFFFFEu) slot_acc[11] += clock64() - slot_t0;  // classes
 #endif
-                const long long abase = hh & ~(long long)(V - 1);
-                uint4 araw = make_uint4(0, 0, 0, 0);
-                if (alt) araw = *reinterpret_cast<const uint4 *>(M.slot_v + abase + (long long)lane * V);
                 const bool ok = c != (int)C::VISITED;
+                // every mover reads its class's fields (same address within a
+                // group: one broadcast), so the reads do not wait for the grouping
+#ifndef SLOT_LEADER_FIELDS
+                int live_c = 0, pold = 0;
+                if (ok) {
+                    live_c = (int)M.c_live[c];
+                    pold = (int)M.c_prev[c];
+                }
+#endif
                 if (ok && parent) parent[y] = (O)x;
                 const uint32_t vm = __ballot_sync(CH_FULL, ok);
                 const uint32_t peers = __match_any_sync(CH_FULL, ok ? c : -1) & vm;
@@ -502,55 +537,23 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
 #ifdef SLOT_PROFILE
                 if (__reduce_or_sync(CH_FULL, (unsigned)(cnt)) != 0xFFFFFFF3u) slot_acc[12] += clock64() - slot_t0;
 #endif
+#ifdef SLOT_LEADER_FIELDS
                 int live_c = 0, pold = 0;
                 if (leader) {
                     live_c = (int)M.c_live[c];
                     pold = (int)M.c_prev[c];
                 }
+#endif
 #ifdef SLOT_PROFILE
                 if (__reduce_or_sync(CH_FULL, (unsigned)(live_c + pold)) != 0xFFFFFFF3u) slot_acc[13] += clock64() - slot_t0;
 #endif
-                int acl[V];
-                {
-                    const I *av = reinterpret_cast<const I *>(&araw);
-#pragma unroll
-                    for (int j = 0; j < V; ++j) {
-                        const long long sj = abase + (long long)lane * V + j;
-                        acl[j] = (alt && sj >= hh && sj < he) ? (int)M.cls[(int)av[j]] : -1;
-                    }
-                }
                 int hmv = ok && c == hc ? y : (MODE == CHORDAL_TIE_DESCENDING ? -1 : 0x7FFFFFFF);
                 const int hmf = MODE == CHORDAL_TIE_DESCENDING ? __reduce_max_sync(CH_FULL, hmv)
                                                                : (int)__reduce_min_sync(CH_FULL, (unsigned)hmv);
-                // next pivot if the head class keeps its segment: its first live
-                // slot after x (x's class) or its first live slot (the next class)
-                auto first_in_window = [&](const uint4 &raw, long long wb, const int *cl, int want, long long lo,
-                                           long long hi, int &gv_out, long long &gs_out) {
-                    const I *cv = reinterpret_cast<const I *>(&raw);
-                    int fj = V, fv = -1;
-#pragma unroll
-                    for (int j = V - 1; j >= 0; --j) {
-                        const long long sj = wb + (long long)lane * V + j;
-                        if (sj >= lo && sj < hi && cl[j] == want) {
-                            fj = j;
-                            fv = (int)cv[j];
-                        }
-                    }
-                    const uint32_t gm = __ballot_sync(CH_FULL, fj < V);
-                    gv_out = -1;
-                    gs_out = -1;
-                    if (gm) {
-                        const int src_l = __ffs(gm) - 1;
-                        gv_out = __shfl_sync(CH_FULL, fv, src_l);
-                        gs_out = wb + (long long)src_l * V + __shfl_sync(CH_FULL, fj, src_l);
-                    }
-                };
+                // next pivot if the head class keeps its segment
                 int guess = -1;
                 long long gslot = -1;
-                if (alt)
-                    first_in_window(araw, abase, acl, hc, hh, he, guess, gslot);
-                else
-                    first_in_window(cand_raw, cand_base, ccl, c0, xs + 1, e0, guess, gslot);
+                window_first(guess, gslot);
                 // new classes: one per split group, segments laid out in lane order
                 const bool split = leader && cnt != live_c;
                 const uint32_t sm = __ballot_sync(CH_FULL, split);
@@ -650,22 +653,7 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
         int guess = -1;
         long long gslot = -1;
         if (kTrack) {
-            const I *cv = reinterpret_cast<const I *>(&cand_raw);
-            int fj = V, fv = -1;
-#pragma unroll
-            for (int j = V - 1; j >= 0; --j) {
-                const long long sj = cand_base + (long long)lane * V + j;
-                if (hc == c0 && sj > xs && sj < e0 && ccl[j] == c0) {
-                    fj = j;
-                    fv = (int)cv[j];
-                }
-            }
-            const uint32_t gm = __ballot_sync(CH_FULL, fj < V);
-            if (gm) {
-                const int src_l = __ffs(gm) - 1;
-                guess = __shfl_sync(CH_FULL, fv, src_l);
-                gslot = cand_base + (long long)src_l * V + __shfl_sync(CH_FULL, fj, src_l);
-            }
+            window_first(guess, gslot);
             hm = MODE == CHORDAL_TIE_DESCENDING ? __reduce_max_sync(CH_FULL, hm)
                                                 : (int)__reduce_min_sync(CH_FULL, (unsigned)hm);
         }
