@@ -311,6 +311,7 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
     constexpr bool kTrack = MODE == CHORDAL_TIE_ASCENDING || MODE == CHORDAL_TIE_DESCENDING ||
                             MODE == CHORDAL_TIE_SEEDED_PARTITION;
     constexpr int V = 16 / sizeof(I);
+    constexpr bool kProbeWin = sizeof(I) == 2;  // next-pivot candidates: 32-slot probe (u16) or wide window
     int nx = -1;
     long long nxs = -1;
 
@@ -393,11 +394,21 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
             xs = slot_detail::first_live<I, S>(M, c0, (long long)M.c_head[c0], e0, &x);
         }
         if (x < 0) x = (int)M.slot_v[xs];
-        // the slots after x in its class: candidates for the next pivot (their
-        // classes are fetched before pass 1 and tested after it)
+        // the 32 slots after x (bounded by x's segment later): candidates for
+        // the next pivot, and their classes (slots below `top` all hold vertices)
+        // (u16 state -- shared memory -- probes 32 slots, one per lane; int32
+        // state in global memory reads a 32 * V-slot window with 16-byte loads:
+        // its classes are fragmented by dead slots, and the probe measured
+        // slower there: configuration 5 1.46 -> 1.65 s, CSR n = 8192 8.38 ->
+        // 7.21 ms with it)
+        int pA = -1, pclA = -1;
+        if (kTrack && kProbeWin && xs + 1 + lane < top) {
+            pA = (int)M.slot_v[xs + 1 + lane];
+            pclA = (int)M.cls[pA];
+        }
         const long long cand_base = (xs + 1) & ~(long long)(V - 1);
         uint4 cand_raw = make_uint4(0, 0, 0, 0);
-        if (kTrack) cand_raw = *reinterpret_cast<const uint4 *>(M.slot_v + cand_base + (long long)lane * V);
+        if (kTrack && !kProbeWin) cand_raw = *reinterpret_cast<const uint4 *>(M.slot_v + cand_base + (long long)lane * V);
         __syncwarp();
         if (lane == 0) {
             if ((MODE != CHORDAL_TIE_SEEDED_ARB && MODE != CHORDAL_TIE_SEEDED_LABELS) || xs == (long long)M.c_head[c0])
@@ -452,25 +463,70 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
             src.bounds(x, nb0, nb1);
         }
         const int hc = chead;  // head class before this step's splits
-        // The next-pivot window: the head class after x's removal -- x's class
-        // (the slots after x, fetched with x) or, when x emptied it, the next
-        // class from its segment start -- and the class ids of its 32 * V slots,
-        // read once for both the fast step and the general path.  Bounds are
-        // lane-relative, so each slot costs 32-bit compares only.
+        // The next-pivot candidates: the head class after x's removal -- x's
+        // class (the 32 slots after x, read with x) or, when x emptied it, the
+        // next class (the first 32 slots of its segment) -- with their classes,
+        // read once for the fast step and the general path.
         const bool alt = hc != c0 && hc != (int)C::NIL;  // head class after x: not x's class
-        long long wb = cand_base, wlo = xs + 1, whi = e0;
-        uint4 wraw = cand_raw;
-        if (kTrack && alt) {
+        long long wlo = xs + 1, whi = e0;
+        int pv = pA, pcl = xs + 1 + lane < e0 ? pclA : -1;
+        if (kTrack && kProbeWin && alt) {
             wlo = (long long)M.c_head[hc];
             whi = (long long)M.c_end[hc];
-            wb = wlo & ~(long long)(V - 1);
+            pv = pcl = -1;
+            if (wlo + lane < whi) {
+                pv = (int)M.slot_v[wlo + lane];
+                pcl = (int)M.cls[pv];
+            }
+        }
+        // the head class's first live slot (its classes as read before this
+        // step's moves: a head class that loses members to a split gets a new
+        // segment and its first mover is the next pivot instead)
+        auto window_probe = [&](int &gv_out, long long &gs_out) {
+            gv_out = -1;
+            gs_out = -1;
+            const uint32_t gm = __ballot_sync(CH_FULL, pcl == hc);
+            if (gm) {
+                const int src_l = __ffs(gm) - 1;
+                gv_out = __shfl_sync(CH_FULL, pv, src_l);
+                gs_out = wlo + src_l;
+                return;
+            }
+            // none of the first 32 is live: the 32 * V slots behind them
+            const long long wb = (wlo + 32) & ~(long long)(V - 1), l0 = wb + (long long)lane * V;
+            const uint4 raw = *reinterpret_cast<const uint4 *>(M.slot_v + l0);
+            const int rlo = (int)(wlo - l0 < 0 ? 0 : (wlo - l0 > V ? V : wlo - l0));
+            const int rhi = (int)(whi - l0 < 0 ? 0 : (whi - l0 > V ? V : whi - l0));
+            const I *cv = reinterpret_cast<const I *>(&raw);
+            int fj = V, fv = -1;
+#pragma unroll
+            for (int j = V - 1; j >= 0; --j)
+                if (j >= rlo && j < rhi && (int)M.cls[(int)cv[j]] == hc) {
+                    fj = j;
+                    fv = (int)cv[j];
+                }
+            const uint32_t gm2 = __ballot_sync(CH_FULL, fj < V);
+            if (gm2) {
+                const int src_l = __ffs(gm2) - 1;
+                gv_out = __shfl_sync(CH_FULL, fv, src_l);
+                gs_out = wb + (long long)src_l * V + __shfl_sync(CH_FULL, fj, src_l);
+            }
+        };
+        // int32 state: the same candidates as a 32 * V-slot window (16-byte
+        // loads), bounds lane-relative so each slot costs 32-bit compares only.
+        long long wb = cand_base, wlo2 = xs + 1, whi2 = e0;
+        uint4 wraw = cand_raw;
+        if (kTrack && !kProbeWin && alt) {
+            wlo2 = (long long)M.c_head[hc];
+            whi2 = (long long)M.c_end[hc];
+            wb = wlo2 & ~(long long)(V - 1);
             wraw = *reinterpret_cast<const uint4 *>(M.slot_v + wb + (long long)lane * V);
         }
         int wcl[V];  // class of each window slot inside [wlo, whi), else -1
-        if (kTrack) {
+        if (kTrack && !kProbeWin) {
             const long long l0 = wb + (long long)lane * V;
-            const int rlo = (int)(wlo - l0 < 0 ? 0 : (wlo - l0 > V ? V : wlo - l0));
-            const int rhi = (int)(whi - l0 < 0 ? 0 : (whi - l0 > V ? V : whi - l0));
+            const int rlo = (int)(wlo2 - l0 < 0 ? 0 : (wlo2 - l0 > V ? V : wlo2 - l0));
+            const int rhi = (int)(whi2 - l0 < 0 ? 0 : (whi2 - l0 > V ? V : whi2 - l0));
             const I *cv = reinterpret_cast<const I *>(&wraw);
 #pragma unroll
             for (int j = 0; j < V; ++j) wcl[j] = (j >= rlo && j < rhi) ? (int)M.cls[(int)cv[j]] : -1;
@@ -478,7 +534,7 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
         // the head class's first live slot in the window (its classes as read
         // before this step's moves: a head class that loses members to a split
         // gets a new segment and its first mover is the next pivot instead)
-        auto window_first = [&](int &gv_out, long long &gs_out) {
+        auto window_wide = [&](int &gv_out, long long &gs_out) {
             const I *cv = reinterpret_cast<const I *>(&wraw);
             int fj = V, fv = -1;
 #pragma unroll
@@ -495,6 +551,12 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
                 gv_out = __shfl_sync(CH_FULL, fv, src_l);
                 gs_out = wb + (long long)src_l * V + __shfl_sync(CH_FULL, fj, src_l);
             }
+        };
+        auto window_first = [&](int &gv_out, long long &gs_out) {
+            if constexpr (kProbeWin)
+                window_probe(gv_out, gs_out);
+            else
+                window_wide(gv_out, gs_out);
         };
         // ---- fast step: at most 32 neighbours (97 % of the configuration-5 steps) --
         // One chunk holds every mover of the step, so a class's group in the
