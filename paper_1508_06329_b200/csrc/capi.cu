@@ -106,8 +106,13 @@ const char *chordal_strerror(int status) {
 // Engine choice for a dense-stored graph: n <= 32768 runs the single-CTA
 // touched-segment arrangement kernel (lexbfs_seg.cu, state in shared memory,
 // O(deg/32 + movers + split classes) per step, any density); larger graphs are
-// converted to CSR on the device and run the slot engine.
-static bool use_seg(int64_t n) { return n <= CHORDAL_DENSE_LEXBFS_MAX_N; }
+// converted to CSR on the device and run the slot engine -- and so do sparse
+// graphs (known m, average degree <= 20) with 1024 < n <= 8836, whose slot
+// engine keeps all its state in shared memory: 0.78-0.92x the CTA engine's time
+// including the conversion (tools/engine_cross.py; configuration 2 chordal
+// 7.98 -> 7.25 + 0.1 ms), while at average degree >= 40 it is 1.1-1.3x slower.
+static bool small_sparse(int64_t n, int64_t m) { return n > 1024 && n <= 8836 && m > 0 && 2 * m <= 20 * n; }
+static bool use_seg(int64_t n, int64_t m) { return n <= CHORDAL_DENSE_LEXBFS_MAX_N && !small_sparse(n, m); }
 
 struct DenseWs {  // workspace carve-up (bytes) of the dense entry points
     size_t key, parent, indptr, indices, slot, total;
@@ -117,7 +122,7 @@ struct DenseWs {  // workspace carve-up (bytes) of the dense entry points
         key = o; o = a(o + 16);
         parent = o; o = a(o + sizeof(int32_t) * (size_t)n);
         indptr = indices = slot = o;
-        if (!use_seg(n)) {
+        if (!use_seg(n, m)) {
             indptr = o; o = a(o + sizeof(int64_t) * (size_t)(n + 1));
             indices = o; o = a(o + sizeof(int32_t) * (size_t)(2 * m + 1));
             slot = o; o = a(o + csr_workspace_bytes(n, m));
@@ -166,7 +171,7 @@ int chordal_lexbfs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int6
     if (tie_rule < 0 || tie_rule > 2) return CHORDAL_EINVAL;
     cudaStream_t s = as_stream(stream);
     const uint64_t cell = current_cell(crc32_str("current"));
-    if (use_seg(n))
+    if (use_seg(n, m))
         return launch_lexbfs_seg(adj_dev, n, stride, m, tie_rule, seed, cell, order_dev, pos_dev, parent_dev, s);
     if (m < 0) {
         rc = count_edges_sync(adj_dev, n, stride, s, &m);
@@ -264,7 +269,7 @@ int chordal_is_chordal_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, 
                              uint64_t seed, int32_t *order_dev, int32_t *pos_dev, void *ws, size_t ws_bytes,
                              int32_t *witness_dev, void *stream) {
     cudaStream_t s = as_stream(stream);
-    if (n > 0 && m < 0 && !use_seg(n)) {
+    if (n > 0 && m < 0 && !use_seg(n, m)) {
         int rc0 = check_dense(adj_dev, n, stride);
         if (rc0) return rc0;
         rc0 = count_edges_sync(adj_dev, n, stride, s, &m);
@@ -280,7 +285,7 @@ int chordal_is_chordal_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, 
     // engine (n > 32768) keeps recording them.
     // The one-warp engine (n <= 1024) records them in shared memory and copies
     // them out with the order.
-    int32_t *parent = (use_seg(n) && n > 1024) ? nullptr : reinterpret_cast<int32_t *>(w + L.parent);
+    int32_t *parent = (use_seg(n, m) && n > 1024) ? nullptr : reinterpret_cast<int32_t *>(w + L.parent);
     int rc = chordal_lexbfs_dense(adj_dev, n, stride, m, tie_rule, seed, order_dev, pos_dev, parent, ws, ws_bytes,
                                   stream);
     if (rc) return rc;
@@ -847,7 +852,7 @@ int chordal_is_chordal_dense_nccl(const uint8_t *adj_dev, int64_t n, int64_t str
     if (n == 0) return cudaMemsetAsync(witness_dev, 0xFF, 3 * sizeof(int32_t), s) == cudaSuccess ? CHORDAL_OK
                                                                                                   : CHORDAL_ECUDA;
     if (!order_dev || !pos_dev || !ws) return CHORDAL_EINVAL;
-    if (!use_seg(n) && m < 0) return CHORDAL_EINVAL;  // every rank sizes the same workspace
+    if (!use_seg(n, m) && m < 0) return CHORDAL_EINVAL;  // every rank sizes the same workspace
     const ShardWs L(n, DenseWs(n, m < 0 ? 0 : m).total);
     if (ws_bytes < L.total) return CHORDAL_EINVAL;
     const NcclApi &api = nccl_api();
@@ -860,12 +865,12 @@ int chordal_is_chordal_dense_nccl(const uint8_t *adj_dev, int64_t n, int64_t str
     int32_t *parent = reinterpret_cast<int32_t *>(w + L.parent);
     if (rank == root) {
         // the CTA engine leaves the parents to the PEO check (-2 = search them)
-        if (use_seg(n)) {
+        if (use_seg(n, m)) {
             rc = launch_fill_i32(parent, n, -2, s);
             if (rc) return rc;
         }
         rc = chordal_lexbfs_dense(adj_dev, n, stride, m, tie_rule, seed, order_dev, pos_dev,
-                                  use_seg(n) ? nullptr : parent, w + L.rest, ws_bytes - L.rest, stream);
+                                  use_seg(n, m) ? nullptr : parent, w + L.rest, ws_bytes - L.rest, stream);
         if (rc) return rc;
     }
     rc = shard_exchange(api, nccl_comm, root, n, order_dev, pos_dev, parent, key, s, [&](int64_t lo, int64_t hi) {
