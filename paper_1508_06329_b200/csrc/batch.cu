@@ -67,7 +67,10 @@ batch_chordal_kernel(const uint8_t *__restrict__ adj_all, long long batch, int n
     const uint16_t *ord = M.A, *pos = M.P, *par = M.par;
 
     // ---- LexBFS -------------------------------------------------------------------
-    warp_seg_lexbfs<CHORDAL_TIE_ASCENDING, false, false>(A32, sw, n, M);
+    if (n <= 512)
+        warp_seg_lexbfs<CHORDAL_TIE_ASCENDING, false, false, 16>(A32, sw, n, M);
+    else
+        warp_seg_lexbfs<CHORDAL_TIE_ASCENDING, false, false, 32>(A32, sw, n, M);
     const bool have_parent = true;
 
     // ---- write the order ---------------------------------------------------

@@ -74,7 +74,9 @@ __device__ __forceinline__ int excl_prefix6(int c, uint32_t lt, int &total) {
 }  // namespace wseg
 
 // rows: the graph's packed rows (global), sw: row pitch in 32-bit words.
-template <int MODE, bool LATENCY = false, bool SMEM_ROWS = false>
+// SPAN: lanes that can hold words (32; 16 for graphs of <= 512 vertices, whose
+// shuffle scans then need four rounds instead of five)
+template <int MODE, bool LATENCY = false, bool SMEM_ROWS = false, int SPAN = 32>
 __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n, const WarpSegMem &M) {
     using namespace wseg;
     const int l = threadIdx.x & 31;
@@ -213,12 +215,12 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
             const int ec = __popc(ext);
             int incl = ec;
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
+            for (int d = 1; d < SPAN; d <<= 1) {
                 const int o = __shfl_up_sync(CH_FULL, incl, d);
                 if (l >= d) incl += o;
             }
             xe = incl - ec;
-            ktot = __shfl_sync(CH_FULL, incl, 31);
+            ktot = __shfl_sync(CH_FULL, incl, SPAN - 1);
         }
 
         WSEG_T(2);
@@ -260,9 +262,11 @@ __device__ void warp_seg_lexbfs(const uint32_t *__restrict__ rows, int sw, int n
                     if (!below) LBr = 0;
                     if (!above) NBr = kBig;
                 } else {
+                    // (lanes >= SPAN hold no class start: il = kBig there, so
+                    // the suffix minima of lanes < SPAN are complete)
                     int ia = fc, ih = hb, il = lb;
 #pragma unroll
-                    for (int d = 1; d < 32; d <<= 1) {
+                    for (int d = 1; d < SPAN; d <<= 1) {
                         const int oa = __shfl_up_sync(CH_FULL, ia, d), oh = __shfl_up_sync(CH_FULL, ih, d);
                         const int ol = __shfl_down_sync(CH_FULL, il, d);
                         if (l >= d) { ia += oa; ih = max(ih, oh); }
