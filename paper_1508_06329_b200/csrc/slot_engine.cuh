@@ -41,6 +41,8 @@
 // touched per neighbour) and global ones.  I is the vertex/class index type,
 // S the slot index type.
 #pragma once
+#include <type_traits>
+
 #include "common.cuh"
 #include "philox.cuh"
 
@@ -182,7 +184,7 @@ __device__ __forceinline__ void for_each_chunk(const Src &src, int64_t b, int64_
 // consecutive slots fetched with one 16-byte load, so a warp skips 32*V dead
 // slots per memory round trip.  The slot array is padded by kSlotPad entries
 // and 16-byte aligned, so the over-read past e stays inside the allocation.
-constexpr int kSlotPad = 256;  // >= 32 * V for V = 8 (u16) and 4 (int32)
+constexpr int kSlotPad = 256;  // >= 32 * V for V = 8 (u16) and 4 (int32); 32 * 8 int32 for a 32-byte window
 template <typename I, typename S>
 __device__ __forceinline__ long long first_live(const SlotMem<I, S> &M, int c, long long h, long long e,
                                                int *vert = nullptr) {
@@ -311,6 +313,15 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
     constexpr bool kTrack = MODE == CHORDAL_TIE_ASCENDING || MODE == CHORDAL_TIE_DESCENDING ||
                             MODE == CHORDAL_TIE_SEEDED_PARTITION;
     constexpr int V = 16 / sizeof(I);
+#ifndef SLOT_WIN_BYTES
+#define SLOT_WIN_BYTES 16
+#endif
+    // the int32 form's next-pivot window: VW slots per lane (16 bytes; 8 bytes
+    // measured 1.466 -> 1.517 s on configuration 5, 32 bytes 1.578 s)
+    constexpr int VW = SLOT_WIN_BYTES / sizeof(I);
+    struct alignas(16) Win32 { uint4 a, b; };
+    using WinT = typename std::conditional<SLOT_WIN_BYTES == 32, Win32,
+                                           typename std::conditional<SLOT_WIN_BYTES == 16, uint4, uint2>::type>::type;
     constexpr bool kProbeWin = sizeof(I) == 2;  // next-pivot candidates: 32-slot probe (u16) or wide window
     int nx = -1;
     long long nxs = -1;
@@ -406,9 +417,9 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
             pA = (int)M.slot_v[xs + 1 + lane];
             pclA = (int)M.cls[pA];
         }
-        const long long cand_base = (xs + 1) & ~(long long)(V - 1);
-        uint4 cand_raw = make_uint4(0, 0, 0, 0);
-        if (kTrack && !kProbeWin) cand_raw = *reinterpret_cast<const uint4 *>(M.slot_v + cand_base + (long long)lane * V);
+        const long long cand_base = (xs + 1) & ~(long long)(VW - 1);
+        WinT cand_raw{};
+        if (kTrack && !kProbeWin) cand_raw = *reinterpret_cast<const WinT *>(M.slot_v + cand_base + (long long)lane * VW);
         __syncwarp();
         if (lane == 0) {
             if ((MODE != CHORDAL_TIE_SEEDED_ARB && MODE != CHORDAL_TIE_SEEDED_LABELS) || xs == (long long)M.c_head[c0])
@@ -515,41 +526,41 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
         // int32 state: the same candidates as a 32 * V-slot window (16-byte
         // loads), bounds lane-relative so each slot costs 32-bit compares only.
         long long wb = cand_base, wlo2 = xs + 1, whi2 = e0;
-        uint4 wraw = cand_raw;
+        WinT wraw = cand_raw;
         if (kTrack && !kProbeWin && alt) {
             wlo2 = (long long)M.c_head[hc];
             whi2 = (long long)M.c_end[hc];
-            wb = wlo2 & ~(long long)(V - 1);
-            wraw = *reinterpret_cast<const uint4 *>(M.slot_v + wb + (long long)lane * V);
+            wb = wlo2 & ~(long long)(VW - 1);
+            wraw = *reinterpret_cast<const WinT *>(M.slot_v + wb + (long long)lane * VW);
         }
-        int wcl[V];  // class of each window slot inside [wlo, whi), else -1
+        int wcl[VW];  // class of each window slot inside [wlo, whi), else -1
         if (kTrack && !kProbeWin) {
-            const long long l0 = wb + (long long)lane * V;
-            const int rlo = (int)(wlo2 - l0 < 0 ? 0 : (wlo2 - l0 > V ? V : wlo2 - l0));
-            const int rhi = (int)(whi2 - l0 < 0 ? 0 : (whi2 - l0 > V ? V : whi2 - l0));
+            const long long l0 = wb + (long long)lane * VW;
+            const int rlo = (int)(wlo2 - l0 < 0 ? 0 : (wlo2 - l0 > VW ? VW : wlo2 - l0));
+            const int rhi = (int)(whi2 - l0 < 0 ? 0 : (whi2 - l0 > VW ? VW : whi2 - l0));
             const I *cv = reinterpret_cast<const I *>(&wraw);
 #pragma unroll
-            for (int j = 0; j < V; ++j) wcl[j] = (j >= rlo && j < rhi) ? (int)M.cls[(int)cv[j]] : -1;
+            for (int j = 0; j < VW; ++j) wcl[j] = (j >= rlo && j < rhi) ? (int)M.cls[(int)cv[j]] : -1;
         }
         // the head class's first live slot in the window (its classes as read
         // before this step's moves: a head class that loses members to a split
         // gets a new segment and its first mover is the next pivot instead)
         auto window_wide = [&](int &gv_out, long long &gs_out) {
             const I *cv = reinterpret_cast<const I *>(&wraw);
-            int fj = V, fv = -1;
+            int fj = VW, fv = -1;
 #pragma unroll
-            for (int j = V - 1; j >= 0; --j)
+            for (int j = VW - 1; j >= 0; --j)
                 if (wcl[j] == hc) {
                     fj = j;
                     fv = (int)cv[j];
                 }
-            const uint32_t gm = __ballot_sync(CH_FULL, fj < V);
+            const uint32_t gm = __ballot_sync(CH_FULL, fj < VW);
             gv_out = -1;
             gs_out = -1;
             if (gm) {
                 const int src_l = __ffs(gm) - 1;
                 gv_out = __shfl_sync(CH_FULL, fv, src_l);
-                gs_out = wb + (long long)src_l * V + __shfl_sync(CH_FULL, fj, src_l);
+                gs_out = wb + (long long)src_l * VW + __shfl_sync(CH_FULL, fj, src_l);
             }
         };
         auto window_first = [&](int &gv_out, long long &gs_out) {
