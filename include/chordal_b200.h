@@ -97,10 +97,13 @@ size_t chordal_dense_workspace_bytes(int64_t n, int64_t m);
  * Engines: n <= 1024 (LOWEST_INDEX / descending) runs the one-warp engine; up to
  * n <= 32768 the persistent single-CTA touched-segment kernel (state in shared
  * memory, any density; m, when known, picks its dense or sparse form -- pass
- * m < 0 or 0 if unknown: the sparse form is then used); larger
- * graphs are converted to CSR on the device and run the O(deg)-per-step slot
- * kernel, which needs the edge count m (Graph.m): pass m < 0 to let the call
- * count the edges, which synchronises `stream` once. */
+ * m < 0 or 0 if unknown: the sparse form is then used) -- except sparse graphs
+ * with 1024 < n <= 8836 and a known m of average degree <= 20, which like all
+ * larger graphs are converted to CSR on the device and run the O(deg)-per-step
+ * slot kernel (for n <= 8836 with all its state in shared memory).  The CSR route
+ * needs the edge count m (Graph.m; the workspace is sized from it, and an
+ * understated m is rejected): for n > 32768 pass m < 0 to let the call count the
+ * edges, which synchronises `stream` once. */
 int chordal_lexbfs_dense(const uint8_t *adj_dev, int64_t n, int64_t stride, int64_t m, int32_t tie_rule,
                          uint64_t seed, int32_t *order_dev, int32_t *pos_dev, int32_t *parent_dev, void *ws,
                          size_t ws_bytes, void *stream);
