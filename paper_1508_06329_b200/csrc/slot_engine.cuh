@@ -604,6 +604,20 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
 #endif
                 if (ok && parent) parent[y] = (O)x;
                 const uint32_t vm = __ballot_sync(CH_FULL, ok);
+                if (vm == 0) {  // no unvisited neighbour: nothing moves, only the next pivot
+                    int guess;
+                    long long gslot;
+                    window_first(guess, gslot);
+                    nx = guess;
+                    nxs = gslot;
+                    if (nx >= 0 && nx != gv) {
+                        src.bounds_issue(nx, gb0, gb1);
+                        gv = nx;
+                    }
+                    __syncwarp();
+                    SLOT_T(2);
+                    continue;
+                }
                 const uint32_t peers = __match_any_sync(CH_FULL, ok ? c : -1) & vm;
                 const bool leader = ok && (peers & lt) == 0;
                 const int cnt = __popc(peers);
@@ -630,6 +644,17 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
                 // new classes: one per split group, segments laid out in lane order
                 const bool split = leader && cnt != live_c;
                 const uint32_t sm = __ballot_sync(CH_FULL, split);
+                if (sm == 0) {  // only whole classes move (they keep their place): the next pivot only
+                    nx = guess;
+                    nxs = gslot;
+                    if (nx >= 0 && nx != gv) {
+                        src.bounds_issue(nx, gb0, gb1);
+                        gv = nx;
+                    }
+                    __syncwarp();
+                    SLOT_T(2);
+                    continue;
+                }
                 const int d = __shfl_sync(CH_FULL, frl, __popc(sm & lt));
                 const int kk = split ? cnt : 0;
 #ifndef SLOT_SCAN_SHFL
@@ -637,11 +662,15 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
                 // give the exclusive prefix and the total (a shorter chain than a
                 // five-round shuffle scan)
                 int excl = 0, ktot = 0;
+                if ((sm & (sm - 1)) == 0) {  // at most one class splits (most steps): no scan
+                    ktot = sm ? __shfl_sync(CH_FULL, kk, __ffs(sm) - 1) : 0;
+                } else {
 #pragma unroll
-                for (int bit = 0; bit < 6; ++bit) {
-                    const uint32_t bm = __ballot_sync(CH_FULL, (kk >> bit) & 1);
-                    excl += __popc(bm & lt) << bit;
-                    ktot += __popc(bm) << bit;
+                    for (int bit = 0; bit < 6; ++bit) {
+                        const uint32_t bm = __ballot_sync(CH_FULL, (kk >> bit) & 1);
+                        excl += __popc(bm & lt) << bit;
+                        ktot += __popc(bm) << bit;
+                    }
                 }
                 const int incl = excl + kk;
 #else
