@@ -96,7 +96,8 @@ lexbfs_csr_kernel(const int64_t *__restrict__ indptr, const int32_t *__restrict_
     // recent head class / step, and a stale one costs a useless prefetch.
     const CsrWs L(n, m, 4, 4);
     volatile int *prog = reinterpret_cast<volatile int *>(ws + L.prog);
-    const SlotMem<int32_t, int32_t> M = carve<int32_t, int32_t>(ws, L);
+    SlotMem<int32_t, int32_t> M = carve<int32_t, int32_t>(ws, L);
+    slot_set_bounds(M, n, slot_detail::kSlotPad);
     if (threadIdx.x == 0) prog[0] = prog[1] = prog[2] = 0;
     __syncthreads();
     if (threadIdx.x >= 32) {
@@ -124,6 +125,7 @@ lexbfs_csr_smem_kernel(const int64_t *__restrict__ indptr, const int32_t *__rest
     M.c_cnt = sm16 + ((n + 7) & ~7);
     M.c_tgt = M.c_cnt + ((n + 2 + 7) & ~7);
     uint16_t *nbuf = M.c_tgt + ((n + 2 + 7) & ~7);
+    slot_set_bounds(M, n, slot_detail::kSlotPad);
     CsrStagedSource<uint16_t> src{indptr, indices, nbuf, kNbrBuf, 0};
     slot_lexbfs<uint16_t, int32_t, MODE, CsrStagedSource<uint16_t>, int32_t>(src, n, M, order, pos, parent, seed,
                                                                               cell);
@@ -192,6 +194,7 @@ lexbfs_csr_allsmem_kernel(const int64_t *__restrict__ indptr, const int32_t *__r
     M.touched = reinterpret_cast<uint16_t *>(smb + L.touched);
     M.scratch = reinterpret_cast<uint16_t *>(smb + L.scratch);
     M.cap = cap;
+    slot_set_bounds(M, n, slot_detail::kSlotPad);
     uint16_t *nbuf = reinterpret_cast<uint16_t *>(smb + L.nbuf);
     CsrStagedSource<uint16_t> src{indptr, indices, nbuf, kAllNbrBuf, 0};
     slot_lexbfs<uint16_t, uint16_t, MODE, CsrStagedSource<uint16_t>, int32_t>(src, n, M, order, pos, parent, seed,

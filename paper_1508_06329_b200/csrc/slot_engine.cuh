@@ -42,25 +42,84 @@
 // S the slot index type.
 #pragma once
 #include <type_traits>
+#ifdef CHORDAL_SLOT_BOUNDS
+#include <cstdio>
+#endif
 
 #include "common.cuh"
 #include "philox.cuh"
 
 namespace chordal {
 
+// Bounds-checked build (-DCHORDAL_SLOT_BOUNDS, tools/bounds_check.sh): every
+// subscript and pointer offset of the slot state is range-checked against its
+// array length and traps with the array's name.  It stands in for
+// compute-sanitizer memcheck, which this pool no longer runs; the product
+// build compiles the fields as plain pointers.
+#ifdef CHORDAL_SLOT_BOUNDS
+template <typename T>
+struct ChkPtr {
+    T *p = nullptr;
+    long long len = 0x7fffffffffffffffLL;  // unchecked until slot_set_bounds
+    const char *name = "?";
+    __host__ __device__ ChkPtr() {}
+    __host__ __device__ ChkPtr(T *q) : p(q) {}
+    __device__ __forceinline__ void check(long long i) const {
+        if (i < 0 || i >= len) {
+            printf("slot bounds: %s[%lld] outside [0, %lld) (block %d lane %d)\n", name, i, len, blockIdx.x,
+                   threadIdx.x);
+            __trap();
+        }
+    }
+    template <typename J>
+    __device__ __forceinline__ T &operator[](J i) const { check((long long)i); return p[i]; }
+    template <typename J>
+    __device__ __forceinline__ T *operator+(J i) const { check((long long)i); return p + i; }
+    __host__ __device__ operator T *() const { return p; }
+};
+template <typename T>
+using SlotPtr = ChkPtr<T>;
+#else
+template <typename T>
+using SlotPtr = T *;
+#endif
+
 template <typename I, typename S>
 struct SlotMem {
-    I *cls;                        // [n]   class of vertex, VISITED once consumed
-    I *slot_v;                     // [cap + kSlotPad] vertex stored in a slot (16-byte aligned)
-    S *c_head, *c_end;             // [n+2] segment bounds (slot indices < cap)
-    I *c_live, *c_prev, *c_next;   // [n+2]
-    I *c_tgt;                      // [n+2] split target of a touched class
-    I *c_cnt;                      // [n+2] movers (pass 1) / next free slot - step base (pass 2); 0 between steps
-    I *freel;                      // [n+2] free class ids
-    I *touched;                    // [n+2] classes touched in the current step
-    I *scratch;                    // [n]   compaction buffer
-    long long cap;                 // slot capacity (>= 2n + 32: compaction leaves <= n live slots)
+    SlotPtr<I> cls;                        // [n]   class of vertex, VISITED once consumed
+    SlotPtr<I> slot_v;                     // [cap + kSlotPad] vertex stored in a slot (16-byte aligned)
+    SlotPtr<S> c_head, c_end;              // [n+2] segment bounds (slot indices < cap)
+    SlotPtr<I> c_live, c_prev, c_next;     // [n+2]
+    SlotPtr<I> c_tgt;                      // [n+2] split target of a touched class
+    SlotPtr<I> c_cnt;                      // [n+2] movers (pass 1) / next free slot - step base (pass 2); 0 between steps
+    SlotPtr<I> freel;                      // [n+2] free class ids
+    SlotPtr<I> touched;                    // [n+2] classes touched in the current step
+    SlotPtr<I> scratch;                    // [n]   compaction buffer
+    long long cap;                          // slot capacity (>= 2n + 32: compaction leaves <= n live slots)
 };
+
+// Array lengths for the checked build (no-op otherwise); pad = slot_v's tail
+// beyond cap (slot_detail::kSlotPad).
+template <typename I, typename S>
+__device__ __forceinline__ void slot_set_bounds(SlotMem<I, S> &M, long long n, long long pad) {
+#ifdef CHORDAL_SLOT_BOUNDS
+    const long long nc = n + 2;
+    M.cls.len = n; M.cls.name = "cls";
+    M.slot_v.len = M.cap + pad; M.slot_v.name = "slot_v";
+    M.c_head.len = nc; M.c_head.name = "c_head";
+    M.c_end.len = nc; M.c_end.name = "c_end";
+    M.c_live.len = nc; M.c_live.name = "c_live";
+    M.c_prev.len = nc; M.c_prev.name = "c_prev";
+    M.c_next.len = nc; M.c_next.name = "c_next";
+    M.c_tgt.len = nc; M.c_tgt.name = "c_tgt";
+    M.c_cnt.len = nc; M.c_cnt.name = "c_cnt";
+    M.freel.len = nc; M.freel.name = "freel";
+    M.touched.len = nc; M.touched.name = "touched";
+    M.scratch.len = n; M.scratch.name = "scratch";
+#else
+    (void)M; (void)n; (void)pad;
+#endif
+}
 
 template <typename I>
 struct SlotConst {
