@@ -74,7 +74,9 @@ __device__ __forceinline__ SlotMem<I, S> carve(uint8_t *ws, const CsrWs &L) {
 // Look-ahead warp (slot_lookahead): the next CSR_LOOKAHEAD live vertices of the
 // class list, re-walked every CSR_LOOKAHEAD_EVERY steps (0: no look-ahead warp).
 // Config 5: 1.85 s without, 1.615 s with 64 / 8, 1.67 s with 128 / 8, 1.595 s
-// with 32 / 4 (tools/ab_variants.sh).
+// with 32 / 4 (tools/ab_variants.sh).  Re-measured after the fast-step early
+// exits (profiles/r02_ab_la_final.txt): 32 / 4 1.316 s, 32 / 2 1.317 s, 64 / 4
+// 1.321 s, 16 / 2 1.364 s -- 32 / 4 kept.
 #ifndef CSR_LOOKAHEAD
 #define CSR_LOOKAHEAD 32
 #endif
