@@ -970,7 +970,8 @@ __device__ void slot_lexbfs(const Src &src, int n, const SlotMem<I, S> &M, O *__
 // the search is mutating are harmless: a wrong guess costs one useless prefetch).
 // the nearest SLOT_LOOKAHEAD_L1 of the look-ahead vertices also get their list
 // entries read and their neighbours' class ids prefetched into L1 (config 5:
-// 1.626 -> 1.552 s with 16; 32: 1.553 s)
+// 1.626 -> 1.552 s with 16; 32: 1.553 s; re-measured on the current kernel,
+// profiles/r02_ab_l1_final.txt: 16 1.317 s, 8 1.324 s, 32 1.328 s)
 #ifndef SLOT_LOOKAHEAD_L1
 #define SLOT_LOOKAHEAD_L1 16
 #endif
